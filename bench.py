@@ -1,0 +1,266 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the B200 forward JTFS (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE configs[2], "instrument-note batch"): N = 2^16, J = 12, Q = 16,
+J_fr = 5, Q_fr = 1, T = 2^13, F = 4, 256 synthetic notes per GPU.
+A step is one forward JTFS of the whole batch (every stage KA..KE).  Multi-GPU:
+one process per GPU (torchrun), each rank its own 256 signals (weak scaling,
+no data-path collective); timing = max over ranks of the summed per-step CUDA
+event times; the L2 is flushed (256 MiB write) before every timed step.
+Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle
+(the reference arm of this tier) on the same workload, one signal per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(N=2 ** 16, J=12, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
+METRIC = "JTFS signals/s (N=2^16,J=12,Q=16) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "signals/s"
+WORKLOAD = "instrument-note batch (BASELINE configs[2]): N=2^16, J=12, Q=16, J_fr=5, Q_fr=1, T=2^13, F=4"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(sample_signals: int = 1):
+    """The fp64 oracle as it stands, on the host cores, on c3 notes."""
+    import numpy as np
+    from oracle import jtfs_oracle as O
+    from paper_2204_08269_b200 import signals
+    cores = os.cpu_count() or 1
+    O.set_workers(cores)
+    prm = O.Params(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], T=CFG["T"], F=CFG["F"])
+    s = O.schedule(prm)
+    X = signals.notes(sample_signals, seed0=1000)
+    t0 = time.perf_counter()
+    for b in range(sample_signals):
+        O.jtfs_forward(X[b].astype(np.float64), prm, s=s)
+    dt = time.perf_counter() - t0
+    return {"value": sample_signals / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{sample_signals} c3 note signal(s), full forward JTFS in fp64, scipy.fft workers={cores}",
+            "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import numpy as np
+    from oracle import jtfs_oracle as O
+    from paper_2204_08269_b200 import signals
+    cores = os.cpu_count() or 1
+    O.set_workers(cores)
+    prm = O.Params(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], T=CFG["T"], F=CFG["F"])
+    s = O.schedule(prm)
+    X = signals.notes(args.warmup + args.steps, seed0=1000)
+    for w in range(args.warmup):
+        O.jtfs_forward(X[w].astype(np.float64), prm, s=s)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        O.jtfs_forward(X[args.warmup + k].astype(np.float64), prm, s=s)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch_per_step": 1, **CFG},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"1 c3 note signal per step, fp64 oracle, scipy.fft workers={cores}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=256, help="signals per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2204_08269_b200 import build as _build
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2204_08269_b200 import jtfs, signals
+
+    B = args.batch
+    plan = jtfs.Plan(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], Q_fr=CFG["Q_fr"], T=CFG["T"],
+                     F=CFG["F"], device=local)
+    fps = plan.floats_per_signal
+    X = signals.notes(B, seed0=1000 + rank * B)
+    x = torch.from_numpy(X).to(dev)
+    out = torch.empty(B, fps, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.forward(x, out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    plan.profile_read(reset=True)
+    plan.profile_enable(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)                      # L2 flush between timed steps (not timed)
+        ev[k][0].record(stream)
+        plan.forward(x, out)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    plan.profile_enable(False)
+    prof = plan.profile_read(reset=True)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    value = B * world * args.steps / (total_ms / 1e3)
+    launches = int(sum(v[1] for v in prof.values()))
+
+    # ---- end to end through the C ABI with host buffers (pinned), copies timed ----
+    xh = torch.from_numpy(X).pin_memory()
+    oh = torch.empty(B, fps, dtype=torch.float32).pin_memory()
+    plan.forward_host(xh, oh, x, out)
+    k_e2e = max(1, min(args.steps, 3))
+    t_e2e = torch.zeros(1, dtype=torch.float64, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(k_e2e):
+        plan.forward_host(xh, oh, x, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e[0] = e0.elapsed_time(e1)
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = B * world * k_e2e / (float(t_e2e.item()) / 1e3)
+
+    # ---- roofline of the dominant kernel (KD, ALU-bound) ----
+    cost = plan.cost()
+    peaks, src = _peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12            # TFLOP/s fp32 FMA, DESIGN.md §5
+    kd_ms = prof["KD_joint"][0]
+    kd_flops = cost["KD_joint"][0] * B * args.steps
+    kd_tflops = kd_flops / (kd_ms / 1e3) / 1e12 if kd_ms > 0 else None
+    stage_share = {k: round(v[0] / max(sum(u[0] for u in prof.values()), 1e-9), 4) for k, v in prof.items()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+                       "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                       "l2": "flushed before every timed step (256 MiB write)", **CFG},
+            "roofline": {"bound": "alu", "kernel": "KD (k_kd_simt: lambda contraction + |.| + phi_T pooling)",
+                         "achieved": kd_tflops, "peak": alu_peak, "unit": "TFLOP/s",
+                         "frac": (kd_tflops / alu_peak) if kd_tflops else None, "traffic": None,
+                         "peak_source": f"148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz ({src} sm_max_mhz)",
+                         "algorithmic_flops_per_signal": cost["KD_joint"][0]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
+                    "d2h_bytes_per_step": int(oh.numel() * 4)},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "stages_ms": {k: round(v[0], 3) for k, v in prof.items()},
+            "stage_share": stage_share,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,213 @@
+/*
+ * jtfs.h -- C ABI of the B200-native forward Joint Time-Frequency Scattering.
+ *
+ * Operator: PAPER.md (arXiv 2204.08269, DAFx-22), Sec. 2:
+ *   scalogram  X(t,lambda) = |x * psi_lambda|(t)
+ *   Eq. (1)    psi_alpha(t) = 2^a psi(2^a t),
+ *              psi_{beta,theta}(lambda) = 2^b psi(theta 2^b lambda)
+ *   Eq. (2)    Psi_{alpha,beta,theta} = psi_alpha(t) psi_{beta,theta}(lambda)
+ *   Eq. (3)    S2 = | X *_{t,lambda} Psi | *_{t,lambda} Phi_{T,F}
+ *   Eq. (4)    S2 = | X *_{t,lambda} Psi | *_t Phi_T
+ *   first order S1 = U1 * phi_T (no Phi_F), out_3D layout,
+ * with the readings of DESIGN.md §3 for everything the paper
+ * leaves unstated (filter constants, critical subsampling, padding,
+ * admissibility, lambda-axis boundary, spin orientation, path order).
+ *
+ * Conventions for every function:
+ *   - extern "C", returns jtfs_status (0 = JTFS_OK); no C++ exception crosses the ABI;
+ *   - on error a thread-local message is available from jtfs_last_error();
+ *   - "device" pointers are CUDA global-memory pointers on the plan's device,
+ *     "host" pointers are ordinary CPU memory;
+ *   - the caller owns every buffer it passes; the plan owns its device tables
+ *     and frees them in jtfs_plan_destroy.
+ */
+#ifndef JTFS_H_
+#define JTFS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define JTFS_API __attribute__((visibility("default")))
+#else
+#define JTFS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  JTFS_OK = 0,
+  JTFS_ERR_INVALID_ARG = 1,  /* bad parameter / null or misaligned pointer / bad size */
+  JTFS_ERR_UNSUPPORTED = 2,  /* valid but not supported (e.g. forward on a host-only plan) */
+  JTFS_ERR_OOM = 3,          /* device or host allocation failed */
+  JTFS_ERR_CUDA = 4,         /* a CUDA runtime call or kernel launch failed */
+  JTFS_ERR_WORKSPACE = 5,    /* workspace smaller than jtfs_workspace_size() */
+  JTFS_ERR_NONFINITE = 6     /* JTFS_CHECK_FINITE set and the input holds NaN/Inf */
+} jtfs_status;
+
+/* flags */
+#define JTFS_CHECK_FINITE 1u   /* forward scans x for NaN/Inf first (one device sync) */
+
+/* pad modes (reading R6) */
+#define JTFS_PAD_REFLECT 0     /* numpy 'reflect' to N_pad = 2N, centred */
+#define JTFS_PAD_PERIODIC 1    /* N_pad = N, circular (exact-invariant tests) */
+
+typedef struct jtfs_plan_s* jtfs_plan_t;  /* opaque; immutable after creation */
+
+/* Operator parameters (Sec. 4.2, Sec. 3.3).
+ *   N      signal length, power of two
+ *   J      octaves of the temporal banks (2^J <= N)
+ *   Q      first-order wavelets per octave (>= 1)
+ *   Q2     second-order wavelets per octave (paper: 1)
+ *   T      temporal lowpass support, power of two, T <= N
+ *   J_fr   octaves of the frequential bank (>= 1)
+ *   Q_fr   frequential wavelets per octave (paper: 1)
+ *   F      frequential lowpass support, power of two (0 -> 2^J_fr)
+ *   average_fr  1: Eq. (3) (Phi_{T,F}); 0: Eq. (4) (Phi_T only)
+ *   pad_mode    JTFS_PAD_REFLECT or JTFS_PAD_PERIODIC
+ *   device      CUDA device ordinal; -1 = host-only plan (queries only, no forward)
+ *   flags       JTFS_CHECK_FINITE
+ */
+typedef struct {
+  int32_t N, J, Q, Q2, T, J_fr, Q_fr, F;
+  int32_t average_fr, pad_mode, device;
+  uint32_t flags;
+} jtfs_params;
+
+/* Packed out_3D record of one signal (DESIGN.md §3 R-O11/O12), fp32:
+ *   [ S0 : n_frames ][ S1 : n1 x n_frames ][ S2 : n_paths x lambda_out x n_frames ]
+ * all row-major; S1 rows in descending centre frequency; frames are the
+ * un-padded time frames m in [frame0, frame0 + n_frames) at rate T. */
+typedef struct {
+  int32_t n1;            /* first-order filters (lambda rows) */
+  int32_t n_frames;      /* time frames per coefficient = ceil(N / T) */
+  int32_t frame0;        /* first retained frame index on the padded grid */
+  int32_t lambda_out;    /* S2 log-frequency rows: ceil(n1/F) (Eq. 3) or n1 (Eq. 4) */
+  int32_t n_paths;       /* S2 paths lambda2 = (alpha, beta, theta) incl. phi-only paths */
+  int32_t n_alpha;       /* active second-order temporal wavelets */
+  int32_t n_beta;        /* frequential wavelets per spin */
+  int32_t N_pad;         /* padded length */
+  int32_t N_fr;          /* frequential (lambda) grid length */
+  int32_t reserved;
+  int64_t off_s0, off_s1, off_s2;  /* float offsets inside one record */
+  int64_t floats_per_signal;
+} jtfs_layout_t;
+
+/* Path kinds, in output order (DESIGN.md R-O11). */
+#define JTFS_PATH_SPIN 0        /* psi_alpha (x) psi_{beta,theta} */
+#define JTFS_PATH_PSI_T_PHI_F 1 /* psi_alpha (x) phi_F */
+#define JTFS_PATH_PHI_T_PSI_F 2 /* phi_T (x) psi_beta (one spin, real input) */
+#define JTFS_PATH_PHI_T_PHI_F 3 /* phi_T (x) phi_F (no modulus) */
+
+typedef struct {
+  int32_t kind;     /* JTFS_PATH_* */
+  int32_t theta;    /* -1 / +1 for spinned paths, 0 otherwise */
+  int32_t alpha;    /* index into the second-order bank G(J,Q2) (0 = highest xi), -1 if none */
+  int32_t beta;     /* index into the frequential bank G(J_fr,Q_fr), -1 if none */
+  double xi_alpha;  /* centre frequency of psi_alpha, cycles/sample (0 if none) */
+  double xi_beta;   /* centre frequency of psi_beta, cycles/bin (0 if none) */
+} jtfs_path_t;
+
+/* North-star form (north_star's jtfs_plan(N,J,Q,J_fr,Q_fr,T,F,...)): equivalent
+ * to jtfs_plan_create with Q2 = 1, average_fr = 1 (Eq. (3)), reflect
+ * padding, device = current CUDA device, flags as given. */
+JTFS_API jtfs_status jtfs_plan(int N, int J, int Q, int J_fr, int Q_fr, int T, int F, int flags,
+                      jtfs_plan_t* out);
+
+/* Build a plan: validates every constraint of DESIGN.md §3 (pow2 N, T, F;
+ * 2^J <= N; T <= N; n1 >= 4; F <= N_fr), generates the filter banks in fp64,
+ * derives the schedule, and (device >= 0) uploads fp32 tables to the device.
+ * *out receives the handle (NULL on error). */
+JTFS_API jtfs_status jtfs_plan_create(const jtfs_params* params, jtfs_plan_t* out);
+
+/* Frees the plan's device tables.  NULL-safe.  Must not race a forward on it. */
+JTFS_API jtfs_status jtfs_plan_destroy(jtfs_plan_t plan);
+
+/* Output layout of one signal (host query, valid for host-only plans). */
+JTFS_API jtfs_status jtfs_layout(jtfs_plan_t plan, jtfs_layout_t* out);
+
+/* Path metadata in output order; writes min(cap, n_paths) entries to out (host). */
+JTFS_API jtfs_status jtfs_paths(jtfs_plan_t plan, jtfs_path_t* out, int32_t cap);
+
+/* First-order centre frequencies xi_lambda (cycles/sample), descending; host. */
+JTFS_API jtfs_status jtfs_lambda_xi(jtfs_plan_t plan, double* out, int32_t cap);
+
+/* Device workspace bytes jtfs_forward needs for a batch of `batch` signals. */
+JTFS_API jtfs_status jtfs_workspace_size(jtfs_plan_t plan, int64_t batch, size_t* bytes);
+
+/* Forward JTFS of a batch.
+ *   x      device, fp32 [B][N] row-major, 16-byte aligned
+ *   B      number of signals (>= 0; B = 0 is a no-op)
+ *   out    device, fp32 [B][floats_per_signal], 16-byte aligned
+ *   ws     device workspace of ws_bytes >= jtfs_workspace_size(plan, B), 256-byte aligned
+ *   stream cudaStream_t (NULL = legacy default stream)
+ * Asynchronous: enqueues kernels on `stream` and returns; asynchronous faults
+ * surface at the caller's next synchronisation.  Output bytes are a
+ * deterministic function of (plan, x) independent of B and of the GPU count. */
+JTFS_API jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* out,
+                         void* ws, size_t ws_bytes, void* stream);
+
+/* End-to-end variant with HOST buffers: copies x_host (fp32 [B][N]) to the
+ * device, runs jtfs_forward, copies the result to out_host (fp32
+ * [B][floats_per_signal]) and synchronises `stream`.  x_dev / out_dev are
+ * caller-owned device staging buffers of the same shapes.  Host buffers should
+ * be pinned for full copy bandwidth. */
+JTFS_API jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B,
+                              float* out_host, float* x_dev, float* out_dev,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* Debug taps for kernel-level tests (device outputs, synchronous).
+ *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
+ *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)
+ *   tap 2: Y2      -> out complex (float2) [B][sum_alpha K_alpha L_alpha] (alpha-major, lambda, time)
+ *   tap 3: Yphi    -> out fp32 [B][n1][N_pad/T]
+ * `out_floats` is the capacity of out in floats. */
+JTFS_API jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* x, int64_t B,
+                           float* out, int64_t out_floats, void* ws, size_t ws_bytes,
+                           void* stream);
+
+/* Size in floats of a debug tap for B signals. */
+JTFS_API jtfs_status jtfs_debug_tap_size(jtfs_plan_t plan, int32_t tap, int64_t B, int64_t* floats);
+
+/* Host copy of a sampled filter spectrum as the plan generated it (fp64), for
+ * cross-checking the plan generator against the oracle's independent one.
+ *   bank 1: psi_lambda, 2: psi_alpha, 3: psi_beta (theta=-1), 4: phi_T, 5: phi_F
+ *   idx   filter index in its bank (ignored for lowpass)
+ *   L, n_grid  grid length and physical spacing 1/n_grid (R8)
+ * out: L doubles. */
+JTFS_API jtfs_status jtfs_debug_filter(jtfs_plan_t plan, int32_t bank, int32_t idx, int32_t L,
+                              int32_t n_grid, double* out);
+
+/* Algorithmic cost of one signal per stage (same stage numbering as profiling),
+ * for roofline reporting; cost model of DESIGN.md §5 (SURVEY App. B conventions:
+ * complex FFT 5 L log2 L, real FFT 2.5 L log2 L, complex modulus 5, pooling
+ * 2 per frame per element).  flops[s]: the cheapest exact formulation of the
+ * stage's arithmetic (for KD the FFT-along-lambda form); bytes[s]: the stage's
+ * unavoidable HBM traffic (input + output of the whole path are charged to
+ * KA / KS / KE).  Host query. */
+JTFS_API jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap);
+
+/* Stage profiling (tracing).  When enabled, jtfs_forward records a CUDA event
+ * pair on the caller's stream around each stage of every micro-batch:
+ *   0 KA pad+DFT, 1 KB first order (U1, U1hat), 2 KS phi_T averaging (S0, S1, Y_phi),
+ *   3 KC second order in time (Y2), 4 KD frequential contraction + modulus +
+ *   phi_T pooling, 5 KE phi_F pooling + phi paths + packing.
+ * jtfs_profile_read synchronises on the recorded events, writes the summed
+ * milliseconds per stage into stage_ms[cap] and the number of kernel launches
+ * per stage (counted whether or not profiling is enabled) into
+ * stage_launches[cap], and (reset != 0) clears both.  Profiling state is the
+ * only mutable part of a plan: do not profile one plan from two threads. */
+#define JTFS_N_STAGES 6
+JTFS_API jtfs_status jtfs_profile_enable(jtfs_plan_t plan, int32_t enable);
+JTFS_API jtfs_status jtfs_profile_read(jtfs_plan_t plan, double* stage_ms, int64_t* stage_launches,
+                                       int32_t cap, int32_t reset);
+
+JTFS_API const char* jtfs_status_string(jtfs_status s);
+JTFS_API const char* jtfs_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JTFS_H_ */

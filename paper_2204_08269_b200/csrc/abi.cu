@@ -1,0 +1,507 @@
+// C ABI of libjtfs.so (declared in include/jtfs.h): plan lifecycle, queries,
+// workspace, forward orchestration over micro-batches, debug taps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "jtfs_internal.h"
+#include "kernels.h"
+
+struct jtfs_plan_s {
+  jtfs::Plan P;
+};
+
+namespace {
+thread_local std::string g_err;
+
+jtfs_status fail(jtfs_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+jtfs_status cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return JTFS_ERR_CUDA;
+}
+
+bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+template <class T>
+cudaError_t upload(jtfs::Plan& P, T** dst, const void* src, size_t bytes) {
+  *dst = nullptr;
+  if (bytes == 0) bytes = 16;
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return e;
+  P.allocations.push_back(d);
+  if (src) e = cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice);
+  *dst = (T*)d;
+  return e;
+}
+
+void free_device(jtfs::Plan& P) {
+  if (P.device >= 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(P.device);
+    for (void* p : P.allocations) cudaFree(p);
+    cudaSetDevice(cur);
+  }
+  P.allocations.clear();
+}
+
+// record the device tables of a host plan
+jtfs_status upload_plan(jtfs::Plan& P) {
+  using namespace jtfs;
+  cudaError_t e;
+#define UP(dst, src, bytes)                                    \
+  do {                                                         \
+    e = upload(P, &(dst), (src), (bytes));                     \
+    if (e != cudaSuccess) return cuda_fail(e, "plan upload");  \
+  } while (0)
+  UP(P.d_bandvals, P.bandvals.data(), P.bandvals.size() * 4);
+  UP(P.d_A, P.A.data(), P.A.size() * 4);
+  UP(P.d_g, P.g.data(), P.g.size() * 4);
+  UP(P.d_W, P.W.data(), P.W.size() * 4);
+  UP(P.d_hphi, P.hphi.data(), P.hphi.size() * 4);
+  UP(P.d_twiddle, P.twiddle.data(), P.twiddle.size() * 4);
+  for (auto& g : P.u1_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
+  for (auto& g : P.y2_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
+  UP(P.d_u1_off, P.u1_off.data(), P.u1_off.size() * 8);
+  {
+    std::vector<int32_t> k1(P.k1.begin(), P.k1.end());
+    UP(P.d_k1, k1.data(), k1.size() * 4);
+  }
+  UP(P.d_band_L1, P.band_phiT_L1.data(), P.band_phiT_L1.size() * sizeof(Band));
+  {
+    std::vector<DevAlpha> da;
+    for (const auto& d : P.kd) da.push_back(DevAlpha{d.nchunks, 0, d.part_off});
+    UP(P.d_alphas, da.data(), da.size() * sizeof(DevAlpha));
+  }
+  {
+    std::vector<DevFilter> df;
+    std::vector<int32_t> rp;
+    for (const auto& f : P.fr) {
+      df.push_back(DevFilter{f.k, f.nrows, f.row0, (int32_t)rp.size(), f.w_off});
+      rp.insert(rp.end(), f.rprime.begin(), f.rprime.end());
+    }
+    UP(P.d_fr, df.data(), df.size() * sizeof(DevFilter));
+    UP(P.d_rprime, rp.data(), rp.size() * 4);
+  }
+  {
+    std::vector<DevPath> dp;
+    for (size_t i = 0; i < P.paths.size(); ++i) {
+      const auto& p = P.paths[i];
+      int slot = -1;
+      for (size_t a = 0; a < P.kd.size(); ++a)
+        if (P.kd[a].alpha == p.alpha) slot = (int)a;
+      dp.push_back(DevPath{p.kind, P.path_filter[i], slot, p.beta});
+    }
+    UP(P.d_paths, dp.data(), dp.size() * sizeof(DevPath));
+  }
+#undef UP
+  e = jtfs::ke_set_smem(P);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_ke)");
+  return JTFS_OK;
+}
+
+struct WsPtrs {
+  float2 *xhat, *tmp, *u1hat, *y2;
+  float *u1, *yphi, *part;
+  int* flag;
+};
+
+WsPtrs carve(const jtfs::Plan& P, void* ws, int64_t mb) {
+  const jtfs::WsLayout L = jtfs::ws_layout(P, mb);
+  char* c = (char*)ws;
+  WsPtrs w{};
+  w.xhat = (float2*)c; c += L.xhat;
+  w.tmp = (float2*)c; c += L.tmp;
+  w.u1 = (float*)c; c += L.u1;
+  w.u1hat = (float2*)c; c += L.u1hat;
+  w.yphi = (float*)c; c += L.yphi;
+  w.y2 = (float2*)c; c += L.y2;
+  w.part = (float*)c; c += L.part;
+  w.flag = (int*)c;
+  return w;
+}
+
+void layout_of(const jtfs::Plan& P, jtfs_layout_t* o) {
+  o->n1 = P.n1;
+  o->n_frames = P.n_frames;
+  o->frame0 = P.frame0;
+  o->lambda_out = P.lam_out;
+  o->n_paths = (int32_t)P.paths.size();
+  o->n_alpha = (int32_t)P.kd.size();
+  o->n_beta = (int32_t)P.bf.xi.size();
+  o->N_pad = P.N_pad;
+  o->N_fr = P.N_fr;
+  o->reserved = 0;
+  o->off_s0 = 0;
+  o->off_s1 = P.n_frames;
+  o->off_s2 = o->off_s1 + (int64_t)P.n1 * P.n_frames;
+  o->floats_per_signal = o->off_s2 + (int64_t)P.paths.size() * P.lam_out * P.n_frames;
+}
+
+// stage tracing (jtfs_profile_enable)
+struct StageScope {
+  jtfs::Plan& P;
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t e1 = nullptr;
+  StageScope(jtfs::Plan& P_, int s, cudaStream_t st_) : P(P_), stage(s), st(st_) {
+    if (P.prof) {
+      cudaEvent_t e0;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+      P.prof_events[stage].push_back({(void*)e0, (void*)e1});
+    }
+  }
+  void done(int nlaunch) {
+    P.launches[stage] += nlaunch;
+    if (P.prof) cudaEventRecord(e1, st);
+  }
+};
+
+// enqueue every stage for one micro-batch of nb signals
+void run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, const WsPtrs& w, bool keep_u1,
+                    int upto_stage, cudaStream_t st) {
+  using namespace jtfs;
+  jtfs_layout_t lay;
+  layout_of(P, &lay);
+  { StageScope s(P, 0, st); s.done(launch_pad_fft(P, x, nb, w.xhat, w.tmp, st)); }
+  if (upto_stage == 0) return;
+  { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st)); }
+  {
+    StageScope s(P, 2, st);
+    s.done(launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, out, lay.floats_per_signal, lay.off_s0, lay.off_s1,
+                            P.d_u1_off, P.d_k1, P.d_band_L1, st));
+  }
+  if (upto_stage == 1) return;
+  { StageScope s(P, 3, st); s.done(launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
+  if (upto_stage == 2) return;
+  { StageScope s(P, 4, st); s.done(launch_kd(P, w.y2, nb, w.part, st)); }
+  KEParams kp{};
+  kp.paths = (const DevPath*)P.d_paths;
+  kp.filters = (const DevFilter*)P.d_fr;
+  kp.alphas = (const DevAlpha*)P.d_alphas;
+  kp.rprime = P.d_rprime;
+  kp.W = P.d_W;
+  const int nbeta = (int)P.bf.xi.size();
+  kp.hpsi = (const float2*)P.d_hphi;
+  kp.hphiF = P.d_hphi + (size_t)2 * nbeta * P.N_fr;
+  kp.gT = kp.hphiF + P.N_fr;
+  kp.part = w.part;
+  kp.yphi = w.yphi;
+  kp.out = out;
+  kp.fps = lay.floats_per_signal;
+  kp.off_s2 = lay.off_s2;
+  kp.part_stride = P.part_total;
+  kp.n1 = P.n1;
+  kp.NPT = P.NPT;
+  kp.N_fr = P.N_fr;
+  kp.lam_out = P.lam_out;
+  kp.n_frames = P.n_frames;
+  kp.frame0 = P.frame0;
+  kp.Mpad = P.Mpad;
+  kp.k_phiphi = P.prm.average_fr ? P.log2F : 0;
+  { StageScope s(P, 5, st); s.done(launch_ke(P, kp, nb, st)); }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+const char* jtfs_status_string(jtfs_status s) {
+  switch (s) {
+    case JTFS_OK: return "ok";
+    case JTFS_ERR_INVALID_ARG: return "invalid argument";
+    case JTFS_ERR_UNSUPPORTED: return "unsupported";
+    case JTFS_ERR_OOM: return "out of memory";
+    case JTFS_ERR_CUDA: return "CUDA error";
+    case JTFS_ERR_WORKSPACE: return "workspace too small";
+    case JTFS_ERR_NONFINITE: return "non-finite input";
+  }
+  return "unknown status";
+}
+
+const char* jtfs_last_error(void) { return g_err.c_str(); }
+
+jtfs_status jtfs_plan_create(const jtfs_params* params, jtfs_plan_t* out) {
+  if (!out) return fail(JTFS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!params) return fail(JTFS_ERR_INVALID_ARG, "params is NULL");
+  jtfs_plan_s* h = new (std::nothrow) jtfs_plan_s();
+  if (!h) return fail(JTFS_ERR_OOM, "host allocation failed");
+  std::string err;
+  try {
+    err = jtfs::build_plan(*params, h->P);
+  } catch (const std::bad_alloc&) {
+    delete h;
+    return fail(JTFS_ERR_OOM, "host allocation failed while building the plan");
+  } catch (const std::exception& e) {
+    err = e.what();
+  }
+  if (!err.empty()) {
+    delete h;
+    return fail(JTFS_ERR_INVALID_ARG, err);
+  }
+  jtfs::Plan& P = h->P;
+  // micro-batch: keep one micro-batch's workspace around <= 4 GiB
+  const size_t per = jtfs::ws_layout(P, 1).total;
+  P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ((size_t)4 << 30) / std::max<size_t>(per, 1)));
+  if (params->device >= 0) {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || params->device >= ndev) {
+      delete h;
+      return e != cudaSuccess ? cuda_fail(e, "cudaGetDeviceCount")
+                              : fail(JTFS_ERR_INVALID_ARG, "device ordinal out of range");
+    }
+    P.device = params->device;
+    DeviceGuard g(P.device);
+    jtfs_status s = upload_plan(P);
+    if (s != JTFS_OK) {
+      free_device(P);
+      delete h;
+      return s;
+    }
+  }
+  *out = h;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_plan(int N, int J, int Q, int J_fr, int Q_fr, int T, int F, int flags, jtfs_plan_t* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    if (out) *out = nullptr;
+    return cuda_fail(e, "cudaGetDevice");
+  }
+  jtfs_params p{};
+  p.N = N; p.J = J; p.Q = Q; p.Q2 = 1; p.T = T; p.J_fr = J_fr; p.Q_fr = Q_fr; p.F = F;
+  p.average_fr = 1; p.pad_mode = JTFS_PAD_REFLECT; p.device = dev; p.flags = (uint32_t)flags;
+  return jtfs_plan_create(&p, out);
+}
+
+jtfs_status jtfs_plan_destroy(jtfs_plan_t plan) {
+  if (!plan) return JTFS_OK;
+  free_device(plan->P);
+  delete plan;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_layout(jtfs_plan_t plan, jtfs_layout_t* out) {
+  if (!plan || !out) return fail(JTFS_ERR_INVALID_ARG, "NULL argument");
+  layout_of(plan->P, out);
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_paths(jtfs_plan_t plan, jtfs_path_t* out, int32_t cap) {
+  if (!plan || (!out && cap > 0) || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const int n = std::min<int>(cap, (int)plan->P.paths.size());
+  for (int i = 0; i < n; ++i) out[i] = plan->P.paths[i];
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_lambda_xi(jtfs_plan_t plan, double* out, int32_t cap) {
+  if (!plan || (!out && cap > 0) || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const int n = std::min<int>(cap, plan->P.n1);
+  for (int i = 0; i < n; ++i) out[i] = plan->P.b1.xi[i];
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_workspace_size(jtfs_plan_t plan, int64_t batch, size_t* bytes) {
+  if (!plan || !bytes || batch < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const int64_t mb = std::max<int64_t>(1, std::min<int64_t>(batch, plan->P.mb));
+  *bytes = jtfs::ws_layout(plan->P, mb).total;
+  return JTFS_OK;
+}
+
+static jtfs_status check_forward_args(jtfs_plan_t plan, const void* x, int64_t B, const void* out, void* ws,
+                                      size_t ws_bytes) {
+  if (!plan) return fail(JTFS_ERR_INVALID_ARG, "plan is NULL");
+  if (plan->P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan (device = -1) cannot run forward");
+  if (B < 0) return fail(JTFS_ERR_INVALID_ARG, "B < 0");
+  if (B == 0) return JTFS_OK;
+  if (!x || !out || !ws) return fail(JTFS_ERR_INVALID_ARG, "NULL buffer");
+  if (!aligned(x, 16) || !aligned(out, 16)) return fail(JTFS_ERR_INVALID_ARG, "x / out must be 16-byte aligned");
+  if (!aligned(ws, 256)) return fail(JTFS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  size_t need = 0;
+  jtfs_workspace_size(plan, B, &need);
+  if (ws_bytes < need)
+    return fail(JTFS_ERR_WORKSPACE, "workspace " + std::to_string(ws_bytes) + " < required " + std::to_string(need));
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* out, void* ws, size_t ws_bytes,
+                         void* stream) {
+  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK || B == 0) return s;
+  jtfs::Plan& P = plan->P;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mb = std::min<int64_t>(B, P.mb);
+  WsPtrs w = carve(P, ws, mb);
+  if (P.prm.flags & JTFS_CHECK_FINITE) {
+    cudaMemsetAsync(w.flag, 0, sizeof(int), st);
+    jtfs::launch_check_finite(x, B * (int64_t)P.N, w.flag, st);
+    int h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "finite check");
+    if (h) return fail(JTFS_ERR_NONFINITE, "input holds NaN or Inf");
+  }
+  jtfs_layout_t lay;
+  layout_of(P, &lay);
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    const int nb = (int)std::min<int64_t>(mb, B - b0);
+    run_microbatch(P, x + b0 * P.N, nb, out + b0 * lay.floats_per_signal, w, false, 99, st);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B, float* out_host, float* x_dev,
+                              float* out_dev, void* ws, size_t ws_bytes, void* stream) {
+  jtfs_status s = check_forward_args(plan, x_dev, B, out_dev, ws, ws_bytes);
+  if (s != JTFS_OK || B == 0) return s;
+  if (!x_host || !out_host) return fail(JTFS_ERR_INVALID_ARG, "NULL host buffer");
+  const jtfs::Plan& P = plan->P;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  jtfs_layout_t lay;
+  layout_of(P, &lay);
+  cudaError_t e = cudaMemcpyAsync(x_dev, x_host, (size_t)B * P.N * 4, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  s = jtfs_forward(plan, x_dev, B, out_dev, ws, ws_bytes, stream);
+  if (s != JTFS_OK) return s;
+  e = cudaMemcpyAsync(out_host, out_dev, (size_t)B * lay.floats_per_signal * 4, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_debug_tap_size(jtfs_plan_t plan, int32_t tap, int64_t B, int64_t* floats) {
+  if (!plan || !floats || B < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const jtfs::Plan& P = plan->P;
+  switch (tap) {
+    case 0: *floats = B * (int64_t)P.N_pad * 2; break;
+    case 1: *floats = B * P.u1_total; break;
+    case 2: *floats = B * P.y2_total * 2; break;
+    case 3: *floats = B * (int64_t)P.n1 * P.NPT; break;
+    default: return fail(JTFS_ERR_INVALID_ARG, "unknown tap");
+  }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* x, int64_t B, float* out,
+                           int64_t out_floats, void* ws, size_t ws_bytes, void* stream) {
+  int64_t need = 0;
+  jtfs_status s = jtfs_debug_tap_size(plan, tap, B, &need);
+  if (s != JTFS_OK) return s;
+  if (!out || out_floats < need) return fail(JTFS_ERR_INVALID_ARG, "tap output too small");
+  if (B > plan->P.mb) return fail(JTFS_ERR_INVALID_ARG, "debug taps take at most one micro-batch");
+  jtfs_layout_t lay;
+  layout_of(plan->P, &lay);
+  s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK || B == 0) return s;
+  jtfs::Plan& P = plan->P;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  WsPtrs w = carve(P, ws, B);
+  float* scratch = nullptr;
+  cudaError_t e = cudaMalloc(&scratch, (size_t)B * lay.floats_per_signal * 4);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc scratch");
+  const int stage = tap == 0 ? 0 : (tap == 1 || tap == 3) ? 1 : 2;
+  run_microbatch(P, x, (int)B, scratch, w, true, stage, st);
+  const void* src = tap == 0 ? (const void*)w.xhat : tap == 1 ? (const void*)w.u1 : tap == 2 ? (const void*)w.y2
+                                                                                               : (const void*)w.yphi;
+  e = cudaMemcpyAsync(out, src, (size_t)need * 4, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(scratch);
+  if (e != cudaSuccess) return cuda_fail(e, "debug tap");
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "debug tap launch");
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap) {
+  if (!plan || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  double f[6], b[6];
+  jtfs::stage_cost(plan->P, f, b);
+  for (int i = 0; i < std::min(cap, 6); ++i) {
+    if (flops) flops[i] = f[i];
+    if (bytes) bytes[i] = b[i];
+  }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_profile_enable(jtfs_plan_t plan, int32_t enable) {
+  if (!plan) return fail(JTFS_ERR_INVALID_ARG, "plan is NULL");
+  plan->P.prof = enable != 0;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_profile_read(jtfs_plan_t plan, double* stage_ms, int64_t* stage_launches, int32_t cap,
+                              int32_t reset) {
+  if (!plan || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  jtfs::Plan& P = plan->P;
+  for (int s = 0; s < JTFS_N_STAGES; ++s) {
+    double ms = 0;
+    for (auto& pr : P.prof_events[s]) {
+      float t = 0;
+      cudaError_t e = cudaEventSynchronize((cudaEvent_t)pr.second);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&t, (cudaEvent_t)pr.first, (cudaEvent_t)pr.second);
+      if (e != cudaSuccess) return cuda_fail(e, "profile events");
+      ms += t;
+    }
+    if (s < cap) {
+      if (stage_ms) stage_ms[s] = ms;
+      if (stage_launches) stage_launches[s] = P.launches[s];
+    }
+    if (reset) {
+      for (auto& pr : P.prof_events[s]) {
+        cudaEventDestroy((cudaEvent_t)pr.first);
+        cudaEventDestroy((cudaEvent_t)pr.second);
+      }
+      P.prof_events[s].clear();
+      P.launches[s] = 0;
+    }
+  }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_debug_filter(jtfs_plan_t plan, int32_t bank, int32_t idx, int32_t L, int32_t n_grid,
+                              double* out) {
+  if (!plan || !out || L < 1 || n_grid < 1) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const jtfs::Plan& P = plan->P;
+  const jtfs::Bank* b = bank == 1 ? &P.b1 : bank == 2 ? &P.b2 : bank == 3 ? &P.bf : nullptr;
+  if (b) {
+    if (idx < 0 || idx >= (int)b->xi.size()) return fail(JTFS_ERR_INVALID_ARG, "filter index out of range");
+    jtfs::morlet_hat(b->xi[idx], b->sigma[idx], L, n_grid, out);
+    return JTFS_OK;
+  }
+  if (bank == 4) { jtfs::gauss_hat(0.1 / P.T, L, n_grid, out); return JTFS_OK; }
+  if (bank == 5) { jtfs::gauss_hat(0.1 / P.F, L, n_grid, out); return JTFS_OK; }
+  return fail(JTFS_ERR_INVALID_ARG, "unknown bank");
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// Shared-memory Stockham FFT for sm_100a (radix-8 passes + one radix-2/4 pass).
+//
+// G rows of length L = 2^LOG2L live contiguously in shared memory; NT threads
+// run each pass: every thread loads its butterflies' inputs into registers,
+// barrier, twiddle + in-register radix-R DFT, then stores to the Stockham
+// output positions, barrier.  (One buffer, in place: reads and writes of a
+// pass are separated by the barrier.)  Twiddles come from a fp32 table
+// W[t] = exp(-2 pi i t / N_tw) built in fp64 on the host.
+// DIR = -1: forward DFT  sum_n x[n] e^{-2 pi i k n / L};  DIR = +1: unnormalised inverse.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace jtfs {
+namespace dev {
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+template <int DIR>
+__device__ __forceinline__ float2 twiddle(const float2* __restrict__ W, int u) {
+  const float2 w = __ldg(W + u);
+  return DIR < 0 ? w : make_float2(w.x, -w.y);
+}
+
+// cos / sin of 2 pi j / 16, j in [0, 8)
+__device__ __forceinline__ float c16(int j) {
+  switch (j) {
+    case 0: return 1.0f;
+    case 1: return 0.92387953251128674f;
+    case 2: return 0.70710678118654752f;
+    case 3: return 0.38268343236508977f;
+    case 4: return 0.0f;
+    case 5: return -0.38268343236508977f;
+    case 6: return -0.70710678118654752f;
+    default: return -0.92387953251128674f;
+  }
+}
+__device__ __forceinline__ float s16(int j) {
+  switch (j) {
+    case 0: return 0.0f;
+    case 1: return 0.38268343236508977f;
+    case 2: return 0.70710678118654752f;
+    case 3: return 0.92387953251128674f;
+    case 4: return 1.0f;
+    case 5: return 0.92387953251128674f;
+    case 6: return 0.70710678118654752f;
+    default: return 0.38268343236508977f;
+  }
+}
+
+// multiply by exp(DIR * 2 pi i j / 16) with j a compile-time constant after unrolling
+template <int DIR>
+__device__ __forceinline__ float2 rot16(float2 a, int j) {
+  if (j == 0) return a;
+  if (j == 4) return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+  const float c = c16(j), s = DIR * s16(j);
+  return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+}
+
+__host__ __device__ constexpr int bitrev(int v, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+
+// In-register R-point DFT (R = 2, 4, 8, 16): radix-2 decimation in frequency,
+// then the bit-reversal permutation so that v[r] = X[r] on exit.
+template <int R, int DIR>
+__device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+#pragma unroll
+  for (int span = R / 2; span >= 1; span >>= 1) {
+#pragma unroll
+    for (int start = 0; start < R; start += 2 * span) {
+#pragma unroll
+      for (int k = 0; k < span; ++k) {
+        const float2 a = v[start + k], b = v[start + k + span];
+        v[start + k] = cadd(a, b);
+        v[start + k + span] = rot16<DIR>(csub(a, b), k * (16 / (2 * span)));
+      }
+    }
+  }
+  constexpr int bits = ilog2c(R);
+  float2 t[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) t[r] = v[bitrev(r, bits)];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = t[r];
+}
+
+// One Stockham pass of radix R over G rows of length L held in smem s[g*LS + e]
+// (LS >= L is the row stride; LS = L + 1 breaks bank conflicts of column gathers).
+template <int LOG2L, int R, int G, int NT, int DIR, int LS>
+__device__ __forceinline__ void stockham_pass(float2* s, int log2Ns, const float2* __restrict__ W,
+                                              int log2Ntw) {
+  constexpr int L = 1 << LOG2L;
+  constexpr int LR = L / R;
+  constexpr int NBF = G * LR;
+  constexpr int BPT = (NBF + NT - 1) / NT;
+  constexpr int LOG2R = ilog2c(R);
+  const int Ns = 1 << log2Ns;
+  const int twshift = log2Ntw - (log2Ns + LOG2R);
+  float2 v[BPT][R];
+  int base[BPT];
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    const int bf = threadIdx.x + i * NT;
+    base[i] = -1;
+    if ((NBF % NT == 0) || bf < NBF) {
+      const int g = bf / LR, j = bf % LR;
+      const float2* row = s + g * LS;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[i][r] = row[j + r * LR];
+      const int k = j & (Ns - 1);
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twiddle<DIR>(W, (r * k) << twshift));
+      }
+      dft_reg<R, DIR>(v[i]);
+      base[i] = g * LS + (j - k) * R + k;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    if (base[i] >= 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[base[i] + r * Ns] = v[i][r];
+    }
+  }
+  __syncthreads();
+}
+
+// Full FFT of G rows in smem (caller has __syncthreads()'d after filling s).
+template <int LOG2L, int G, int NT, int DIR, int LS = (1 << LOG2L)>
+__device__ __forceinline__ void fft_smem(float2* s, const float2* __restrict__ W, int log2Ntw) {
+  constexpr int REM = LOG2L % 3;
+  int log2Ns = 0;
+  if constexpr (REM != 0) {
+    stockham_pass<LOG2L, (1 << REM), G, NT, DIR, LS>(s, 0, W, log2Ntw);
+    log2Ns = REM;
+  }
+  if constexpr (LOG2L >= 3) {
+#pragma unroll 1
+    for (int p = 0; p < LOG2L / 3; ++p) {
+      stockham_pass<LOG2L, 8, G, NT, DIR, LS>(s, log2Ns, W, log2Ntw);
+      log2Ns += 3;
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace jtfs

@@ -1,0 +1,146 @@
+// Internal plan of the B200 JTFS path.  Host-side schedule + device tables.
+// Written from PAPER.md Sec. 2 and DESIGN.md §3 readings; shares no
+// code with oracle/ (the fp64 numpy oracle).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/jtfs.h"
+
+namespace jtfs {
+
+// ---- filter generator G(J', Q')  (R1, R2, R5) --------------------------
+struct Bank {
+  std::vector<double> xi, sigma;  // cycles/sample (or cycles/bin), descending xi
+  std::vector<int> j;             // critical subsampling exponent
+};
+Bank morlet_bank(int J, int Q);
+void morlet_hat(double xi, double sigma, int L, int n_grid, double* out);
+void gauss_hat(double sigma, int L, int n_grid, double* out);
+
+// A circular arc [m0, m0+len) (mod grid length) of a sampled spectrum whose
+// values are stored in Plan::bandvals[off .. off+len).
+struct Band {
+  int32_t m0 = 0, len = 0;
+  int64_t off = 0;
+};
+
+// One FFT row of a fused band-multiply + fold + FFT launch (per signal).
+struct FoldRow {
+  int64_t src_off;   // complex offset of the source spectrum row inside one signal's source buffer
+  int32_t Lsrc;      // source grid length
+  int32_t m0, len;   // band arc on the source grid
+  int64_t band_off;  // offset into bandvals
+  int64_t dst_off;   // offset of the output row inside one signal's destination buffer
+  float scale;       // output scale
+  int32_t pad;
+};
+
+// A launch group: all rows (per signal) that share one FFT length.
+struct FoldGroup {
+  int log2L;
+  std::vector<FoldRow> rows;
+  FoldRow* d_rows = nullptr;
+};
+
+// One active second-order temporal wavelet psi_alpha and its KD problem.
+struct AlphaKD {
+  int alpha;        // index in bank 2
+  int K;            // admissible lambda rows [0, K)
+  int k_alpha;      // time exponent
+  int L;            // time length N_pad >> k_alpha
+  int D;            // pooling stride 2^(log2T - k_alpha)
+  int64_t y2_off;   // complex offset of Y2_alpha in one signal's Y2 buffer
+  int Kpad;         // K rounded up to the contraction chunk
+  int64_t a_off;    // complex offset of A_alpha^T [Kpad][Mpad] in the A table
+  int64_t g_off;    // float offset of the time-pooling taps g_alpha[L]
+  int chunk;        // time columns per KD work unit
+  int nchunks;      // L / chunk
+  int64_t part_off; // float offset of partials [nchunks][Mpad][n_frames] in one signal
+};
+
+// A frequential filter f of the joint stage (rows of every A_alpha).
+struct FrFilter {
+  int kind;         // 0 psi_beta (spin), 1 phi_F
+  int theta;        // -1/+1 for psi
+  int beta;
+  int k;            // lambda decimation exponent
+  int R;            // N_fr >> k
+  int row0, nrows;  // row block inside the M rows of every alpha
+  std::vector<int> rprime;  // the retained rows r' (decimated grid indices)
+  int64_t w_off;    // float offset of the lambda-pooling matrix W [lambda_out][nrows]
+};
+
+struct Plan {
+  jtfs_params prm{};
+  // derived scalars
+  int N = 0, N_pad = 0, pad_left = 0, T = 0, log2T = 0, F = 0, log2F = 0;
+  int n1 = 0, N_fr = 0, frame0 = 0, n_frames = 0, lam_out = 0, NPT = 0;  // NPT = N_pad / T
+  Bank b1, b2, bf;
+  std::vector<int> k1, L1;
+  std::vector<int64_t> u1_off;   // per lambda offset in U1 / U1hat (per signal)
+  int64_t u1_total = 0;          // sum of L1
+  std::vector<AlphaKD> kd;       // active alphas in bank order
+  int64_t y2_total = 0;          // complex elements of Y2 per signal
+  int M = 0, Mpad = 0;           // joint-stage rows per alpha
+  std::vector<FrFilter> fr;      // frequential filters: theta=-1 (beta), theta=+1 (beta), phi_F
+  std::vector<jtfs_path_t> paths;
+  std::vector<int> path_filter;  // path -> fr index (or -1)
+  int64_t part_total = 0;        // floats of KD partials per signal
+
+  // ---- host tables (fp32 unless noted) ----
+  std::vector<float> bandvals;
+  std::vector<Band> band_psi1;           // per lambda, on the N_pad grid
+  Band band_phiT_pad;                    // phi_T on the N_pad grid (S0)
+  std::vector<Band> band_phiT_L1;        // phi_T on the grid N_pad >> k, k = 0..log2T
+  std::vector<FoldGroup> u1_groups;      // first-order IFFT rows grouped by L1
+  std::vector<FoldGroup> y2_groups;      // second-order rows grouped by L_alpha
+  std::vector<float> A;                  // complex interleaved A_alpha^T tables
+  std::vector<float> g;                  // time pooling taps per alpha
+  std::vector<float> W;                  // lambda pooling matrices per filter
+  std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
+                                         // then [N_fr] real phi_F taps, then [NPT] real phi_T taps
+  std::vector<float> twiddle;            // complex exp(-2 pi i t / N_tw), t < N_tw
+  int N_tw = 0;
+
+  // ---- device copies ----
+  int device = -1;
+  float* d_bandvals = nullptr;
+  float* d_A = nullptr;
+  float* d_g = nullptr;
+  float* d_W = nullptr;
+  float* d_hphi = nullptr;
+  float* d_twiddle = nullptr;
+  void* d_alphas = nullptr;    // DevAlpha[n_alpha]
+  void* d_fr = nullptr;        // DevFilter[n_filters]
+  int32_t* d_rprime = nullptr; // concatenated retained rows of every filter
+  void* d_paths = nullptr;     // DevPath[n_paths]
+  int64_t* d_u1_off = nullptr; // per lambda
+  int32_t* d_k1 = nullptr;     // per lambda
+  Band* d_band_L1 = nullptr;   // phi_T bands per k
+  std::vector<void*> allocations;
+
+  int mb = 16;                 // signals per micro-batch
+
+  // ---- profiling (the only mutable state; see jtfs_profile_enable) ----
+  bool prof = false;
+  std::vector<std::pair<void*, void*>> prof_events[6];  // cudaEvent_t pairs per stage
+  int64_t launches[6] = {0, 0, 0, 0, 0, 0};
+};
+
+// plan.cpp
+std::string build_plan(const jtfs_params& p, Plan& plan);   // returns "" or an error message
+int ilog2_exact(int64_t v);  // -1 if not a power of two
+
+// workspace layout (per micro-batch of mb signals), in bytes
+struct WsLayout {
+  size_t xhat, tmp, u1, u1hat, yphi, y2, part, flag, total;
+};
+WsLayout ws_layout(const Plan& p, int64_t mb);
+
+// algorithmic per-signal cost per stage (jtfs_cost)
+void stage_cost(const Plan& p, double flops[6], double bytes[6]);
+
+}  // namespace jtfs

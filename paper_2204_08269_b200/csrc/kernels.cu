@@ -1,0 +1,698 @@
+// CUDA kernels (sm_100a) of the forward JTFS hot path.
+//
+//   KA  reflect-pad + DFT of x                                  (R6)
+//   KB  band-multiply psi_lambda + fold + IDFT + modulus -> U1, DFT(U1) -> U1hat
+//       (scalogram X = |x * psi_lambda|, critically subsampled: P:71; R5)
+//   KS  S0 / S1 / Y_phi: phi_T averaging at rate T by spectral folding
+//   KC  U1hat * psi_alpha + fold + IDFT -> Y2_alpha (Eq. (1) temporal rate)
+//   KD  frequential contraction along lambda with psi_{beta,theta} / phi_F (Eq. (1)
+//       P:79, Eq. (2)) + complex modulus + phi_T pooling (Eq. (3))
+//   KE  phi_F pooling along lambda, phi-only paths, out_3D packing
+//
+// Every spectral decimation is done by folding (aliasing-sum) the band-limited
+// product spectrum to the decimated length before a shorter inverse FFT, which is
+// the exact identity IDFT_L(X)[n d] = (1/d) IDFT_{L/d}(fold X)[n].
+#include <cstdint>
+#include <cstdio>
+
+#include "fft.cuh"
+#include "jtfs_internal.h"
+#include "kernels.h"
+
+namespace jtfs {
+namespace dev {
+
+// ---------------------------------------------------------------------------------
+// gather: output bin i (of a length-L fold) of the band-limited product src * band
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ float2 fold_value(const float2* __restrict__ src, const FoldRow& d,
+                                             const float* __restrict__ bandvals, int i, int L) {
+  float2 acc = make_float2(0.f, 0.f);
+  int t = (i - d.m0) % L;
+  if (t < 0) t += L;
+  for (; t < d.len; t += L) {
+    int p = d.m0 + t;
+    if (p >= d.Lsrc) p -= d.Lsrc;
+    const float2 x = src[d.src_off + p];
+    const float f = __ldg(bandvals + d.band_off + t);
+    acc.x = fmaf(x.x, f, acc.x);
+    acc.y = fmaf(x.y, f, acc.y);
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------------
+// problems: load(rho, i) -> element i of input row rho; store(rho, o, v)
+// ---------------------------------------------------------------------------------
+struct ProbPad {  // KA: x_pad[b][i] = x[b][reflect(i - pad_left)]
+  const float* x;
+  float2* xhat;
+  int N, N_pad, pad_left, periodic;
+  __device__ float2 load(int b, int i) const {
+    int n = i - pad_left;
+    if (!periodic) {
+      if (n < 0) n = -n;
+      if (n >= N) n = 2 * (N - 1) - n;
+    }
+    return make_float2(__ldg(x + (int64_t)b * N + n), 0.f);
+  }
+  __device__ void store(int b, int o, float2 v) const { xhat[(int64_t)b * N_pad + o] = v; }
+};
+
+struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
+  const float2* src;
+  int64_t src_stride;
+  const FoldRow* rows;
+  int nrows;
+  const float* bandvals;
+  int L;
+  // outputs
+  float* dst_real;   // modulus output (U1) or nullptr
+  float2* dst_cplx;  // complex output (Y2) or nullptr
+  int64_t dst_stride;
+  __device__ float2 load(int rho, int i) const {
+    const int b = rho / nrows, r = rho % nrows;
+    return fold_value(src + (int64_t)b * src_stride, rows[r], bandvals, i, L);
+  }
+  __device__ void store(int rho, int o, float2 v) const {
+    const int b = rho / nrows, r = rho % nrows;
+    const FoldRow& d = rows[r];
+    if (dst_real) {
+      dst_real[(int64_t)b * dst_stride + d.dst_off + o] = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * d.scale;
+    } else {
+      dst_cplx[(int64_t)b * dst_stride + d.dst_off + o] = cscale(v, d.scale);
+    }
+  }
+};
+
+struct ProbRealFwd {  // U1 (real) -> U1hat
+  const float* u1;
+  float2* u1hat;
+  int64_t stride;
+  const FoldRow* rows;
+  int nrows;
+  __device__ float2 load(int rho, int i) const {
+    const int b = rho / nrows, r = rho % nrows;
+    return make_float2(u1[(int64_t)b * stride + rows[r].dst_off + i], 0.f);
+  }
+  __device__ void store(int rho, int o, float2 v) const {
+    const int b = rho / nrows, r = rho % nrows;
+    u1hat[(int64_t)b * stride + rows[r].dst_off + o] = v;
+  }
+};
+
+// ---------------------------------------------------------------------------------
+// single-CTA FFT of G rows per block
+// ---------------------------------------------------------------------------------
+template <int LOG2L, int G, int NT, int DIR, class P>
+__global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const float2* __restrict__ W,
+                                                 int log2Ntw) {
+  constexpr int L = 1 << LOG2L;
+  extern __shared__ float2 smem[];
+  const int rho0 = blockIdx.x * G;
+  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
+    const int g = idx / L, e = idx % L;
+    smem[idx] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  fft_smem<LOG2L, G, NT, DIR>(smem, W, log2Ntw);
+  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
+    const int g = idx / L, e = idx % L;
+    if (rho0 + g < nrows) prob.store(rho0 + g, e, smem[idx]);
+  }
+}
+
+// fused first order for L1 <= 4096: fold -> IDFT -> |.| scale -> DFT -> U1hat (+U1)
+template <int LOG2L, int G, int NT>
+__global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restrict__ u1hat,
+                                                 float* __restrict__ u1dbg, int nrows,
+                                                 const float2* __restrict__ W, int log2Ntw) {
+  constexpr int L = 1 << LOG2L;
+  extern __shared__ float2 smem[];
+  const int rho0 = blockIdx.x * G;
+  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
+    const int g = idx / L, e = idx % L;
+    smem[idx] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  fft_smem<LOG2L, G, NT, +1>(smem, W, log2Ntw);
+  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
+    const int g = idx / L;
+    const int rho = min(rho0 + g, nrows - 1);
+    const float sc = prob.rows[rho % prob.nrows].scale;
+    const float2 v = smem[idx];
+    smem[idx] = make_float2(sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc, 0.f);
+  }
+  __syncthreads();
+  if (u1dbg) {
+    for (int idx = threadIdx.x; idx < G * L; idx += NT) {
+      const int g = idx / L, e = idx % L;
+      const int rho = rho0 + g;
+      if (rho < nrows) {
+        const int b = rho / prob.nrows, r = rho % prob.nrows;
+        u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = smem[idx].x;
+      }
+    }
+  }
+  fft_smem<LOG2L, G, NT, -1>(smem, W, log2Ntw);
+  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
+    const int g = idx / L, e = idx % L;
+    const int rho = rho0 + g;
+    if (rho < nrows) {
+      const int b = rho / prob.nrows, r = rho % prob.nrows;
+      u1hat[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = smem[idx];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// four-step FFT, L = La * Lb:  step A: column FFTs (length La) of x[na*Lb + nb] then
+// twiddle W_L^{ka nb};  step B: row FFTs (length Lb) -> X[ka + La kb]
+// ---------------------------------------------------------------------------------
+template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
+__global__ void __launch_bounds__(NT) k_fft4_a(P prob, float2* __restrict__ tmp,
+                                               const float2* __restrict__ W, int log2Ntw) {
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
+  constexpr int LS = La + 1;
+  extern __shared__ float2 smem[];
+  constexpr int CPB = Lb / G;  // column groups per big row
+  const int rho = blockIdx.x / CPB;
+  const int nb0 = (blockIdx.x % CPB) * G;
+  for (int idx = threadIdx.x; idx < G * La; idx += NT) {
+    const int g = idx % G, na = idx / G;
+    smem[g * LS + na] = prob.load(rho, na * Lb + nb0 + g);
+  }
+  __syncthreads();
+  fft_smem<LOG2A, G, NT, DIR, LS>(smem, W, log2Ntw);
+  float2* out = tmp + (int64_t)rho * L;
+  for (int idx = threadIdx.x; idx < G * La; idx += NT) {
+    const int g = idx % G, ka = idx / G;
+    const int u = (ka * (nb0 + g)) << (log2Ntw - (LOG2A + LOG2B));
+    out[ka * Lb + nb0 + g] = cmul(smem[g * LS + ka], twiddle<DIR>(W, u));
+  }
+}
+
+template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
+__global__ void __launch_bounds__(NT) k_fft4_b(P prob, const float2* __restrict__ tmp,
+                                               const float2* __restrict__ W, int log2Ntw) {
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
+  constexpr int LS = Lb + 1;
+  extern __shared__ float2 smem[];
+  constexpr int RPB = La / G;
+  const int rho = blockIdx.x / RPB;
+  const int ka0 = (blockIdx.x % RPB) * G;
+  const float2* in = tmp + (int64_t)rho * L;
+  for (int idx = threadIdx.x; idx < G * Lb; idx += NT) {
+    const int g = idx / Lb, e = idx % Lb;
+    smem[g * LS + e] = in[(ka0 + g) * Lb + e];
+  }
+  __syncthreads();
+  fft_smem<LOG2B, G, NT, DIR, LS>(smem, W, log2Ntw);
+  for (int idx = threadIdx.x; idx < G * Lb; idx += NT) {
+    const int g = idx % G, kb = idx / G;
+    prob.store(rho, ka0 + g + La * kb, smem[g * LS + kb]);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// KS: phi_T averaging at rate T by folding the band-limited spectrum to NPT bins.
+// One warp per (signal, row).  row < 0 denotes S0 (source X_hat on the N_pad grid).
+// ---------------------------------------------------------------------------------
+struct KSParams {
+  const float2* xhat;
+  const float2* u1hat;
+  float* yphi;
+  float* out;
+  const float* bandvals;
+  const float2* W;
+  int log2Ntw;
+  int n1, NPT, N_pad, frame0, n_frames;
+  int64_t u1_stride, fps, off_s0, off_s1;
+  const int64_t* u1_off;  // per lambda
+  const int* k1;          // per lambda
+  Band band_pad;          // phi_T on the N_pad grid
+  const Band* band_L1;    // phi_T on grid N_pad >> k
+  int nsig;
+};
+
+__global__ void __launch_bounds__(128) k_phi_first(KSParams p) {
+  __shared__ float2 fold[4][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * 4 + warp;  // item = b * (n1 + 1) + (row + 1)
+  const int per = p.n1 + 1;
+  if (item >= p.nsig * per) return;
+  const int b = item / per, row = item % per - 1;
+  const float2* src;
+  int Lsrc;
+  Band bd;
+  float scale;
+  if (row < 0) {
+    src = p.xhat + (int64_t)b * p.N_pad;
+    Lsrc = p.N_pad;
+    bd = p.band_pad;
+    scale = 1.f / (float)p.N_pad;
+  } else {
+    src = p.u1hat + (int64_t)b * p.u1_stride + p.u1_off[row];
+    const int k = p.k1[row];
+    Lsrc = p.N_pad >> k;
+    bd = p.band_L1[k];
+    scale = 1.f / (float)Lsrc;
+  }
+  const int NPT = p.NPT;
+  for (int i = lane; i < NPT; i += 32) {
+    float2 acc = make_float2(0.f, 0.f);
+    int t = (i - bd.m0) % NPT;
+    if (t < 0) t += NPT;
+    for (; t < bd.len; t += NPT) {
+      int q = bd.m0 + t;
+      if (q >= Lsrc) q -= Lsrc;
+      const float2 x = src[q];
+      const float f = __ldg(p.bandvals + bd.off + t);
+      acc.x = fmaf(x.x, f, acc.x);
+      acc.y = fmaf(x.y, f, acc.y);
+    }
+    fold[warp][i] = acc;
+  }
+  __syncwarp();
+  const int shift = p.log2Ntw - (31 - __clz(NPT));
+  for (int n = lane; n < NPT; n += 32) {
+    float acc = 0.f;
+    for (int m = 0; m < NPT; ++m) {  // Re of IDFT: sum_m F[m] e^{+2 pi i m n / NPT}
+      const float2 w = twiddle<+1>(p.W, ((m * n) & (NPT - 1)) << shift);
+      acc = fmaf(fold[warp][m].x, w.x, acc);
+      acc = fmaf(-fold[warp][m].y, w.y, acc);
+    }
+    acc *= scale;
+    if (row < 0) {
+      const int m = n - p.frame0;
+      if (m >= 0 && m < p.n_frames) p.out[(int64_t)b * p.fps + p.off_s0 + m] = acc;
+    } else {
+      p.yphi[((int64_t)b * p.n1 + row) * NPT + n] = acc;
+      const int m = n - p.frame0;
+      if (m >= 0 && m < p.n_frames)
+        p.out[(int64_t)b * p.fps + p.off_s1 + (int64_t)row * p.n_frames + m] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// KD (SIMT v1): per (signal, alpha, chunk, 64-row block): Z = A_alpha Y2_alpha over a
+// 64 x 128 tile (complex fp32, 4 FFMA per complex MAC), |Z|, phi_T pooling into the
+// retained frames with taps g_alpha; per-unit partials written in fixed order.
+// ---------------------------------------------------------------------------------
+template <int NF>
+__global__ void __launch_bounds__(256) k_kd_simt(KDParams p) {
+  __shared__ float2 As[8][64];
+  __shared__ float2 Ys[8][128];
+  __shared__ float gs[NF][128];
+  const int nmb = p.Mpad / 64;
+  int u = blockIdx.x;
+  const int mblk = u % nmb;
+  u /= nmb;
+  const int ch = u % p.nchunks;
+  const int b = u / p.nchunks;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float2* Y = p.y2 + (int64_t)b * p.y2_stride + p.y2_off;
+  const float2* A = p.A + mblk * 64;
+  float part[4][NF];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int m = 0; m < NF; ++m) part[i][m] = 0.f;
+  const int col_end = (ch + 1) * p.chunk;
+  const int ntile = (p.chunk + 127) / 128;
+  for (int tile = 0; tile < ntile; ++tile) {
+    const int c0 = ch * p.chunk + tile * 128;
+    // pooling taps for this tile
+    for (int idx = threadIdx.x; idx < NF * 128; idx += 256) {
+      const int m = idx / 128, c = idx % 128;
+      float w = 0.f;
+      if (m < p.nframes && c0 + c < col_end) {
+        int t = ((p.frame0 + m) * p.D - (c0 + c)) % p.L;
+        if (t < 0) t += p.L;
+        w = __ldg(p.g + t);
+      }
+      gs[m][c] = w;
+    }
+    float2 acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int k0 = 0; k0 < p.Kpad; k0 += 8) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int idx = threadIdx.x + q * 256;
+        const int kk = idx / 64, r = idx % 64;
+        As[kk][r] = A[(int64_t)(k0 + kk) * p.Mpad + r];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = threadIdx.x + q * 256;
+        const int kk = idx / 128, c = idx % 128;
+        float2 y = make_float2(0.f, 0.f);
+        if (k0 + kk < p.K && c0 + c < col_end) y = Y[(int64_t)(k0 + kk) * p.L + c0 + c];
+        Ys[kk][c] = y;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        float2 a[4], y[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) y[j] = Ys[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc[i][j].x = fmaf(a[i].x, y[j].x, acc[i][j].x);
+            acc[i][j].x = fmaf(-a[i].y, y[j].y, acc[i][j].x);
+            acc[i][j].y = fmaf(a[i].x, y[j].y, acc[i][j].y);
+            acc[i][j].y = fmaf(a[i].y, y[j].x, acc[i][j].y);
+          }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float w[NF];
+#pragma unroll
+      for (int m = 0; m < NF; ++m) w[m] = gs[m][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float mag = sqrtf(fmaf(acc[i][j].x, acc[i][j].x, acc[i][j].y * acc[i][j].y));
+#pragma unroll
+        for (int m = 0; m < NF; ++m) part[i][m] = fmaf(w[m], mag, part[i][m]);
+      }
+    }
+    __syncthreads();  // gs reuse
+  }
+  // reduce over the 16 column lanes (fixed xor tree -> deterministic)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int m = 0; m < NF; ++m) {
+      float v = part[i][m];
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      part[i][m] = v;
+    }
+  if (tx == 0) {
+    float* dst = p.part + (int64_t)b * p.part_stride + p.part_off +
+                 ((int64_t)ch * p.Mpad + mblk * 64 + ty * 4) * p.nframes;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int m = 0; m < NF; ++m)
+        if (m < p.nframes) dst[i * p.nframes + m] = part[i][m];
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// KE: lambda pooling (phi_F) of the pooled rows, phi-only paths, packing of S2.
+// One block per (signal, path).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ke(KEParams p) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x;
+  const int pi = blockIdx.y;
+  const DevPath P = p.paths[pi];
+  const int nf = p.n_frames;
+  float* outp = p.out + (int64_t)b * p.fps + p.off_s2 + (int64_t)pi * p.lam_out * nf;
+  if (P.kind == JTFS_PATH_PHI_T_PHI_F) {
+    const float* yphi = p.yphi + (int64_t)b * p.n1 * p.NPT;
+    for (int idx = threadIdx.x; idx < p.lam_out * nf; idx += blockDim.x) {
+      const int q = idx / nf, m = idx % nf;
+      float acc = 0.f;
+      for (int l = 0; l < p.n1; ++l) {
+        int d = ((q << p.k_phiphi) - l) % p.N_fr;
+        if (d < 0) d += p.N_fr;
+        acc = fmaf(__ldg(p.hphiF + d), yphi[l * p.NPT + p.frame0 + m], acc);
+      }
+      outp[idx] = acc;
+    }
+    return;
+  }
+  const DevFilter f = p.filters[P.filter];
+  float* Pm = sm;  // [nrows][nf]
+  if (P.kind == JTFS_PATH_PHI_T_PSI_F) {
+    const float* yphi = p.yphi + (int64_t)b * p.n1 * p.NPT;
+    float* ys = sm + f.nrows * nf;           // [n1][NPT]
+    float* u2 = ys + p.n1 * p.NPT;           // [nrows][NPT]
+    for (int idx = threadIdx.x; idx < p.n1 * p.NPT; idx += blockDim.x) ys[idx] = yphi[idx];
+    __syncthreads();
+    const float2* h = p.hpsi + (int64_t)P.beta * p.N_fr;
+    for (int idx = threadIdx.x; idx < f.nrows * p.NPT; idx += blockDim.x) {
+      const int r = idx / p.NPT, n = idx % p.NPT;
+      const int rp = p.rprime[f.rp_off + r] << f.k;
+      float2 z = make_float2(0.f, 0.f);
+      for (int l = 0; l < p.n1; ++l) {
+        int d = (rp - l) % p.N_fr;
+        if (d < 0) d += p.N_fr;
+        const float2 hv = __ldg(h + d);
+        const float yv = ys[l * p.NPT + n];
+        z.x = fmaf(hv.x, yv, z.x);
+        z.y = fmaf(hv.y, yv, z.y);
+      }
+      u2[idx] = sqrtf(fmaf(z.x, z.x, z.y * z.y));
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < f.nrows * nf; idx += blockDim.x) {
+      const int r = idx / nf, m = idx % nf;
+      float acc = 0.f;
+      for (int n = 0; n < p.NPT; ++n) {
+        int d = (p.frame0 + m - n) % p.NPT;
+        if (d < 0) d += p.NPT;
+        acc = fmaf(__ldg(p.gT + d), u2[r * p.NPT + n], acc);
+      }
+      Pm[idx] = acc;
+    }
+    __syncthreads();
+  } else {
+    // spinned or psi_t x phi_f: sum the KD partials over chunks in fixed order
+    const DevAlpha a = p.alphas[P.alpha_slot];
+    const float* part = p.part + (int64_t)b * p.part_stride + a.part_off;
+    for (int idx = threadIdx.x; idx < f.nrows * nf; idx += blockDim.x) {
+      const int r = idx / nf, m = idx % nf;
+      float acc = 0.f;
+      for (int c = 0; c < a.nchunks; ++c)
+        acc += part[((int64_t)c * p.Mpad + f.row0 + r) * nf + m];
+      Pm[idx] = acc;
+    }
+    __syncthreads();
+  }
+  const float* Wf = p.W + f.w_off;
+  for (int idx = threadIdx.x; idx < p.lam_out * nf; idx += blockDim.x) {
+    const int q = idx / nf, m = idx % nf;
+    float acc = 0.f;
+    for (int r = 0; r < f.nrows; ++r) acc = fmaf(__ldg(Wf + (int64_t)q * f.nrows + r), Pm[r * nf + m], acc);
+    outp[idx] = acc;
+  }
+}
+
+// check for NaN / Inf in x
+__global__ void k_check_finite(const float* x, int64_t n, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) atomicOr(flag, 1);
+}
+
+}  // namespace dev
+
+// =================================================================================
+// host launchers
+// =================================================================================
+using namespace dev;
+
+namespace {
+template <int LOG2L>
+constexpr int rows_G() { return (LOG2L >= 11) ? 1 : (2048 >> LOG2L); }
+template <int LOG2L>
+constexpr int rows_NT() { return (rows_G<LOG2L>() << LOG2L) / 8 < 32 ? 32 : (rows_G<LOG2L>() << LOG2L) / 8; }
+
+template <int LOG2L, int DIR, class P>
+void launch_rows(const P& prob, int nrows, const float2* W, int log2Ntw, cudaStream_t st) {
+  constexpr int G = rows_G<LOG2L>();
+  constexpr int NT = rows_NT<LOG2L>();
+  const int grid = (nrows + G - 1) / G;
+  const size_t sm = (size_t)G * (1 << LOG2L) * sizeof(float2);
+  k_fft_rows<LOG2L, G, NT, DIR, P><<<grid, NT, sm, st>>>(prob, nrows, W, log2Ntw);
+}
+
+template <int LOG2L>
+void launch_u1_fused(const ProbFold& prob, float2* u1hat, float* u1dbg, int nrows, const float2* W,
+                     int log2Ntw, cudaStream_t st) {
+  constexpr int G = rows_G<LOG2L>();
+  constexpr int NT = rows_NT<LOG2L>();
+  const int grid = (nrows + G - 1) / G;
+  const size_t sm = (size_t)G * (1 << LOG2L) * sizeof(float2);
+  k_u1_fused<LOG2L, G, NT><<<grid, NT, sm, st>>>(prob, u1hat, u1dbg, nrows, W, log2Ntw);
+}
+
+template <int LOG2L, int DIR, class PA, class PB>
+void launch_fft4(const PA& pa, const PB& pb, int nbig, float2* tmp, const float2* W, int log2Ntw,
+                 cudaStream_t st) {
+  constexpr int LOG2A = (LOG2L + 1) / 2, LOG2B = LOG2L / 2;
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B;
+  constexpr int GA = 4096 / La, GB = 4096 / Lb;
+  constexpr int NT = 512;
+  k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA>
+      <<<nbig * (Lb / GA), NT, (size_t)GA * (La + 1) * sizeof(float2), st>>>(pa, tmp, W, log2Ntw);
+  k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB>
+      <<<nbig * (La / GB), NT, (size_t)GB * (Lb + 1) * sizeof(float2), st>>>(pb, tmp, W, log2Ntw);
+}
+
+template <class F>
+void dispatch_log2(int lg, F&& f) {
+  switch (lg) {
+#define JTFS_CASE(n) \
+  case n: f(std::integral_constant<int, n>{}); break;
+    JTFS_CASE(1) JTFS_CASE(2) JTFS_CASE(3) JTFS_CASE(4) JTFS_CASE(5) JTFS_CASE(6)
+    JTFS_CASE(7) JTFS_CASE(8) JTFS_CASE(9) JTFS_CASE(10) JTFS_CASE(11) JTFS_CASE(12)
+    JTFS_CASE(13) JTFS_CASE(14) JTFS_CASE(15) JTFS_CASE(16) JTFS_CASE(17) JTFS_CASE(18)
+#undef JTFS_CASE
+    default: break;
+  }
+}
+}  // namespace
+
+int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2* tmp, cudaStream_t st) {
+  ProbPad pr{x, xhat, P.N, P.N_pad, P.pad_left, P.prm.pad_mode == JTFS_PAD_PERIODIC};
+  const float2* W = (const float2*)P.d_twiddle;
+  const int ltw = ilog2_exact(P.N_tw);
+  dispatch_log2(ilog2_exact(P.N_pad), [&](auto c) {
+    constexpr int LG = decltype(c)::value;
+    if constexpr (LG <= 12) {
+      launch_rows<LG, -1>(pr, nsig, W, ltw, st);
+    } else {
+      launch_fft4<LG, -1>(pr, pr, nsig, tmp, W, ltw, st);
+    }
+  });
+  return ilog2_exact(P.N_pad) <= 12 ? 1 : 2;
+}
+
+int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,
+                       bool keep_u1, cudaStream_t st) {
+  const float2* W = (const float2*)P.d_twiddle;
+  const int ltw = ilog2_exact(P.N_tw);
+  int n = 0;
+  for (const auto& g : P.u1_groups) {
+    n += g.log2L <= 12 ? 1 : 4;
+    const int nr = (int)g.rows.size();
+    ProbFold pf{xhat, P.N_pad, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, u1, nullptr, P.u1_total};
+    ProbRealFwd prf{u1, u1hat, P.u1_total, g.d_rows, nr};
+    dispatch_log2(g.log2L, [&](auto c) {
+      constexpr int LG = decltype(c)::value;
+      if constexpr (LG <= 12) {
+        launch_u1_fused<LG>(pf, u1hat, keep_u1 ? u1 : nullptr, nsig * nr, W, ltw, st);
+      } else {
+        launch_fft4<LG, +1>(pf, pf, nsig * nr, tmp, W, ltw, st);
+        launch_fft4<LG, -1>(prf, prf, nsig * nr, tmp, W, ltw, st);
+      }
+    });
+  }
+  return n;
+}
+
+int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int nsig, float* yphi, float* out,
+                      int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
+                      const Band* d_band_L1, cudaStream_t st) {
+  KSParams p{};
+  p.xhat = xhat;
+  p.u1hat = u1hat;
+  p.yphi = yphi;
+  p.out = out;
+  p.bandvals = P.d_bandvals;
+  p.W = (const float2*)P.d_twiddle;
+  p.log2Ntw = ilog2_exact(P.N_tw);
+  p.n1 = P.n1;
+  p.NPT = P.NPT;
+  p.N_pad = P.N_pad;
+  p.frame0 = P.frame0;
+  p.n_frames = P.n_frames;
+  p.u1_stride = P.u1_total;
+  p.fps = fps;
+  p.off_s0 = off_s0;
+  p.off_s1 = off_s1;
+  p.u1_off = d_u1_off;
+  p.k1 = d_k1;
+  p.band_pad = P.band_phiT_pad;
+  p.band_L1 = d_band_L1;
+  p.nsig = nsig;
+  const int items = nsig * (P.n1 + 1);
+  k_phi_first<<<(items + 3) / 4, 128, 0, st>>>(p);
+  return 1;
+}
+
+int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float2* y2, float2* tmp, cudaStream_t st) {
+  const float2* W = (const float2*)P.d_twiddle;
+  const int ltw = ilog2_exact(P.N_tw);
+  int n = 0;
+  for (const auto& g : P.y2_groups) {
+    n += g.log2L <= 12 ? 1 : 2;
+    const int nr = (int)g.rows.size();
+    ProbFold pf{u1hat, P.u1_total, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, nullptr, y2, P.y2_total};
+    dispatch_log2(g.log2L, [&](auto c) {
+      constexpr int LG = decltype(c)::value;
+      if constexpr (LG <= 12) {
+        launch_rows<LG, +1>(pf, nsig * nr, W, ltw, st);
+      } else {
+        launch_fft4<LG, +1>(pf, pf, nsig * nr, tmp, W, ltw, st);
+      }
+    });
+  }
+  return n;
+}
+
+int launch_kd(const Plan& P, const float2* y2, int nsig, float* part, cudaStream_t st) {
+  for (const auto& d : P.kd) {
+    KDParams k{};
+    k.A = (const float2*)P.d_A + d.a_off;
+    k.y2 = y2;
+    k.g = P.d_g + d.g_off;
+    k.part = part;
+    k.K = d.K;
+    k.Kpad = d.Kpad;
+    k.Mpad = P.Mpad;
+    k.L = d.L;
+    k.D = d.D;
+    k.frame0 = P.frame0;
+    k.nframes = P.n_frames;
+    k.chunk = d.chunk;
+    k.nchunks = d.nchunks;
+    k.y2_off = d.y2_off;
+    k.part_off = d.part_off;
+    k.y2_stride = P.y2_total;
+    k.part_stride = P.part_total;
+    const int grid = nsig * d.nchunks * (P.Mpad / 64);
+    if (P.n_frames <= 8) k_kd_simt<8><<<grid, 256, 0, st>>>(k);
+    else if (P.n_frames <= 16) k_kd_simt<16><<<grid, 256, 0, st>>>(k);
+    else k_kd_simt<32><<<grid, 256, 0, st>>>(k);
+  }
+  return (int)P.kd.size();
+}
+
+size_t ke_smem_bytes(const Plan& P) {
+  int maxrows = 0;
+  for (const auto& f : P.fr) maxrows = std::max(maxrows, f.nrows);
+  return (size_t)(maxrows * P.n_frames + P.n1 * P.NPT + maxrows * P.NPT) * sizeof(float);
+}
+
+int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st) {
+  const size_t sm = ke_smem_bytes(P);
+  dim3 grid(nsig, (unsigned)P.paths.size());
+  k_ke<<<grid, 256, sm, st>>>(kp);
+  return 1;
+}
+
+cudaError_t ke_set_smem(const Plan& P) {
+  return cudaFuncSetAttribute(k_ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke_smem_bytes(P));
+}
+
+void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st) {
+  k_check_finite<<<296, 256, 0, st>>>(x, n, flag);
+}
+
+}  // namespace jtfs

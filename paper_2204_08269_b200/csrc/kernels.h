@@ -1,0 +1,61 @@
+// Launch interface between the C ABI (abi.cu) and the kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "jtfs_internal.h"
+
+namespace jtfs {
+
+struct KDParams {
+  const float2* A;   // A_alpha^T [Kpad][Mpad]
+  const float2* y2;  // micro-batch Y2 base
+  const float* g;    // time pooling taps g_alpha[L]
+  float* part;       // micro-batch partials base
+  int K, Kpad, Mpad, L, D, frame0, nframes, chunk, nchunks;
+  int64_t y2_off, part_off, y2_stride, part_stride;
+};
+
+struct DevPath {
+  int32_t kind, filter, alpha_slot, beta;
+};
+struct DevFilter {
+  int32_t k, nrows, row0, rp_off;
+  int64_t w_off;
+};
+struct DevAlpha {
+  int32_t nchunks, pad;
+  int64_t part_off;
+};
+
+struct KEParams {
+  const DevPath* paths;
+  const DevFilter* filters;
+  const DevAlpha* alphas;
+  const int32_t* rprime;
+  const float* W;
+  const float2* hpsi;  // [n_beta][N_fr] psi_{beta,+1} taps
+  const float* hphiF;  // [N_fr]
+  const float* gT;     // [NPT]
+  const float* part;
+  const float* yphi;
+  float* out;
+  int64_t fps, off_s2, part_stride;
+  int n1, NPT, N_fr, lam_out, n_frames, frame0, Mpad, k_phiphi;
+};
+
+int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2* tmp, cudaStream_t st);
+int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,
+                        bool keep_u1, cudaStream_t st);
+int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int nsig, float* yphi, float* out,
+                      int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
+                      const Band* d_band_L1, cudaStream_t st);
+int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float2* y2, float2* tmp, cudaStream_t st);
+int launch_kd(const Plan& P, const float2* y2, int nsig, float* part, cudaStream_t st);
+size_t ke_smem_bytes(const Plan& P);
+int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
+cudaError_t ke_set_smem(const Plan& P);
+void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
+
+}  // namespace jtfs

@@ -1,0 +1,504 @@
+// Host-side plan generator (fp64 -> fp32 device tables) for the B200 JTFS path.
+//
+// Written from PAPER.md Sec. 2 and the readings of DESIGN.md §3
+// (SURVEY.md §8(c)); it shares no code with oracle/ (checked against it only
+// in tests, through jtfs_debug_filter and the forward output).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <map>
+#include <stdexcept>
+
+#include "jtfs_internal.h"
+
+namespace jtfs {
+
+namespace {
+constexpr double kSigma0 = 0.1;             // sigma_phi = 0.1 / T        (R4)
+constexpr double kAlphaC = 5.0;             // critical-rate support rule (R5)
+constexpr double kEpsBand = 1e-9;           // spectral band truncation (relative to peak)
+constexpr double kEpsPool = 1e-9;           // lambda-pooling row truncation (relative)
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+double xi_max(int Q) { return std::max(1.0 / (1.0 + std::pow(2.0, 3.0 / Q)), 0.35); }
+
+double sigma_ratio(int Q) {
+  const double q = std::pow(2.0, -1.0 / Q);
+  const double r = 1.0 / std::sqrt(2.0);  // neighbours cross at ~ -3 dB (R2)
+  return (1.0 - q) / (1.0 + q) / std::sqrt(2.0 * std::log(1.0 / r));
+}
+
+int dyadic_j(double xi, double sigma) {
+  const int j = (int)std::floor(-std::log2(std::min(xi + kAlphaC * sigma, 0.5))) - 1;
+  return std::max(j, 0);
+}
+
+// cos/sin of 2 pi a / b with exact integer range reduction
+std::complex<double> unit_root(int64_t a, int64_t b) {
+  a %= b;
+  if (a < 0) a += b;
+  const double th = kTwoPi * (double)a / (double)b;
+  return {std::cos(th), std::sin(th)};
+}
+
+// inverse DFT (with 1/L) of a length-L spectrum, direct O(L * nnz)
+std::vector<std::complex<double>> idft(const std::vector<std::complex<double>>& X) {
+  const int64_t L = (int64_t)X.size();
+  std::vector<std::complex<double>> x(L);
+  std::vector<int64_t> nz;
+  double mx = 0;
+  for (int64_t m = 0; m < L; ++m) mx = std::max(mx, std::abs(X[m]));
+  for (int64_t m = 0; m < L; ++m)
+    if (std::abs(X[m]) > 1e-300 && std::abs(X[m]) >= 1e-30 * mx) nz.push_back(m);
+  for (int64_t n = 0; n < L; ++n) {
+    std::complex<double> acc = 0;
+    for (int64_t m : nz) acc += X[m] * unit_root(m * n, L);
+    x[n] = acc / (double)L;
+  }
+  return x;
+}
+
+Band add_band(std::vector<float>& vals, const std::vector<double>& f) {
+  // minimal circular arc holding every bin with |f| >= eps * max|f|
+  const int L = (int)f.size();
+  double mx = 0;
+  for (double v : f) mx = std::max(mx, std::fabs(v));
+  std::vector<int> on;
+  for (int m = 0; m < L; ++m)
+    if (mx > 0 && std::fabs(f[m]) >= kEpsBand * mx) on.push_back(m);
+  Band b;
+  b.off = (int64_t)vals.size();
+  if (on.empty()) { b.m0 = 0; b.len = 0; return b; }
+  // largest circular gap between consecutive "on" bins
+  int best_gap = -1, best_after = 0;
+  for (size_t i = 0; i < on.size(); ++i) {
+    const int a = on[i], nxt = on[(i + 1) % on.size()];
+    const int gap = (i + 1 < on.size()) ? (nxt - a - 1) : (nxt + L - a - 1);
+    if (gap > best_gap) { best_gap = gap; best_after = (int)((i + 1) % on.size()); }
+  }
+  b.m0 = on[best_after];
+  b.len = L - best_gap;
+  if (b.len > L) b.len = L;
+  for (int t = 0; t < b.len; ++t) vals.push_back((float)f[(b.m0 + t) % L]);
+  return b;
+}
+}  // namespace
+
+int ilog2_exact(int64_t v) {
+  if (v < 1 || (v & (v - 1))) return -1;
+  int r = 0;
+  while ((1LL << r) < v) ++r;
+  return r;
+}
+
+Bank morlet_bank(int J, int Q) {
+  // G(J,Q) (R2): constant-Q ladder xi_i = xi_max 2^{-i/Q}, sigma_i = c xi_i while
+  // sigma_i > sigma0 / 2^J, then Q-1 linearly spaced tail filters at sigma_min.
+  Bank b;
+  const double xm = xi_max(Q), c = sigma_ratio(Q), smin = kSigma0 / std::pow(2.0, J);
+  for (int i = 0;; ++i) {
+    const double xi = xm * std::pow(2.0, -(double)i / Q);
+    const double s = c * xi;
+    if (!(s > smin)) break;
+    b.xi.push_back(xi);
+    b.sigma.push_back(s);
+  }
+  if (b.xi.empty()) throw std::runtime_error("filter bank has no constant-Q filter");
+  const double xl = b.xi.back();
+  for (int q = 1; q < Q; ++q) {
+    b.xi.push_back((double)(Q - q) / Q * xl);
+    b.sigma.push_back(smin);
+  }
+  for (size_t i = 0; i < b.xi.size(); ++i) b.j.push_back(dyadic_j(b.xi[i], b.sigma[i]));
+  return b;
+}
+
+void morlet_hat(double xi, double sigma, int L, int n_grid, double* out) {
+  // R1 + R8: Gabor on the one-sided grid w+ = m / n_grid minus kappa * Gaussian
+  // on the two-sided grid (fftfreq), kappa making psi_hat[0] exactly 0.
+  const double two_s2 = 2.0 * sigma * sigma;
+  const double kappa = std::exp(-(xi * xi) / two_s2);
+  for (int m = 0; m < L; ++m) {
+    const double wp = (double)m / n_grid;
+    const double wpm = (m < L / 2 ? (double)m : (double)(m - L)) / n_grid;
+    const double gab = (m == 0) ? kappa : std::exp(-((wp - xi) * (wp - xi)) / two_s2);
+    out[m] = gab - kappa * std::exp(-(wpm * wpm) / two_s2);
+  }
+}
+
+void gauss_hat(double sigma, int L, int n_grid, double* out) {
+  const double two_s2 = 2.0 * sigma * sigma;
+  for (int m = 0; m < L; ++m) {
+    const double wpm = (m < L / 2 ? (double)m : (double)(m - L)) / n_grid;
+    out[m] = std::exp(-(wpm * wpm) / two_s2);
+  }
+}
+
+static std::vector<double> morlet_vec(double xi, double s, int L, int n) {
+  std::vector<double> v(L);
+  morlet_hat(xi, s, L, n, v.data());
+  return v;
+}
+static std::vector<double> gauss_vec(double s, int L, int n) {
+  std::vector<double> v(L);
+  gauss_hat(s, L, n, v.data());
+  return v;
+}
+
+std::string build_plan(const jtfs_params& p, Plan& P) {
+  P.prm = p;
+  // ---- validation ----
+  const int log2N = ilog2_exact(p.N);
+  if (log2N < 4) return "N must be a power of two >= 16";
+  if (ilog2_exact(p.T) < 0 || p.T > p.N) return "T must be a power of two with T <= N";
+  if (p.J < 1 || (1LL << p.J) > p.N) return "J must satisfy 1 <= J and 2^J <= N";
+  if (p.Q < 1 || p.Q2 < 1 || p.Q_fr < 1) return "Q, Q2, Q_fr must be >= 1";
+  if (p.J_fr < 1) return "J_fr must be >= 1";
+  if (p.pad_mode != JTFS_PAD_REFLECT && p.pad_mode != JTFS_PAD_PERIODIC) return "bad pad_mode";
+  if (p.average_fr != 0 && p.average_fr != 1) return "average_fr must be 0 or 1";
+  if (p.Q > 64 || p.J > 24 || p.J_fr > 12) return "J / Q / J_fr out of supported range";
+  P.N = p.N;
+  P.T = p.T;
+  P.log2T = ilog2_exact(p.T);
+  P.F = p.F ? p.F : (1 << p.J_fr);
+  P.log2F = ilog2_exact(P.F);
+  if (P.log2F < 0) return "F must be a power of two";
+  if (p.pad_mode == JTFS_PAD_REFLECT) { P.N_pad = 2 * p.N; P.pad_left = p.N / 2; }
+  else { P.N_pad = p.N; P.pad_left = 0; }
+  if (P.N_pad > (1 << 18)) return "N_pad > 2^18 is not supported";
+  P.NPT = P.N_pad / P.T;
+  try {
+    P.b1 = morlet_bank(p.J, p.Q);
+    P.b2 = morlet_bank(p.J, p.Q2);
+    P.bf = morlet_bank(p.J_fr, p.Q_fr);
+  } catch (const std::exception& e) {
+    return e.what();
+  }
+  P.n1 = (int)P.b1.xi.size();
+  if (P.n1 < 4) return "fewer than 4 first-order filters (n1 < 4)";
+  {
+    int c = 0;
+    while ((1 << c) < P.n1) ++c;
+    P.N_fr = 1 << (c + 1);                       // 2^(ceil(log2 n1) + 1)   (R9)
+  }
+  if (P.F > P.N_fr) return "F larger than the frequential grid N_fr";
+  P.frame0 = (P.pad_left + P.T - 1) / P.T;       // U(log2 T)
+  P.n_frames = (P.N + P.T - 1) / P.T;
+  P.lam_out = p.average_fr ? (P.n1 + P.F - 1) / P.F : P.n1;
+  if (P.n_frames > 32) return "more than 32 output frames (N/T > 32) is not supported";
+
+  // ---- first order ----
+  P.k1.resize(P.n1);
+  P.L1.resize(P.n1);
+  P.u1_off.resize(P.n1);
+  P.u1_total = 0;
+  for (int l = 0; l < P.n1; ++l) {
+    P.k1[l] = std::min(P.b1.j[l], P.log2T);
+    P.L1[l] = P.N_pad >> P.k1[l];
+    P.u1_off[l] = P.u1_total;
+    P.u1_total += P.L1[l];
+    if (l > 0 && P.b1.j[l] < P.b1.j[l - 1]) return "internal: j1 not monotone";
+  }
+  auto& bv = P.bandvals;
+  bv.clear();
+  P.band_psi1.resize(P.n1);
+  for (int l = 0; l < P.n1; ++l)
+    P.band_psi1[l] = add_band(bv, morlet_vec(P.b1.xi[l], P.b1.sigma[l], P.N_pad, P.N_pad));
+  const double sigT = kSigma0 / P.T, sigF = kSigma0 / P.F;
+  P.band_phiT_pad = add_band(bv, gauss_vec(sigT, P.N_pad, P.N_pad));
+  P.band_phiT_L1.resize(P.log2T + 1);
+  for (int k = 0; k <= P.log2T; ++k)
+    P.band_phiT_L1[k] = add_band(bv, gauss_vec(sigT, P.N_pad >> k, P.N_pad));
+
+  // U1 groups by L1
+  P.u1_groups.clear();
+  for (int l = 0; l < P.n1; ++l) {
+    const int lg = ilog2_exact(P.L1[l]);
+    if (P.u1_groups.empty() || P.u1_groups.back().log2L != lg) {
+      P.u1_groups.push_back(FoldGroup{});
+      P.u1_groups.back().log2L = lg;
+    }
+    FoldRow r{};
+    r.src_off = 0;
+    r.Lsrc = P.N_pad;
+    r.m0 = P.band_psi1[l].m0;
+    r.len = P.band_psi1[l].len;
+    r.band_off = P.band_psi1[l].off;
+    r.dst_off = P.u1_off[l];
+    r.scale = (float)(1.0 / P.N_pad);
+    P.u1_groups.back().rows.push_back(r);
+  }
+
+  // ---- second order in time: active alphas, admissibility j1 < j2 (R7) ----
+  P.kd.clear();
+  P.y2_total = 0;
+  std::map<std::pair<int, int>, Band> band2;
+  for (int a = 0; a < (int)P.b2.xi.size(); ++a) {
+    int K = 0;
+    while (K < P.n1 && P.b1.j[K] < P.b2.j[a]) ++K;
+    for (int l = K; l < P.n1; ++l)
+      if (P.b1.j[l] < P.b2.j[a]) return "internal: admissible set not a prefix";
+    if (K == 0) continue;
+    AlphaKD d{};
+    d.alpha = a;
+    d.K = K;
+    d.k_alpha = std::min(P.b2.j[a], P.log2T);
+    d.L = P.N_pad >> d.k_alpha;
+    d.D = 1 << (P.log2T - d.k_alpha);
+    d.y2_off = P.y2_total;
+    P.y2_total += (int64_t)K * d.L;
+    for (int l = 0; l < K; ++l) {
+      auto key = std::make_pair(a, P.k1[l]);
+      if (!band2.count(key))
+        band2[key] = add_band(bv, morlet_vec(P.b2.xi[a], P.b2.sigma[a], P.L1[l], P.N_pad));
+    }
+    P.kd.push_back(d);
+  }
+  if (P.kd.empty()) return "no admissible second-order path";
+  // Y2 groups by L_alpha (descending)
+  P.y2_groups.clear();
+  for (const auto& d : P.kd) {
+    const int lg = ilog2_exact(d.L);
+    FoldGroup* G = nullptr;
+    for (auto& g : P.y2_groups)
+      if (g.log2L == lg) G = &g;
+    if (!G) {
+      P.y2_groups.push_back(FoldGroup{});
+      G = &P.y2_groups.back();
+      G->log2L = lg;
+    }
+    for (int l = 0; l < d.K; ++l) {
+      const Band& b = band2[std::make_pair(d.alpha, P.k1[l])];
+      FoldRow r{};
+      r.src_off = P.u1_off[l];
+      r.Lsrc = P.L1[l];
+      r.m0 = b.m0;
+      r.len = b.len;
+      r.band_off = b.off;
+      r.dst_off = d.y2_off + (int64_t)l * d.L;
+      r.scale = (float)(1.0 / P.L1[l]);
+      G->rows.push_back(r);
+    }
+  }
+
+  // ---- frequential filters and the joint-stage row set (R9, R10, R11) ----
+  const int nb = (int)P.bf.xi.size();
+  P.fr.clear();
+  auto make_filter = [&](int kind, int theta, int beta) {
+    FrFilter f{};
+    f.kind = kind;
+    f.theta = theta;
+    f.beta = beta;
+    if (kind == 0) f.k = p.average_fr ? std::min(P.bf.j[beta], P.log2F) : 0;
+    else f.k = p.average_fr ? P.log2F : 0;
+    f.R = P.N_fr >> f.k;
+    return f;
+  };
+  for (int th : {-1, +1})
+    for (int b = 0; b < nb; ++b) P.fr.push_back(make_filter(0, th, b));
+  P.fr.push_back(make_filter(1, 0, -1));
+  // retained rows and lambda-pooling matrices
+  P.W.clear();
+  P.M = 0;
+  for (auto& f : P.fr) {
+    f.rprime.clear();
+    if (p.average_fr) {
+      std::vector<std::complex<double>> ph(f.R);
+      {
+        auto gv = gauss_vec(sigF, f.R, P.N_fr);
+        for (int m = 0; m < f.R; ++m) ph[m] = gv[m];
+      }
+      auto gF = idft(ph);
+      double mx = 0;
+      for (auto& v : gF) mx = std::max(mx, std::abs(v.real()));
+      const int step = 1 << (P.log2F - f.k);
+      for (int r = 0; r < f.R; ++r) {
+        bool need = false;
+        for (int q = 0; q < P.lam_out && !need; ++q) {
+          const int d = ((q * step - r) % f.R + f.R) % f.R;
+          need = std::fabs(gF[d].real()) >= kEpsPool * mx;
+        }
+        if (need) f.rprime.push_back(r);
+      }
+      f.nrows = (int)f.rprime.size();
+      f.w_off = (int64_t)P.W.size();
+      for (int q = 0; q < P.lam_out; ++q)
+        for (int i = 0; i < f.nrows; ++i) {
+          const int d = ((q * step - f.rprime[i]) % f.R + f.R) % f.R;
+          P.W.push_back((float)gF[d].real());
+        }
+    } else {
+      for (int r = 0; r < P.n1; ++r) f.rprime.push_back(r);
+      f.nrows = P.n1;
+      f.w_off = (int64_t)P.W.size();
+      for (int q = 0; q < P.lam_out; ++q)
+        for (int i = 0; i < f.nrows; ++i) P.W.push_back(q == f.rprime[i] ? 1.f : 0.f);
+    }
+    f.row0 = P.M;
+    P.M += f.nrows;
+  }
+  P.Mpad = (P.M + 63) / 64 * 64;
+  // frequential taps h_f = IDFT_{N_fr}(f_hat) (fp64)
+  std::vector<std::vector<std::complex<double>>> htap(P.fr.size());
+  for (size_t i = 0; i < P.fr.size(); ++i) {
+    const auto& f = P.fr[i];
+    std::vector<std::complex<double>> fh(P.N_fr);
+    if (f.kind == 0) {
+      auto v = morlet_vec(P.bf.xi[f.beta], P.bf.sigma[f.beta], P.N_fr, P.N_fr);
+      for (int m = 0; m < P.N_fr; ++m)  // theta=-1: psi_hat[m]; theta=+1: psi_hat[-m] (R10)
+        fh[m] = (f.theta == -1) ? v[m] : v[(P.N_fr - m) % P.N_fr];
+    } else {
+      auto v = gauss_vec(sigF, P.N_fr, P.N_fr);
+      for (int m = 0; m < P.N_fr; ++m) fh[m] = v[m];
+    }
+    htap[i] = idft(fh);
+  }
+  // A_alpha^T [Kpad][Mpad] complex: A[row][lam] = h_f[(r' 2^k - lam) mod N_fr]
+  P.A.clear();
+  for (auto& d : P.kd) {
+    d.Kpad = (d.K + 7) / 8 * 8;
+    d.a_off = (int64_t)P.A.size() / 2;
+    const size_t base = P.A.size();
+    P.A.resize(base + (size_t)d.Kpad * P.Mpad * 2, 0.f);
+    for (size_t fi = 0; fi < P.fr.size(); ++fi) {
+      const auto& f = P.fr[fi];
+      for (int i = 0; i < f.nrows; ++i) {
+        const int row = f.row0 + i;
+        for (int l = 0; l < d.K; ++l) {
+          const int idx = (((f.rprime[i] << f.k) - l) % P.N_fr + P.N_fr) % P.N_fr;
+          const auto v = htap[fi][idx];
+          P.A[base + ((size_t)l * P.Mpad + row) * 2 + 0] = (float)v.real();
+          P.A[base + ((size_t)l * P.Mpad + row) * 2 + 1] = (float)v.imag();
+        }
+      }
+    }
+  }
+  // time pooling taps g_alpha = IDFT_L(phi_T_hat^(L)) (real, even)
+  P.g.clear();
+  for (auto& d : P.kd) {
+    d.g_off = (int64_t)P.g.size();
+    auto ph = gauss_vec(sigT, d.L, P.N_pad);
+    // band-limited real-even inverse DFT
+    std::vector<int> nz;
+    for (int m = 0; m < d.L; ++m)
+      if (ph[m] > 1e-30) nz.push_back(m);
+    for (int t = 0; t < d.L; ++t) {
+      double acc = 0;
+      for (int m : nz) acc += ph[m] * unit_root((int64_t)m * t, d.L).real();
+      P.g.push_back((float)(acc / d.L));
+    }
+    d.chunk = std::min(d.L, 4096);
+    d.nchunks = d.L / d.chunk;
+  }
+  P.part_total = 0;
+  for (auto& d : P.kd) {
+    d.part_off = P.part_total;
+    P.part_total += (int64_t)d.nchunks * P.Mpad * P.n_frames;
+  }
+  // phi_t paths: psi_{beta,+1} taps (complex), phi_F taps (real), phi_T taps at rate T (real)
+  P.hphi.clear();
+  for (int b = 0; b < nb; ++b)
+    for (int m = 0; m < P.N_fr; ++m) {
+      const auto v = htap[nb + b][m];
+      P.hphi.push_back((float)v.real());
+      P.hphi.push_back((float)v.imag());
+    }
+  for (int m = 0; m < P.N_fr; ++m) P.hphi.push_back((float)htap[2 * nb][m].real());
+  {
+    std::vector<std::complex<double>> ph(P.NPT);
+    auto gv = gauss_vec(sigT, P.NPT, P.N_pad);
+    for (int m = 0; m < P.NPT; ++m) ph[m] = gv[m];
+    auto gt = idft(ph);
+    for (int m = 0; m < P.NPT; ++m) P.hphi.push_back((float)gt[m].real());
+  }
+
+  // ---- paths (R-O11) ----
+  P.paths.clear();
+  P.path_filter.clear();
+  for (int th : {-1, +1})
+    for (const auto& d : P.kd)
+      for (int b = 0; b < nb; ++b) {
+        P.paths.push_back({JTFS_PATH_SPIN, th, d.alpha, b, P.b2.xi[d.alpha], P.bf.xi[b]});
+        P.path_filter.push_back(th == -1 ? b : nb + b);
+      }
+  for (const auto& d : P.kd) {
+    P.paths.push_back({JTFS_PATH_PSI_T_PHI_F, 0, d.alpha, -1, P.b2.xi[d.alpha], 0.0});
+    P.path_filter.push_back(2 * nb);
+  }
+  for (int b = 0; b < nb; ++b) {
+    P.paths.push_back({JTFS_PATH_PHI_T_PSI_F, 0, -1, b, 0.0, P.bf.xi[b]});
+    P.path_filter.push_back(nb + b);
+  }
+  P.paths.push_back({JTFS_PATH_PHI_T_PHI_F, 0, -1, -1, 0.0, 0.0});
+  P.path_filter.push_back(-1);
+
+  // ---- twiddles exp(-2 pi i t / N_tw) ----
+  P.N_tw = P.N_pad;
+  P.twiddle.resize((size_t)P.N_tw * 2);
+  for (int t = 0; t < P.N_tw; ++t) {
+    const auto w = unit_root(-(int64_t)t, P.N_tw);
+    P.twiddle[2 * t] = (float)w.real();
+    P.twiddle[2 * t + 1] = (float)w.imag();
+  }
+  return "";
+}
+
+WsLayout ws_layout(const Plan& p, int64_t mb) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  WsLayout w{};
+  w.xhat = al((size_t)mb * p.N_pad * 8);
+  // four-step intermediate: largest group (rows x L) among U1 / Y2 / KA
+  size_t tmp = (size_t)p.N_pad * 8;
+  for (const auto& g : p.u1_groups)
+    if (g.log2L > 12) tmp = std::max(tmp, g.rows.size() * ((size_t)8 << g.log2L));
+  for (const auto& g : p.y2_groups)
+    if (g.log2L > 12) tmp = std::max(tmp, g.rows.size() * ((size_t)8 << g.log2L));
+  w.tmp = al((size_t)mb * tmp);
+  w.u1 = al((size_t)mb * p.u1_total * 4);
+  w.u1hat = al((size_t)mb * p.u1_total * 8);
+  w.yphi = al((size_t)mb * p.n1 * p.NPT * 4);
+  w.y2 = al((size_t)mb * p.y2_total * 8);
+  w.part = al((size_t)mb * p.part_total * 4);
+  w.flag = 256;
+  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.part + w.flag;
+  return w;
+}
+
+void stage_cost(const Plan& p, double fl[6], double by[6]) {
+  auto lg = [](double L) { return std::log2(L); };
+  for (int i = 0; i < 6; ++i) fl[i] = by[i] = 0;
+  // KA: real DFT of the padded signal; reads x
+  fl[0] = 2.5 * p.N_pad * lg(p.N_pad);
+  by[0] = 4.0 * p.N;
+  // KB: per lambda band multiply, complex IDFT_L1, modulus, real DFT_L1
+  for (int l = 0; l < p.n1; ++l) {
+    const double L1 = p.L1[l];
+    fl[1] += 2.0 * p.band_psi1[l].len + 5.0 * L1 * lg(L1) + 5.0 * L1 + 2.5 * L1 * lg(L1);
+  }
+  // KS: phi_T folds + NPT-point inverse DFTs (S0, S1, Y_phi); writes S0 + S1
+  fl[2] = (double)(p.n1 + 1) * (2.0 * 12 * p.NPT + 5.0 * p.NPT * lg(std::max(p.NPT, 2)));
+  by[2] = 4.0 * p.n_frames * (1 + p.n1);
+  // KC: per admissible (alpha, lambda): band multiply + complex IDFT_{L_alpha}
+  for (const auto& g : p.y2_groups)
+    for (const auto& r : g.rows) {
+      const double L = (double)(1 << g.log2L);
+      fl[3] += 2.0 * r.len + 5.0 * L * lg(L);
+    }
+  // KD: per alpha and time column: DFT_{N_fr} along lambda, per filter multiply + IDFT_R,
+  //     then modulus + pooling on the M retained rows
+  for (const auto& d : p.kd) {
+    double col = 5.0 * p.N_fr * lg(p.N_fr);
+    for (const auto& f : p.fr) col += 2.0 * p.N_fr + 5.0 * f.R * lg(std::max(f.R, 2));
+    fl[4] += (double)d.L * col + (double)p.M * d.L * (5.0 + 2.0 * p.n_frames);
+  }
+  // KE: lambda pooling matrices + phi paths; writes S2
+  for (size_t i = 0; i < p.paths.size(); ++i) {
+    const int fi = p.path_filter[i];
+    const double rows = fi >= 0 ? p.fr[fi].nrows : p.n1;
+    fl[5] += 2.0 * p.lam_out * rows * p.n_frames;
+    if (p.paths[i].kind == JTFS_PATH_PHI_T_PSI_F) fl[5] += rows * p.NPT * (8.0 * p.n1 + 5.0 + 2.0 * p.n_frames);
+  }
+  by[5] = 4.0 * (double)p.paths.size() * p.lam_out * p.n_frames;
+}
+
+}  // namespace jtfs

@@ -1,0 +1,246 @@
+"""Thin ctypes binding of libjtfs.so (include/jtfs.h) -- argument marshalling only.
+
+Every step of the JTFS path runs in the CUDA kernels behind the C ABI; this
+module only converts Python / torch arguments to pointers and sizes.  There is
+no CPU fallback: if the library is missing, importing the binding raises.
+
+    plan = Plan(N=2**16, J=12, Q=16, J_fr=5, T=2**13, F=4)     # jtfs_plan_create
+    out = plan.forward(x)       # x: torch.cuda.FloatTensor [B, N] -> [B, floats_per_signal]
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libjtfs.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2204_08269_b200.build` "
+                      "(there is no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+# --- status codes / constants (jtfs.h) ---
+JTFS_OK, JTFS_ERR_INVALID_ARG, JTFS_ERR_UNSUPPORTED, JTFS_ERR_OOM = 0, 1, 2, 3
+JTFS_ERR_CUDA, JTFS_ERR_WORKSPACE, JTFS_ERR_NONFINITE = 4, 5, 6
+JTFS_CHECK_FINITE = 1
+JTFS_PAD_REFLECT, JTFS_PAD_PERIODIC = 0, 1
+PATH_SPIN, PATH_PSI_T_PHI_F, PATH_PHI_T_PSI_F, PATH_PHI_T_PHI_F = 0, 1, 2, 3
+
+EXPORTS = [
+    "jtfs_plan", "jtfs_plan_create", "jtfs_plan_destroy", "jtfs_layout", "jtfs_paths",
+    "jtfs_lambda_xi", "jtfs_workspace_size", "jtfs_forward", "jtfs_forward_host",
+    "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_cost", "jtfs_profile_enable",
+    "jtfs_profile_read", "jtfs_status_string", "jtfs_last_error",
+]
+STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
+
+
+class jtfs_params(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("N", "J", "Q", "Q2", "T", "J_fr", "Q_fr", "F", "average_fr", "pad_mode", "device")] + \
+               [("flags", C.c_uint32)]
+
+
+class jtfs_layout_t(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("n1", "n_frames", "frame0", "lambda_out", "n_paths", "n_alpha", "n_beta", "N_pad",
+                 "N_fr", "reserved")] + \
+               [(n, C.c_int64) for n in ("off_s0", "off_s1", "off_s2", "floats_per_signal")]
+
+
+class jtfs_path_t(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("theta", C.c_int32), ("alpha", C.c_int32), ("beta", C.c_int32),
+                ("xi_alpha", C.c_double), ("xi_beta", C.c_double)]
+
+
+_P = C.c_void_p
+_lib.jtfs_plan.argtypes = [C.c_int] * 8 + [C.POINTER(_P)]
+_lib.jtfs_plan_create.argtypes = [C.POINTER(jtfs_params), C.POINTER(_P)]
+_lib.jtfs_plan_destroy.argtypes = [_P]
+_lib.jtfs_layout.argtypes = [_P, C.POINTER(jtfs_layout_t)]
+_lib.jtfs_paths.argtypes = [_P, C.POINTER(jtfs_path_t), C.c_int32]
+_lib.jtfs_lambda_xi.argtypes = [_P, C.POINTER(C.c_double), C.c_int32]
+_lib.jtfs_workspace_size.argtypes = [_P, C.c_int64, C.POINTER(C.c_size_t)]
+_lib.jtfs_forward.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
+_lib.jtfs_forward_host.argtypes = [_P, _P, C.c_int64, _P, _P, _P, _P, C.c_size_t, _P]
+_lib.jtfs_debug_tap.argtypes = [_P, C.c_int32, _P, C.c_int64, _P, C.c_int64, _P, C.c_size_t, _P]
+_lib.jtfs_debug_tap_size.argtypes = [_P, C.c_int32, C.c_int64, C.POINTER(C.c_int64)]
+_lib.jtfs_debug_filter.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
+_lib.jtfs_cost.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32]
+_lib.jtfs_profile_enable.argtypes = [_P, C.c_int32]
+_lib.jtfs_profile_read.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32, C.c_int32]
+_lib.jtfs_status_string.argtypes = [C.c_int]
+_lib.jtfs_status_string.restype = C.c_char_p
+_lib.jtfs_last_error.argtypes = []
+_lib.jtfs_last_error.restype = C.c_char_p
+for _n in EXPORTS:
+    if _n not in ("jtfs_status_string", "jtfs_last_error"):
+        getattr(_lib, _n).restype = C.c_int
+
+
+class JTFSError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.jtfs_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {_lib.jtfs_status_string(status).decode()} ({status}): {msg}")
+
+
+def _check(status: int, where: str) -> None:
+    if status != JTFS_OK:
+        raise JTFSError(status, where)
+
+
+def library():
+    """The loaded ctypes CDLL (for symbol checks)."""
+    return _lib
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return int(torch.cuda.current_stream().cuda_stream)
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+class Plan:
+    """jtfs_plan_create / jtfs_plan_destroy and the queries of jtfs.h."""
+
+    def __init__(self, N: int, J: int, Q: int, J_fr: int, T: int, F: int = 0, Q2: int = 1,
+                 Q_fr: int = 1, average_fr: bool = True, pad_mode: int = JTFS_PAD_REFLECT,
+                 device: int | None = None, flags: int = 0):
+        if device is None:
+            import torch
+            device = torch.cuda.current_device() if torch.cuda.is_available() else -1
+        self.params = jtfs_params(N, J, Q, Q2, T, J_fr, Q_fr, F, int(bool(average_fr)), pad_mode,
+                                  device, flags)
+        h = _P()
+        _check(_lib.jtfs_plan_create(C.byref(self.params), C.byref(h)), "jtfs_plan_create")
+        self._h = h
+        lay = jtfs_layout_t()
+        _check(_lib.jtfs_layout(self._h, C.byref(lay)), "jtfs_layout")
+        self.layout = lay
+        self.device = device
+        self._ws = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.jtfs_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- queries ----
+    @property
+    def floats_per_signal(self) -> int:
+        return int(self.layout.floats_per_signal)
+
+    def paths(self):
+        n = self.layout.n_paths
+        arr = (jtfs_path_t * n)()
+        _check(_lib.jtfs_paths(self._h, arr, n), "jtfs_paths")
+        return [(p.kind, p.theta, p.alpha, p.beta, p.xi_alpha, p.xi_beta) for p in arr]
+
+    def lambda_xi(self):
+        n = self.layout.n1
+        arr = (C.c_double * n)()
+        _check(_lib.jtfs_lambda_xi(self._h, arr, n), "jtfs_lambda_xi")
+        return list(arr)
+
+    def workspace_size(self, batch: int) -> int:
+        v = C.c_size_t()
+        _check(_lib.jtfs_workspace_size(self._h, batch, C.byref(v)), "jtfs_workspace_size")
+        return int(v.value)
+
+    def debug_filter(self, bank: int, idx: int, L: int, n_grid: int):
+        arr = (C.c_double * L)()
+        _check(_lib.jtfs_debug_filter(self._h, bank, idx, L, n_grid, arr), "jtfs_debug_filter")
+        return list(arr)
+
+    def cost(self):
+        """{stage: (algorithmic flops, bytes)} per signal (jtfs_cost)."""
+        f = (C.c_double * 6)()
+        b = (C.c_double * 6)()
+        _check(_lib.jtfs_cost(self._h, f, b, 6), "jtfs_cost")
+        return {STAGES[i]: (f[i], b[i]) for i in range(6)}
+
+    # ---- tracing ----
+    def profile_enable(self, on: bool = True):
+        _check(_lib.jtfs_profile_enable(self._h, int(on)), "jtfs_profile_enable")
+
+    def profile_read(self, reset: bool = True):
+        """{stage: (ms, launches)} since the last reset (synchronises on the events)."""
+        ms = (C.c_double * 6)()
+        nl = (C.c_int64 * 6)()
+        _check(_lib.jtfs_profile_read(self._h, ms, nl, 6, int(reset)), "jtfs_profile_read")
+        return {STAGES[i]: (ms[i], nl[i]) for i in range(6)}
+
+    # ---- compute (torch tensors on the plan's device) ----
+    def workspace(self, batch: int):
+        import torch
+        need = self.workspace_size(batch)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def forward(self, x, out=None, stream=None):
+        """x: float32 CUDA tensor [B, N] (contiguous) -> out [B, floats_per_signal]."""
+        import torch
+        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+        B = x.shape[0]
+        if out is None:
+            out = torch.empty(B, self.floats_per_signal, dtype=torch.float32, device=x.device)
+        ws = self.workspace(B)
+        _check(_lib.jtfs_forward(self._h, _ptr(x), B, _ptr(out), _ptr(ws), ws.numel(),
+                                 _stream_handle(stream)), "jtfs_forward")
+        return out
+
+    def forward_host(self, x_host, out_host, x_dev, out_dev, stream=None):
+        """End to end through the C ABI with HOST buffers (pinned torch CPU tensors)."""
+        B = x_host.shape[0]
+        ws = self.workspace(B)
+        _check(_lib.jtfs_forward_host(self._h, _ptr(x_host), B, _ptr(out_host), _ptr(x_dev), _ptr(out_dev),
+                                      _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_forward_host")
+        return out_host
+
+    def debug_tap(self, tap: int, x):
+        import torch
+        B = x.shape[0]
+        n = C.c_int64()
+        _check(_lib.jtfs_debug_tap_size(self._h, tap, B, C.byref(n)), "jtfs_debug_tap_size")
+        out = torch.empty(int(n.value), dtype=torch.float32, device=x.device)
+        ws = self.workspace(B)
+        _check(_lib.jtfs_debug_tap(self._h, tap, _ptr(x), B, _ptr(out), out.numel(), _ptr(ws), ws.numel(),
+                                   _stream_handle(None)), "jtfs_debug_tap")
+        return out
+
+    # ---- unpack the out_3D record ----
+    def unpack(self, out):
+        L = self.layout
+        fr = L.n_frames
+        s0 = out[..., L.off_s0:L.off_s0 + fr]
+        s1 = out[..., L.off_s1:L.off_s2].reshape(*out.shape[:-1], L.n1, fr)
+        s2 = out[..., L.off_s2:].reshape(*out.shape[:-1], L.n_paths, L.lambda_out, fr)
+        return s0, s1, s2
+
+
+def jtfs_plan(N, J, Q, J_fr, Q_fr, T, F, flags=0) -> Plan:
+    """North-star form of jtfs.h's jtfs_plan (Q2 = 1, Eq. (3), reflect padding)."""
+    return Plan(N=N, J=J, Q=Q, J_fr=J_fr, T=T, F=F, Q_fr=Q_fr, flags=flags)
+
+
+def jtfs_forward(plan: Plan, x_batch, out=None, stream=None):
+    """jtfs_forward(plan, x_batch, out) of jtfs.h."""
+    return plan.forward(x_batch, out=out, stream=stream)

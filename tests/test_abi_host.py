@@ -1,0 +1,116 @@
+"""CPU tests of the C-ABI library (no GPU): it loads, exports every symbol jtfs.h
+declares, validates parameters, and its host-side plan (schedule, layout, path
+order, filter generator) agrees with the independent oracle.  No compute calls."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import jtfs_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def jt():
+    from paper_2204_08269_b200 import build
+    build.build()
+    from paper_2204_08269_b200 import jtfs
+    return jtfs
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "jtfs.h")).read()
+    return sorted(set(re.findall(r"^JTFS_API\s+(?:jtfs_status|const char\*)\s+(jtfs_\w+)\s*\(", src, re.M)))
+
+
+def test_exports_every_declared_symbol(jt):
+    lib = jt.library()
+    decl = _header_symbols()
+    assert len(decl) >= 12
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert sorted(jt.EXPORTS) == decl
+
+
+def hostplan(jt, **kw):
+    return jt.Plan(device=-1, **kw)
+
+
+CFGS = {
+    "c1": dict(N=2 ** 10, J=6, Q=8, J_fr=3, T=2 ** 6, F=8),
+    "c2": dict(N=2 ** 13, J=8, Q=16, J_fr=4, T=2 ** 13, F=16, average_fr=False),
+    "c3": dict(N=2 ** 16, J=12, Q=16, J_fr=5, T=2 ** 13, F=4),
+    "c4": dict(N=2 ** 17, J=13, Q=16, J_fr=5, T=2 ** 13, F=4),
+    "p42": dict(N=2 ** 16, J=13, Q=16, J_fr=6, T=2 ** 11, F=4),
+}
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+def test_layout_and_paths_match_oracle(jt, name):
+    kw = CFGS[name]
+    p = hostplan(jt, **kw)
+    s = O.schedule(O.Params(**kw))
+    L = p.layout
+    assert (L.n1, L.n_frames, L.frame0, L.lambda_out, L.n_paths, L.N_pad, L.N_fr) == \
+        (s.n1, s.n_frames, s.frame0, s.lam_out, len(s.paths), s.N_pad, s.N_fr)
+    assert L.floats_per_signal == O.unpack_layout(s)["total"]
+    assert [(k, th, a, b) for (k, th, a, b, _, _) in p.paths()] == list(s.paths)
+    np.testing.assert_allclose(p.lambda_xi(), s.xi1, rtol=1e-15)
+
+
+def test_paper_44_by_32(jt):
+    L = hostplan(jt, **CFGS["p42"]).layout
+    assert (L.lambda_out, L.n_frames) == (44, 32)
+
+
+@pytest.mark.parametrize("bank", [1, 2, 3, 4, 5])
+def test_plan_filters_equal_oracle_filters(jt, bank):
+    kw = CFGS["c1"]
+    p = hostplan(jt, **kw)
+    s = O.schedule(O.Params(**kw))
+    grids = [(s.N_pad, s.N_pad), (s.N_pad // 8, s.N_pad), (s.N_fr, s.N_fr)]
+    if bank in (1, 2, 3):
+        xi, sg = {1: (s.xi1, s.sigma1), 2: (s.xi2, s.sigma2), 3: (s.xif, s.sigmaf)}[bank]
+        for i in range(len(xi)):
+            for L, n in grids:
+                a = np.array(p.debug_filter(bank, i, L, n))
+                b = O.morlet_hat(xi[i], sg[i], L, n)
+                np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-300)
+                assert a[0] == 0.0
+    else:
+        sig = s.sigma_T if bank == 4 else s.sigma_F
+        for L, n in grids:
+            np.testing.assert_allclose(p.debug_filter(bank, 0, L, n), O.gauss_hat(sig, L, n), rtol=1e-13)
+
+
+@pytest.mark.parametrize("bad", [
+    dict(N=1000, J=6, Q=8, J_fr=3, T=64),          # N not pow2
+    dict(N=1024, J=11, Q=8, J_fr=3, T=64),         # 2^J > N
+    dict(N=1024, J=6, Q=8, J_fr=3, T=2048),        # T > N
+    dict(N=1024, J=6, Q=8, J_fr=3, T=63),          # T not pow2
+    dict(N=1024, J=6, Q=0, J_fr=3, T=64),          # Q < 1
+    dict(N=1024, J=6, Q=8, J_fr=3, T=64, F=3),     # F not pow2
+    dict(N=1024, J=6, Q=8, J_fr=0, T=64),          # J_fr < 1
+    dict(N=1024, J=1, Q=1, J_fr=3, T=64),          # n1 < 4
+    dict(N=1024, J=6, Q=8, J_fr=3, T=64, F=1024),  # F > N_fr
+])
+def test_invalid_params_rejected(jt, bad):
+    with pytest.raises(jt.JTFSError) as e:
+        hostplan(jt, **bad)
+    assert e.value.status == jt.JTFS_ERR_INVALID_ARG
+    assert jt.library().jtfs_last_error()
+
+
+def test_host_plan_refuses_forward_and_destroy_null(jt):
+    import ctypes as C
+    lib = jt.library()
+    assert lib.jtfs_plan_destroy(None) == 0
+    p = hostplan(jt, **CFGS["c1"])
+    st = lib.jtfs_forward(p.handle, None, 0, None, None, 0, None)
+    assert st == jt.JTFS_ERR_UNSUPPORTED    # host-only plans refuse every forward
+    st = lib.jtfs_forward(p.handle, C.c_void_p(16), 1, C.c_void_p(16), C.c_void_p(256), 1 << 30, None)
+    assert st == jt.JTFS_ERR_UNSUPPORTED
+    assert p.workspace_size(8) > 0
+    p.close()

@@ -1,0 +1,175 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Intermediate taps (X_hat, U1, Y2, Y_phi) and the full out_3D record, on seeded
+synthetic inputs shaped like the paper's workloads: AM/FM chirps
+(Eq. (5)), notes, white noise; Eq. (3) and Eq. (4); reflect and periodic
+padding; ragged batches; determinism.  Bar: per-path relative L2 <= 1e-4
+(tests/parity.py).
+"""
+import numpy as np
+import pytest
+
+from oracle import jtfs_oracle as O
+from paper_2204_08269_b200 import signals
+
+from .parity import TOL, path_blocks, path_errors
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def jt():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test run without a visible CUDA device")
+    from paper_2204_08269_b200 import build
+    build.build()
+    from paper_2204_08269_b200 import jtfs
+    return jtfs
+
+
+def _run(jt, kw, X):
+    import torch
+    plan = jt.Plan(**kw)
+    x = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float32)).cuda()
+    out = plan.forward(x)
+    torch.cuda.synchronize()
+    return plan, out
+
+
+def _check_signal(plan, out_row, x64, prm, paths=None, tol=TOL):
+    s = O.schedule(prm)
+    ref = O.jtfs_forward(x64, prm, paths=paths, s=s)
+    s0, s1, s2 = plan.unpack(out_row.cpu().numpy().astype(np.float64))
+    g = path_blocks(s0, s1, s2)
+    o = path_blocks(ref["S0"], ref["S1"], ref["S2"])
+    n_first = 1 + s.n1
+    sel = list(range(n_first)) + [n_first + p for p in (paths if paths is not None else range(len(s.paths)))]
+    e = path_errors(g, o, sel)
+    assert e.max() <= tol, (float(e.max()), int(np.argmax(e)), sel[int(np.argmax(e))])
+    return e
+
+
+C1 = dict(N=2 ** 10, J=6, Q=8, J_fr=3, T=2 ** 6, F=8)
+
+
+def _c1_inputs():
+    up = signals.am_chirp(2 ** 10, 1024.0, 64.0, 8.0, 2.0)
+    return np.stack([up, up[::-1].copy(), signals.white(1, 2 ** 10, seed=5)[0],
+                     signals.am_chirp(2 ** 10, 1024.0, 200.0, 30.0, -1.0)])
+
+
+def test_tap_xhat_and_scalogram(jt):
+    import torch
+    prm = O.Params(**C1)
+    s = O.schedule(prm)
+    X = _c1_inputs()
+    plan = jt.Plan(**C1)
+    x = torch.from_numpy(X).cuda()
+    xh = plan.debug_tap(0, x).cpu().numpy().view(np.complex64).reshape(len(X), s.N_pad)
+    u1 = plan.debug_tap(1, x).cpu().numpy().reshape(len(X), -1)
+    y2 = plan.debug_tap(2, x).cpu().numpy().view(np.complex64).reshape(len(X), -1)
+    yp = plan.debug_tap(3, x).cpu().numpy().reshape(len(X), s.n1, -1)
+    for b in range(len(X)):
+        x64 = X[b].astype(np.float64)
+        ref = np.fft.fft(O.pad_signal(x64, s))
+        assert np.abs(xh[b] - ref).max() <= 1e-5 * np.abs(ref).max()
+        S0, S1, Yphi, U1hat, Y2 = O.first_order(x64, s)
+        off = 0
+        for lam in range(s.n1):
+            r = np.fft.ifft(U1hat[lam]).real
+            g = u1[b, off:off + len(r)]
+            assert np.linalg.norm(g - r) <= 1e-5 * max(np.linalg.norm(r), 1e-3 * np.abs(u1[b]).max()), lam
+            off += len(r)
+        off = 0
+        for a in s.alphas:
+            ref2 = Y2[a]
+            g2 = y2[b, off:off + ref2.size].reshape(ref2.shape)
+            assert np.linalg.norm(g2 - ref2) <= 2e-5 * np.linalg.norm(ref2) + 1e-9, a
+            off += ref2.size
+        assert np.abs(yp[b] - Yphi).max() <= 1e-5 * np.abs(Yphi).max()
+
+
+@pytest.mark.parametrize("variant", ["eq3", "eq4", "periodic", "periodic_eq4"])
+def test_c1_full_parity(jt, variant):
+    kw = dict(C1)
+    if "eq4" in variant:
+        kw["average_fr"] = False
+    if "periodic" in variant:
+        kw["pad_mode"] = jt.JTFS_PAD_PERIODIC
+    prm = O.Params(**{k: v for k, v in kw.items() if k != "pad_mode"},
+                   pad="periodic" if "periodic" in variant else "reflect")
+    X = _c1_inputs()
+    plan, out = _run(jt, kw, X)
+    for b in range(len(X)):
+        _check_signal(plan, out[b], X[b].astype(np.float64), prm)
+
+
+def test_c1_spin_selectivity_on_gpu(jt):
+    # Fig. 1: theta=-1 energy dominates for the up-chirp, theta=+1 for the reversal
+    X = _c1_inputs()[:2]
+    plan, out = _run(jt, C1, X)
+    _, _, s2 = plan.unpack(out.cpu().numpy().astype(np.float64))
+    paths = plan.paths()
+    e = np.zeros((2, 2))
+    for i, (k, th, *_r) in enumerate(paths):
+        if k == jt.PATH_SPIN:
+            e[:, (th + 1) // 2] += (s2[:, i] ** 2).sum(axis=(1, 2))
+    assert e[0, 0] / e[0, 1] > 2.0 and e[1, 0] / e[1, 1] < 0.5
+
+
+def test_c2_chirp_grid_parity(jt):
+    kw = dict(N=2 ** 13, J=8, Q=16, J_fr=4, T=2 ** 13, F=16, average_fr=False)
+    prm = O.Params(**kw)
+    _, sig = signals.chirp_grid(n=4)   # corners + interior of the 16^3 ranges
+    X = sig[[0, 21, 42, 63]]
+    plan, out = _run(jt, kw, X)
+    for b in range(len(X)):
+        _check_signal(plan, out[b], X[b].astype(np.float64), prm)
+
+
+def test_c3_full_size_sampled_paths(jt):
+    # BASELINE config c3 (N=2^16, J=12, Q=16, J_fr=5, T=2^13, F=4) in bench's launch
+    # configuration; oracle on a sample of paths of two notes.
+    kw = dict(N=2 ** 16, J=12, Q=16, J_fr=5, T=2 ** 13, F=4)
+    prm = O.Params(**kw)
+    X = signals.notes(3, seed0=1000)
+    plan, out = _run(jt, kw, X)
+    s = O.schedule(prm)
+    P = len(s.paths)
+    sample = sorted({0, 5, 59, 60, 61, 119, P - 17, P - 8, P - 7, P - 2, P - 1})
+    for b in (0, 2):
+        O.set_workers(8)
+        _check_signal(plan, out[b], X[b].astype(np.float64), prm, paths=sample)
+
+
+def test_determinism_and_batch_independence(jt):
+    import torch
+    X = np.concatenate([_c1_inputs(), signals.white(37, 2 ** 10, seed=9)])
+    plan = jt.Plan(**C1)
+    x = torch.from_numpy(X).cuda()
+    a = plan.forward(x).cpu().numpy()
+    b = plan.forward(x).cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    c = plan.forward(x[3:4].contiguous()).cpu().numpy()
+    assert np.array_equal(a[3:4].view(np.uint32), c.view(np.uint32))
+
+
+def test_edge_cases(jt):
+    import torch
+    plan = jt.Plan(**C1)
+    x = torch.zeros(0, C1["N"], device="cuda")
+    assert plan.forward(x).shape == (0, plan.floats_per_signal)
+    z = plan.forward(torch.zeros(2, C1["N"], device="cuda"))
+    assert torch.count_nonzero(z).item() == 0                   # zero -> zero
+    pf = jt.Plan(**C1, flags=jt.JTFS_CHECK_FINITE)
+    xb = torch.zeros(1, C1["N"], device="cuda")
+    xb[0, 7] = float("nan")
+    with pytest.raises(jt.JTFSError) as e:
+        pf.forward(xb)
+    assert e.value.status == jt.JTFS_ERR_NONFINITE
+    lib = jt.library()
+    out = torch.empty(1, plan.floats_per_signal, device="cuda")
+    ws = torch.empty(plan.workspace_size(1), dtype=torch.uint8, device="cuda")
+    st = lib.jtfs_forward(plan.handle, xb.data_ptr(), 1, out.data_ptr(), ws.data_ptr(), 64, None)
+    assert st == jt.JTFS_ERR_WORKSPACE
