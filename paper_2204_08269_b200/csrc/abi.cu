@@ -69,6 +69,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   UP(P.d_W, P.W.data(), P.W.size() * 4);
   UP(P.d_hphi, P.hphi.data(), P.hphi.size() * 4);
   UP(P.d_twiddle, P.twiddle.data(), P.twiddle.size() * 4);
+  UP(P.d_twiddle64, P.twiddle64.data(), P.twiddle64.size() * 8);
   for (auto& g : P.u1_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
   for (auto& g : P.y2_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
   UP(P.d_u1_off, P.u1_off.data(), P.u1_off.size() * 8);

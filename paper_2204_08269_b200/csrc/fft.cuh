@@ -1,10 +1,11 @@
-// Shared-memory Stockham FFT for sm_100a (radix-8 passes + one radix-2/4 pass).
+// Shared-memory Stockham FFT for sm_100a (radix-8 passes + one radix-2/4 pass),
+// generic over the complex type CT = float2 (fp32) or double2 (fp64).
 //
-// G rows of length L = 2^LOG2L live contiguously in shared memory; NT threads
-// run each pass: every thread loads its butterflies' inputs into registers,
-// barrier, twiddle + in-register radix-R DFT, then stores to the Stockham
-// output positions, barrier.  (One buffer, in place: reads and writes of a
-// pass are separated by the barrier.)  Twiddles come from a fp32 table
+// G rows of length L = 2^LOG2L live in shared memory at s[g*LS + e] (LS >= L is
+// the row stride; LS = L + 1 breaks the bank conflicts of column gathers).  NT
+// threads run each pass: every thread loads its butterflies' inputs into
+// registers, barrier, twiddle + in-register radix-R DFT, store to the Stockham
+// output positions, barrier (one buffer, in place).  Twiddles come from a table
 // W[t] = exp(-2 pi i t / N_tw) built in fp64 on the host.
 // DIR = -1: forward DFT  sum_n x[n] e^{-2 pi i k n / L};  DIR = +1: unnormalised inverse.
 #pragma once
@@ -13,52 +14,57 @@
 namespace jtfs {
 namespace dev {
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+template <class CT> struct CxT;
+template <> struct CxT<float2> {
+  using R = float;
+  __device__ static __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+};
+template <> struct CxT<double2> {
+  using R = double;
+  __device__ static __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+};
+
+template <class CT>
+__device__ __forceinline__ CT cadd(CT a, CT b) { return CxT<CT>::make(a.x + b.x, a.y + b.y); }
+template <class CT>
+__device__ __forceinline__ CT csub(CT a, CT b) { return CxT<CT>::make(a.x - b.x, a.y - b.y); }
+template <class CT>
+__device__ __forceinline__ CT cmul(CT a, CT b) {
+  return CxT<CT>::make(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
-template <int DIR>
-__device__ __forceinline__ float2 twiddle(const float2* __restrict__ W, int u) {
-  const float2 w = __ldg(W + u);
-  return DIR < 0 ? w : make_float2(w.x, -w.y);
+template <int DIR, class CT>
+__device__ __forceinline__ CT twiddle(const CT* __restrict__ W, int u) {
+  const CT w = __ldg(W + u);
+  return DIR < 0 ? w : CxT<CT>::make(w.x, -w.y);
 }
 
-// cos / sin of 2 pi j / 16, j in [0, 8)
-__device__ __forceinline__ float c16(int j) {
+// cos(2 pi j / 16), j in [0, 8]
+__device__ __forceinline__ double c16(int j) {
   switch (j) {
-    case 0: return 1.0f;
-    case 1: return 0.92387953251128674f;
-    case 2: return 0.70710678118654752f;
-    case 3: return 0.38268343236508977f;
-    case 4: return 0.0f;
-    case 5: return -0.38268343236508977f;
-    case 6: return -0.70710678118654752f;
-    default: return -0.92387953251128674f;
-  }
-}
-__device__ __forceinline__ float s16(int j) {
-  switch (j) {
-    case 0: return 0.0f;
-    case 1: return 0.38268343236508977f;
-    case 2: return 0.70710678118654752f;
-    case 3: return 0.92387953251128674f;
-    case 4: return 1.0f;
-    case 5: return 0.92387953251128674f;
-    case 6: return 0.70710678118654752f;
-    default: return 0.38268343236508977f;
+    case 0: return 1.0;
+    case 1: return 0.92387953251128675613;
+    case 2: return 0.70710678118654752440;
+    case 3: return 0.38268343236508977173;
+    case 4: return 0.0;
+    case 5: return -0.38268343236508977173;
+    case 6: return -0.70710678118654752440;
+    case 7: return -0.92387953251128675613;
+    default: return -1.0;
   }
 }
 
-// multiply by exp(DIR * 2 pi i j / 16) with j a compile-time constant after unrolling
-template <int DIR>
-__device__ __forceinline__ float2 rot16(float2 a, int j) {
+// multiply by exp(DIR * 2 pi i j / 16), j in [0, 8) a compile-time constant after
+// unrolling; sin(2 pi j / 16) = cos(2 pi |j - 4| / 16)
+template <int DIR, class CT>
+__device__ __forceinline__ CT rot16(CT a, int j) {
+  using R = typename CxT<CT>::R;
   if (j == 0) return a;
-  if (j == 4) return DIR < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
-  const float c = c16(j), s = DIR * s16(j);
-  return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+  if (j == 4) return DIR < 0 ? CxT<CT>::make(a.y, -a.x) : CxT<CT>::make(-a.y, a.x);
+  const R c = (R)c16(j);
+  const R s = (R)(DIR * c16(j < 4 ? 4 - j : j - 4));
+  return CxT<CT>::make(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
 }
 
 __host__ __device__ constexpr int bitrev(int v, int bits) {
@@ -70,33 +76,31 @@ __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c
 
 // In-register R-point DFT (R = 2, 4, 8, 16): radix-2 decimation in frequency,
 // then the bit-reversal permutation so that v[r] = X[r] on exit.
-template <int R, int DIR>
-__device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+template <int R, int DIR, class CT>
+__device__ __forceinline__ void dft_reg(CT (&v)[R]) {
 #pragma unroll
   for (int span = R / 2; span >= 1; span >>= 1) {
 #pragma unroll
     for (int start = 0; start < R; start += 2 * span) {
 #pragma unroll
       for (int k = 0; k < span; ++k) {
-        const float2 a = v[start + k], b = v[start + k + span];
+        const CT a = v[start + k], b = v[start + k + span];
         v[start + k] = cadd(a, b);
         v[start + k + span] = rot16<DIR>(csub(a, b), k * (16 / (2 * span)));
       }
     }
   }
   constexpr int bits = ilog2c(R);
-  float2 t[R];
+  CT t[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) t[r] = v[bitrev(r, bits)];
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = t[r];
 }
 
-// One Stockham pass of radix R over G rows of length L held in smem s[g*LS + e]
-// (LS >= L is the row stride; LS = L + 1 breaks bank conflicts of column gathers).
-template <int LOG2L, int R, int G, int NT, int DIR, int LS>
-__device__ __forceinline__ void stockham_pass(float2* s, int log2Ns, const float2* __restrict__ W,
-                                              int log2Ntw) {
+// One Stockham pass of radix R over G rows of length L held in smem s[g*LS + e].
+template <int LOG2L, int R, int G, int NT, int DIR, int LS, class CT>
+__device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* __restrict__ W, int log2Ntw) {
   constexpr int L = 1 << LOG2L;
   constexpr int LR = L / R;
   constexpr int NBF = G * LR;
@@ -104,7 +108,7 @@ __device__ __forceinline__ void stockham_pass(float2* s, int log2Ns, const float
   constexpr int LOG2R = ilog2c(R);
   const int Ns = 1 << log2Ns;
   const int twshift = log2Ntw - (log2Ns + LOG2R);
-  float2 v[BPT][R];
+  CT v[BPT][R];
   int base[BPT];
 #pragma unroll
   for (int i = 0; i < BPT; ++i) {
@@ -112,7 +116,7 @@ __device__ __forceinline__ void stockham_pass(float2* s, int log2Ns, const float
     base[i] = -1;
     if ((NBF % NT == 0) || bf < NBF) {
       const int g = bf / LR, j = bf % LR;
-      const float2* row = s + g * LS;
+      const CT* row = s + g * LS;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[i][r] = row[j + r * LR];
       const int k = j & (Ns - 1);
@@ -136,8 +140,8 @@ __device__ __forceinline__ void stockham_pass(float2* s, int log2Ns, const float
 }
 
 // Full FFT of G rows in smem (caller has __syncthreads()'d after filling s).
-template <int LOG2L, int G, int NT, int DIR, int LS = (1 << LOG2L)>
-__device__ __forceinline__ void fft_smem(float2* s, const float2* __restrict__ W, int log2Ntw) {
+template <int LOG2L, int G, int NT, int DIR, int LS = (1 << LOG2L), class CT>
+__device__ __forceinline__ void fft_smem(CT* s, const CT* __restrict__ W, int log2Ntw) {
   constexpr int REM = LOG2L % 3;
   int log2Ns = 0;
   if constexpr (REM != 0) {

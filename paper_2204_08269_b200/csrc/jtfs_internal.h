@@ -103,6 +103,7 @@ struct Plan {
   std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
                                          // then [N_fr] real phi_F taps, then [NPT] real phi_T taps
   std::vector<float> twiddle;            // complex exp(-2 pi i t / N_tw), t < N_tw
+  std::vector<double> twiddle64;         // the same in fp64 (KA)
   int N_tw = 0;
 
   // ---- device copies ----
@@ -113,6 +114,7 @@ struct Plan {
   float* d_W = nullptr;
   float* d_hphi = nullptr;
   float* d_twiddle = nullptr;
+  double* d_twiddle64 = nullptr;
   void* d_alphas = nullptr;    // DevAlpha[n_alpha]
   void* d_fr = nullptr;        // DevFilter[n_filters]
   int32_t* d_rprime = nullptr; // concatenated retained rows of every filter

@@ -44,22 +44,26 @@ __device__ __forceinline__ float2 fold_value(const float2* __restrict__ src, con
 // ---------------------------------------------------------------------------------
 // problems: load(rho, i) -> element i of input row rho; store(rho, o, v)
 // ---------------------------------------------------------------------------------
-struct ProbPad {  // KA: x_pad[b][i] = x[b][reflect(i - pad_left)]
+struct ProbPad {  // KA (fp64): x_pad[b][i] = x[b][reflect(i - pad_left)]; X_hat rounded per bin
+  using CT = double2;
   const float* x;
   float2* xhat;
   int N, N_pad, pad_left, periodic;
-  __device__ float2 load(int b, int i) const {
+  __device__ double2 load(int b, int i) const {
     int n = i - pad_left;
     if (!periodic) {
       if (n < 0) n = -n;
       if (n >= N) n = 2 * (N - 1) - n;
     }
-    return make_float2(__ldg(x + (int64_t)b * N + n), 0.f);
+    return make_double2((double)__ldg(x + (int64_t)b * N + n), 0.0);
   }
-  __device__ void store(int b, int o, float2 v) const { xhat[(int64_t)b * N_pad + o] = v; }
+  __device__ void store(int b, int o, double2 v) const {
+    xhat[(int64_t)b * N_pad + o] = make_float2((float)v.x, (float)v.y);
+  }
 };
 
 struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
+  using CT = float2;
   const float2* src;
   int64_t src_stride;
   const FoldRow* rows;
@@ -86,6 +90,7 @@ struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
 };
 
 struct ProbRealFwd {  // U1 (real) -> U1hat
+  using CT = float2;
   const float* u1;
   float2* u1hat;
   int64_t stride;
@@ -105,14 +110,16 @@ struct ProbRealFwd {  // U1 (real) -> U1hat
 // single-CTA FFT of G rows per block
 // ---------------------------------------------------------------------------------
 template <int LOG2L, int G, int NT, int DIR, class P>
-__global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const float2* __restrict__ W,
+__global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typename P::CT* __restrict__ W,
                                                  int log2Ntw) {
+  using CT = typename P::CT;
   constexpr int L = 1 << LOG2L;
-  extern __shared__ float2 smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* smem = reinterpret_cast<CT*>(smem_raw);
   const int rho0 = blockIdx.x * G;
   for (int idx = threadIdx.x; idx < G * L; idx += NT) {
     const int g = idx / L, e = idx % L;
-    smem[idx] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+    smem[idx] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : CxT<CT>::make(0, 0);
   }
   __syncthreads();
   fft_smem<LOG2L, G, NT, DIR>(smem, W, log2Ntw);
@@ -128,7 +135,8 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
                                                  float* __restrict__ u1dbg, int nrows,
                                                  const float2* __restrict__ W, int log2Ntw) {
   constexpr int L = 1 << LOG2L;
-  extern __shared__ float2 smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* smem = reinterpret_cast<float2*>(smem_raw);
   const int rho0 = blockIdx.x * G;
   for (int idx = threadIdx.x; idx < G * L; idx += NT) {
     const int g = idx / L, e = idx % L;
@@ -170,11 +178,13 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
 // twiddle W_L^{ka nb};  step B: row FFTs (length Lb) -> X[ka + La kb]
 // ---------------------------------------------------------------------------------
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
-__global__ void __launch_bounds__(NT) k_fft4_a(P prob, float2* __restrict__ tmp,
-                                               const float2* __restrict__ W, int log2Ntw) {
+__global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restrict__ tmp,
+                                               const typename P::CT* __restrict__ W, int log2Ntw) {
+  using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
   constexpr int LS = La + 1;
-  extern __shared__ float2 smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* smem = reinterpret_cast<CT*>(smem_raw);
   constexpr int CPB = Lb / G;  // column groups per big row
   const int rho = blockIdx.x / CPB;
   const int nb0 = (blockIdx.x % CPB) * G;
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, float2* __restrict__ tmp,
   }
   __syncthreads();
   fft_smem<LOG2A, G, NT, DIR, LS>(smem, W, log2Ntw);
-  float2* out = tmp + (int64_t)rho * L;
+  CT* out = tmp + (int64_t)rho * L;
   for (int idx = threadIdx.x; idx < G * La; idx += NT) {
     const int g = idx % G, ka = idx / G;
     const int u = (ka * (nb0 + g)) << (log2Ntw - (LOG2A + LOG2B));
@@ -193,15 +203,17 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, float2* __restrict__ tmp,
 }
 
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
-__global__ void __launch_bounds__(NT) k_fft4_b(P prob, const float2* __restrict__ tmp,
-                                               const float2* __restrict__ W, int log2Ntw) {
+__global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __restrict__ tmp,
+                                               const typename P::CT* __restrict__ W, int log2Ntw) {
+  using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
   constexpr int LS = Lb + 1;
-  extern __shared__ float2 smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CT* smem = reinterpret_cast<CT*>(smem_raw);
   constexpr int RPB = La / G;
   const int rho = blockIdx.x / RPB;
   const int ka0 = (blockIdx.x % RPB) * G;
-  const float2* in = tmp + (int64_t)rho * L;
+  const CT* in = tmp + (int64_t)rho * L;
   for (int idx = threadIdx.x; idx < G * Lb; idx += NT) {
     const int g = idx / Lb, e = idx % Lb;
     smem[g * LS + e] = in[(ka0 + g) * Lb + e];
@@ -513,11 +525,11 @@ template <int LOG2L>
 constexpr int rows_NT() { return (rows_G<LOG2L>() << LOG2L) / 8 < 32 ? 32 : (rows_G<LOG2L>() << LOG2L) / 8; }
 
 template <int LOG2L, int DIR, class P>
-void launch_rows(const P& prob, int nrows, const float2* W, int log2Ntw, cudaStream_t st) {
+void launch_rows(const P& prob, int nrows, const typename P::CT* W, int log2Ntw, cudaStream_t st) {
   constexpr int G = rows_G<LOG2L>();
   constexpr int NT = rows_NT<LOG2L>();
   const int grid = (nrows + G - 1) / G;
-  const size_t sm = (size_t)G * (1 << LOG2L) * sizeof(float2);
+  const size_t sm = (size_t)G * (1 << LOG2L) * sizeof(typename P::CT);
   k_fft_rows<LOG2L, G, NT, DIR, P><<<grid, NT, sm, st>>>(prob, nrows, W, log2Ntw);
 }
 
@@ -532,16 +544,19 @@ void launch_u1_fused(const ProbFold& prob, float2* u1hat, float* u1dbg, int nrow
 }
 
 template <int LOG2L, int DIR, class PA, class PB>
-void launch_fft4(const PA& pa, const PB& pb, int nbig, float2* tmp, const float2* W, int log2Ntw,
-                 cudaStream_t st) {
+void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, const typename PA::CT* W,
+                 int log2Ntw, cudaStream_t st) {
+  using CT = typename PA::CT;
+  constexpr int ELEMS = sizeof(CT) == 8 ? 4096 : 2048;  // 32 KiB of smem per CTA
   constexpr int LOG2A = (LOG2L + 1) / 2, LOG2B = LOG2L / 2;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B;
-  constexpr int GA = 4096 / La, GB = 4096 / Lb;
-  constexpr int NT = 512;
+  constexpr int GA = ELEMS / La, GB = ELEMS / Lb;
+  constexpr int NT = ELEMS / 8;
+  static_assert(GA >= 1 && GB >= 1 && GA <= Lb && GB <= La, "four-step tile");
   k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA>
-      <<<nbig * (Lb / GA), NT, (size_t)GA * (La + 1) * sizeof(float2), st>>>(pa, tmp, W, log2Ntw);
+      <<<nbig * (Lb / GA), NT, (size_t)GA * (La + 1) * sizeof(CT), st>>>(pa, tmp, W, log2Ntw);
   k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB>
-      <<<nbig * (La / GB), NT, (size_t)GB * (Lb + 1) * sizeof(float2), st>>>(pb, tmp, W, log2Ntw);
+      <<<nbig * (La / GB), NT, (size_t)GB * (Lb + 1) * sizeof(CT), st>>>(pb, tmp, W, log2Ntw);
 }
 
 template <class F>
@@ -559,18 +574,21 @@ void dispatch_log2(int lg, F&& f) {
 }  // namespace
 
 int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2* tmp, cudaStream_t st) {
+  // fp64 DFT of the padded signal: a fp32 FFT's roundoff is proportional to the
+  // global spectral norm and would swamp the weak high-frequency bands that the
+  // top first-order filters select (precision budget).
   ProbPad pr{x, xhat, P.N, P.N_pad, P.pad_left, P.prm.pad_mode == JTFS_PAD_PERIODIC};
-  const float2* W = (const float2*)P.d_twiddle;
+  const double2* W = (const double2*)P.d_twiddle64;
   const int ltw = ilog2_exact(P.N_tw);
   dispatch_log2(ilog2_exact(P.N_pad), [&](auto c) {
     constexpr int LG = decltype(c)::value;
-    if constexpr (LG <= 12) {
+    if constexpr (LG <= 11) {
       launch_rows<LG, -1>(pr, nsig, W, ltw, st);
     } else {
-      launch_fft4<LG, -1>(pr, pr, nsig, tmp, W, ltw, st);
+      launch_fft4<LG, -1>(pr, pr, nsig, (double2*)tmp, W, ltw, st);
     }
   });
-  return ilog2_exact(P.N_pad) <= 12 ? 1 : 2;
+  return ilog2_exact(P.N_pad) <= 11 ? 1 : 2;
 }
 
 int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,

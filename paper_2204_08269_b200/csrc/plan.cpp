@@ -435,10 +435,13 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   // ---- twiddles exp(-2 pi i t / N_tw) ----
   P.N_tw = P.N_pad;
   P.twiddle.resize((size_t)P.N_tw * 2);
+  P.twiddle64.resize((size_t)P.N_tw * 2);
   for (int t = 0; t < P.N_tw; ++t) {
     const auto w = unit_root(-(int64_t)t, P.N_tw);
     P.twiddle[2 * t] = (float)w.real();
     P.twiddle[2 * t + 1] = (float)w.imag();
+    P.twiddle64[2 * t] = w.real();
+    P.twiddle64[2 * t + 1] = w.imag();
   }
   return "";
 }
@@ -448,7 +451,7 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   WsLayout w{};
   w.xhat = al((size_t)mb * p.N_pad * 8);
   // four-step intermediate: largest group (rows x L) among U1 / Y2 / KA
-  size_t tmp = (size_t)p.N_pad * 8;
+  size_t tmp = (size_t)p.N_pad * 16;  // fp64 KA intermediate
   for (const auto& g : p.u1_groups)
     if (g.log2L > 12) tmp = std::max(tmp, g.rows.size() * ((size_t)8 << g.log2L));
   for (const auto& g : p.y2_groups)

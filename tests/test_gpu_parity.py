@@ -75,18 +75,22 @@ def test_tap_xhat_and_scalogram(jt):
         ref = np.fft.fft(O.pad_signal(x64, s))
         assert np.abs(xh[b] - ref).max() <= 1e-5 * np.abs(ref).max()
         S0, S1, Yphi, U1hat, Y2 = O.first_order(x64, s)
-        off = 0
-        for lam in range(s.n1):
-            r = np.fft.ifft(U1hat[lam]).real
-            g = u1[b, off:off + len(r)]
-            assert np.linalg.norm(g - r) <= 1e-5 * max(np.linalg.norm(r), 1e-3 * np.abs(u1[b]).max()), lam
-            off += len(r)
-        off = 0
+        # scalogram rows U1_lambda: per-row relative L2 with the parity floor (tests/parity.py)
+        rows_o = [np.fft.ifft(U1hat[lam]).real for lam in range(s.n1)]
+        offs = np.cumsum([0] + [len(r) for r in rows_o])
+        rows_g = [u1[b, offs[i]:offs[i + 1]] for i in range(s.n1)]
+        e = path_errors(rows_g, rows_o)
+        assert e.max() <= 1e-5, (float(e.max()), int(np.argmax(e)))
+        # Y2 rows (lambda, alpha)
+        rows_o, rows_g, off = [], [], 0
         for a in s.alphas:
             ref2 = Y2[a]
             g2 = y2[b, off:off + ref2.size].reshape(ref2.shape)
-            assert np.linalg.norm(g2 - ref2) <= 2e-5 * np.linalg.norm(ref2) + 1e-9, a
+            rows_o += list(ref2)
+            rows_g += list(g2)
             off += ref2.size
+        e = path_errors(rows_g, rows_o)
+        assert e.max() <= 1e-5, (float(e.max()), int(np.argmax(e)))
         assert np.abs(yp[b] - Yphi).max() <= 1e-5 * np.abs(Yphi).max()
 
 
