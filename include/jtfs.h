@@ -161,7 +161,8 @@ JTFS_API jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, in
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)
- *   tap 2: Y2      -> out complex (float2) [B][sum_alpha K_alpha L_alpha] (alpha-major, lambda, time)
+ *   tap 2: Y2      -> out fp32 [B][sum_alpha 2 K_alpha L_alpha]: per alpha a planar [2 K_alpha][L_alpha]
+ *                     block, row 2*lambda = Re Y2_alpha[lambda], row 2*lambda+1 = Im
  *   tap 3: Yphi    -> out fp32 [B][n1][N_pad/T]
  * `out_floats` is the capacity of out in floats. */
 JTFS_API jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* x, int64_t B,

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 
@@ -65,6 +66,8 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   } while (0)
   UP(P.d_bandvals, P.bandvals.data(), P.bandvals.size() * 4);
   UP(P.d_A, P.A.data(), P.A.size() * 4);
+  UP(P.d_A2hi, P.A2hi.data(), P.A2hi.size() * 4);
+  UP(P.d_A2lo, P.A2lo.data(), P.A2lo.size() * 4);
   UP(P.d_g, P.g.data(), P.g.size() * 4);
   UP(P.d_W, P.W.data(), P.W.size() * 4);
   UP(P.d_hphi, P.hphi.data(), P.hphi.size() * 4);
@@ -107,12 +110,14 @@ jtfs_status upload_plan(jtfs::Plan& P) {
 #undef UP
   e = jtfs::ke_set_smem(P);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_ke)");
+  e = jtfs::tc_setup_device(P);
+  if (e != cudaSuccess) return cuda_fail(e, "tcgen05 KD setup (tensor maps / smem)");
   return JTFS_OK;
 }
 
 struct WsPtrs {
-  float2 *xhat, *tmp, *u1hat, *y2;
-  float *u1, *yphi, *part;
+  float2 *xhat, *tmp, *u1hat;
+  float *u1, *yphi, *y2, *part;
   int* flag;
 };
 
@@ -125,7 +130,7 @@ WsPtrs carve(const jtfs::Plan& P, void* ws, int64_t mb) {
   w.u1 = (float*)c; c += L.u1;
   w.u1hat = (float2*)c; c += L.u1hat;
   w.yphi = (float*)c; c += L.yphi;
-  w.y2 = (float2*)c; c += L.y2;
+  w.y2 = (float*)c; c += L.y2;
   w.part = (float*)c; c += L.part;
   w.flag = (int*)c;
   return w;
@@ -169,24 +174,33 @@ struct StageScope {
   }
 };
 
-// enqueue every stage for one micro-batch of nb signals
-void run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, const WsPtrs& w, bool keep_u1,
-                    int upto_stage, cudaStream_t st) {
+// enqueue every stage for one micro-batch of nb signals; returns "" or an error
+std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, const WsPtrs& w, bool keep_u1,
+                           int upto_stage, cudaStream_t st) {
   using namespace jtfs;
   jtfs_layout_t lay;
   layout_of(P, &lay);
   { StageScope s(P, 0, st); s.done(launch_pad_fft(P, x, nb, w.xhat, w.tmp, st)); }
-  if (upto_stage == 0) return;
+  if (upto_stage == 0) return "";
   { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st)); }
   {
     StageScope s(P, 2, st);
     s.done(launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, out, lay.floats_per_signal, lay.off_s0, lay.off_s1,
                             P.d_u1_off, P.d_k1, P.d_band_L1, st));
   }
-  if (upto_stage == 1) return;
+  if (upto_stage == 1) return "";
   { StageScope s(P, 3, st); s.done(launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
-  if (upto_stage == 2) return;
-  { StageScope s(P, 4, st); s.done(launch_kd(P, w.y2, nb, w.part, st)); }
+  if (upto_stage == 2) return "";
+  {
+    StageScope s(P, 4, st);
+    int err = 0;
+    s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, nb, w.part, st, &err) : launch_kd(P, w.y2, nb, w.part, st));
+    if (err) return "tcgen05 KD: cuTensorMapEncodeTiled failed for the Y2 tensor map";
+    if (std::getenv("JTFS_DEBUG_SYNC")) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return std::string("KD: ") + cudaGetErrorString(e);
+    }
+  }
   KEParams kp{};
   kp.paths = (const DevPath*)P.d_paths;
   kp.filters = (const DevFilter*)P.d_fr;
@@ -212,6 +226,7 @@ void run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, const WsP
   kp.Mpad = P.Mpad;
   kp.k_phiphi = P.prm.average_fr ? P.log2F : 0;
   { StageScope s(P, 5, st); s.done(launch_ke(P, kp, nb, st)); }
+  return "";
 }
 
 struct DeviceGuard {
@@ -372,7 +387,8 @@ jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* out
   layout_of(P, &lay);
   for (int64_t b0 = 0; b0 < B; b0 += mb) {
     const int nb = (int)std::min<int64_t>(mb, B - b0);
-    run_microbatch(P, x + b0 * P.N, nb, out + b0 * lay.floats_per_signal, w, false, 99, st);
+    const std::string err = run_microbatch(P, x + b0 * P.N, nb, out + b0 * lay.floats_per_signal, w, false, 99, st);
+    if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
@@ -432,7 +448,11 @@ jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* x, int64_
   cudaError_t e = cudaMalloc(&scratch, (size_t)B * lay.floats_per_signal * 4);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc scratch");
   const int stage = tap == 0 ? 0 : (tap == 1 || tap == 3) ? 1 : 2;
-  run_microbatch(P, x, (int)B, scratch, w, true, stage, st);
+  const std::string rerr = run_microbatch(P, x, (int)B, scratch, w, true, stage, st);
+  if (!rerr.empty()) {
+    cudaFree(scratch);
+    return fail(JTFS_ERR_CUDA, rerr);
+  }
   const void* src = tap == 0 ? (const void*)w.xhat : tap == 1 ? (const void*)w.u1 : tap == 2 ? (const void*)w.y2
                                                                                                : (const void*)w.yphi;
   e = cudaMemcpyAsync(out, src, (size_t)need * 4, cudaMemcpyDeviceToDevice, st);

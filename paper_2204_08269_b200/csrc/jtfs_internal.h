@@ -59,6 +59,14 @@ struct AlphaKD {
   int chunk;        // time columns per KD work unit
   int nchunks;      // L / chunk
   int64_t part_off; // float offset of partials [nchunks][Mpad][n_frames] in one signal
+  // tensor-core (tcgen05) tiling, see kernels_tc.cu
+  int tc_K8 = 0, tc_Kst = 0, tc_nkc = 0, tc_nbox = 0, tc_BR = 0, tc_colstride = 0;
+  int tc_Nt = 0, tc_ybytes = 0, tc_S = 2, tc_tpu = 1;
+  int64_t tc_a2_off = 0;  // float offset of A''_alpha [2 Mpad][Kst] in the A2 tables
+};
+
+struct TmapBlob {
+  alignas(64) unsigned char b[128];
 };
 
 // A frequential filter f of the joint stage (rows of every A_alpha).
@@ -85,6 +93,8 @@ struct Plan {
   std::vector<AlphaKD> kd;       // active alphas in bank order
   int64_t y2_total = 0;          // complex elements of Y2 per signal
   int M = 0, Mpad = 0;           // joint-stage rows per alpha
+  int tc_n_mpart = 1, tc_n_mblk = 1;  // M-parts per KD work unit, 64-row M-blocks per part
+  int kd_impl = 1;               // 1: tcgen05 (default), 0: SIMT (JTFS_KD=simt, validation)
   std::vector<FrFilter> fr;      // frequential filters: theta=-1 (beta), theta=+1 (beta), phi_F
   std::vector<jtfs_path_t> paths;
   std::vector<int> path_filter;  // path -> fr index (or -1)
@@ -97,7 +107,8 @@ struct Plan {
   std::vector<Band> band_phiT_L1;        // phi_T on the grid N_pad >> k, k = 0..log2T
   std::vector<FoldGroup> u1_groups;      // first-order IFFT rows grouped by L1
   std::vector<FoldGroup> y2_groups;      // second-order rows grouped by L_alpha
-  std::vector<float> A;                  // complex interleaved A_alpha^T tables
+  std::vector<float> A;                  // complex interleaved A_alpha^T tables (SIMT KD)
+  std::vector<float> A2hi, A2lo;         // real-embedded A''_alpha, 3xTF32 split (tcgen05 KD)
   std::vector<float> g;                  // time pooling taps per alpha
   std::vector<float> W;                  // lambda pooling matrices per filter
   std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
@@ -110,6 +121,9 @@ struct Plan {
   int device = -1;
   float* d_bandvals = nullptr;
   float* d_A = nullptr;
+  float* d_A2hi = nullptr;
+  float* d_A2lo = nullptr;
+  std::vector<TmapBlob> tc_maps;  // CUtensorMap of A''_hi / A''_lo per alpha
   float* d_g = nullptr;
   float* d_W = nullptr;
   float* d_hphi = nullptr;
@@ -141,6 +155,9 @@ struct WsLayout {
   size_t xhat, tmp, u1, u1hat, yphi, y2, part, flag, total;
 };
 WsLayout ws_layout(const Plan& p, int64_t mb);
+
+// tensor-core KD planning / device setup (kernels_tc.cu)
+void plan_tc(Plan& P);
 
 // algorithmic per-signal cost per stage (jtfs_cost)
 void stage_cost(const Plan& p, double flops[6], double bytes[6]);

@@ -71,8 +71,8 @@ struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
   const float* bandvals;
   int L;
   // outputs
-  float* dst_real;   // modulus output (U1) or nullptr
-  float2* dst_cplx;  // complex output (Y2) or nullptr
+  float* dst_real;    // modulus output (U1) or nullptr
+  float* dst_planar;  // planar complex output (Y2: re row at dst_off, im row at dst_off + L) or nullptr
   int64_t dst_stride;
   __device__ float2 load(int rho, int i) const {
     const int b = rho / nrows, r = rho % nrows;
@@ -84,7 +84,9 @@ struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
     if (dst_real) {
       dst_real[(int64_t)b * dst_stride + d.dst_off + o] = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * d.scale;
     } else {
-      dst_cplx[(int64_t)b * dst_stride + d.dst_off + o] = cscale(v, d.scale);
+      float* row = dst_planar + (int64_t)b * dst_stride + d.dst_off;
+      row[o] = v.x * d.scale;
+      row[L + o] = v.y * d.scale;
     }
   }
 };
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(256) k_kd_simt(KDParams p) {
   const int ch = u % p.nchunks;
   const int b = u / p.nchunks;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const float2* Y = p.y2 + (int64_t)b * p.y2_stride + p.y2_off;
+  const float* Y = p.y2 + (int64_t)b * p.y2_stride + p.y2_off;  // planar rows 2l (re), 2l+1 (im)
   const float2* A = p.A + mblk * 64;
   float part[4][NF];
 #pragma unroll
@@ -363,7 +365,10 @@ __global__ void __launch_bounds__(256) k_kd_simt(KDParams p) {
         const int idx = threadIdx.x + q * 256;
         const int kk = idx / 128, c = idx % 128;
         float2 y = make_float2(0.f, 0.f);
-        if (k0 + kk < p.K && c0 + c < col_end) y = Y[(int64_t)(k0 + kk) * p.L + c0 + c];
+        if (k0 + kk < p.K && c0 + c < col_end) {
+          const float* row = Y + (int64_t)(2 * (k0 + kk)) * p.L + c0 + c;
+          y = make_float2(row[0], row[p.L]);
+        }
         Ys[kk][c] = y;
       }
       __syncthreads();
@@ -644,14 +649,14 @@ int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int
   return 1;
 }
 
-int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float2* y2, float2* tmp, cudaStream_t st) {
+int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st) {
   const float2* W = (const float2*)P.d_twiddle;
   const int ltw = ilog2_exact(P.N_tw);
   int n = 0;
   for (const auto& g : P.y2_groups) {
     n += g.log2L <= 12 ? 1 : 2;
     const int nr = (int)g.rows.size();
-    ProbFold pf{u1hat, P.u1_total, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, nullptr, y2, P.y2_total};
+    ProbFold pf{u1hat, P.u1_total, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, nullptr, y2, 2 * P.y2_total};
     dispatch_log2(g.log2L, [&](auto c) {
       constexpr int LG = decltype(c)::value;
       if constexpr (LG <= 12) {
@@ -664,7 +669,7 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float2* y2
   return n;
 }
 
-int launch_kd(const Plan& P, const float2* y2, int nsig, float* part, cudaStream_t st) {
+int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st) {
   for (const auto& d : P.kd) {
     KDParams k{};
     k.A = (const float2*)P.d_A + d.a_off;
@@ -680,9 +685,9 @@ int launch_kd(const Plan& P, const float2* y2, int nsig, float* part, cudaStream
     k.nframes = P.n_frames;
     k.chunk = d.chunk;
     k.nchunks = d.nchunks;
-    k.y2_off = d.y2_off;
+    k.y2_off = 2 * d.y2_off;
     k.part_off = d.part_off;
-    k.y2_stride = P.y2_total;
+    k.y2_stride = 2 * P.y2_total;
     k.part_stride = P.part_total;
     const int grid = nsig * d.nchunks * (P.Mpad / 64);
     if (P.n_frames <= 8) k_kd_simt<8><<<grid, 256, 0, st>>>(k);

@@ -10,7 +10,7 @@ namespace jtfs {
 
 struct KDParams {
   const float2* A;   // A_alpha^T [Kpad][Mpad]
-  const float2* y2;  // micro-batch Y2 base
+  const float* y2;   // micro-batch Y2 base (planar complex rows)
   const float* g;    // time pooling taps g_alpha[L]
   float* part;       // micro-batch partials base
   int K, Kpad, Mpad, L, D, frame0, nframes, chunk, nchunks;
@@ -51,11 +51,13 @@ int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, f
 int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int nsig, float* yphi, float* out,
                       int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
                       const Band* d_band_L1, cudaStream_t st);
-int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float2* y2, float2* tmp, cudaStream_t st);
-int launch_kd(const Plan& P, const float2* y2, int nsig, float* part, cudaStream_t st);
+int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st);
+int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st);
 size_t ke_smem_bytes(const Plan& P);
 int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
 cudaError_t ke_set_smem(const Plan& P);
+int launch_kd_tc(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, int* err);
+cudaError_t tc_setup_device(Plan& P);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 
 }  // namespace jtfs

@@ -5,6 +5,8 @@
 // in tests, through jtfs_debug_filter and the forward output).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <complex>
 #include <map>
 #include <stdexcept>
@@ -275,7 +277,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       r.m0 = b.m0;
       r.len = b.len;
       r.band_off = b.off;
-      r.dst_off = d.y2_off + (int64_t)l * d.L;
+      r.dst_off = 2 * d.y2_off + (int64_t)(2 * l) * d.L;  // planar: re row, then im row
       r.scale = (float)(1.0 / P.L1[l]);
       G->rows.push_back(r);
     }
@@ -337,7 +339,18 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     f.row0 = P.M;
     P.M += f.nrows;
   }
-  P.Mpad = (P.M + 63) / 64 * 64;
+  {
+    // M-blocks of 64 complex rows, split into M-parts so that one part's pooled
+    // row accumulators fit the tcgen05 kernel's shared memory (<= 36 KiB)
+    const int n_frames_pad = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
+    const int max_mblk = 144 / n_frames_pad;
+    const int mblocks = (P.M + 63) / 64;
+    P.tc_n_mpart = (mblocks + max_mblk - 1) / max_mblk;
+    P.tc_n_mblk = (mblocks + P.tc_n_mpart - 1) / P.tc_n_mpart;
+    P.Mpad = P.tc_n_mblk * P.tc_n_mpart * 64;
+    const char* e = std::getenv("JTFS_KD");
+    P.kd_impl = (e && std::strcmp(e, "simt") == 0) ? 0 : 1;
+  }
   // frequential taps h_f = IDFT_{N_fr}(f_hat) (fp64)
   std::vector<std::vector<std::complex<double>>> htap(P.fr.size());
   for (size_t i = 0; i < P.fr.size(); ++i) {
@@ -373,6 +386,49 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       }
     }
   }
+  // real-embedded A''_alpha for the tensor cores: row (mb*128 + q*32 + i) is
+  // Re (i < 16) or Im (i >= 16) of complex row mb*64 + q*16 + i%16 (one TMEM lane
+  // quarter per q); column 2l / 2l+1 multiplies Re / Im Y2[l]; 3xTF32 hi/lo split.
+  P.A2hi.clear();
+  P.A2lo.clear();
+  for (auto& d : P.kd) {
+    const int Kst = (2 * d.K + 31) / 32 * 32;
+    d.tc_a2_off = (int64_t)P.A2hi.size();
+    const size_t base = P.A2hi.size();
+    P.A2hi.resize(base + (size_t)2 * P.Mpad * Kst, 0.f);
+    P.A2lo.resize(base + (size_t)2 * P.Mpad * Kst, 0.f);
+    std::vector<int> row_f(P.Mpad, -1), row_i(P.Mpad, 0);
+    for (size_t fi = 0; fi < P.fr.size(); ++fi)
+      for (int i = 0; i < P.fr[fi].nrows; ++i) {
+        row_f[P.fr[fi].row0 + i] = (int)fi;
+        row_i[P.fr[fi].row0 + i] = i;
+      }
+    auto split = [](double v, float& hi, float& lo) {
+      const float f = (float)v;
+      uint32_t u;
+      std::memcpy(&u, &f, 4);
+      u &= 0xFFFFE000u;
+      std::memcpy(&hi, &u, 4);
+      lo = (float)(v - (double)hi);
+    };
+    for (int R = 0; R < 2 * P.Mpad; ++R) {
+      const int mb = R / 128, l = R % 128, q = l / 32, i = l % 32;
+      const int r = mb * 64 + q * 16 + (i & 15);
+      const bool re = i < 16;
+      if (row_f[r] < 0) continue;
+      const auto& f = P.fr[row_f[r]];
+      const int rp = f.rprime[row_i[r]];
+      for (int lam = 0; lam < d.K; ++lam) {
+        const int idx = (((rp << f.k) - lam) % P.N_fr + P.N_fr) % P.N_fr;
+        const auto a = htap[row_f[r]][idx];
+        const double c0 = re ? a.real() : a.imag();   // multiplies Re Y
+        const double c1 = re ? -a.imag() : a.real();  // multiplies Im Y
+        const size_t o = base + (size_t)R * Kst + 2 * lam;
+        split(c0, P.A2hi[o], P.A2lo[o]);
+        split(c1, P.A2hi[o + 1], P.A2lo[o + 1]);
+      }
+    }
+  }
   // time pooling taps g_alpha = IDFT_L(phi_T_hat^(L)) (real, even)
   P.g.clear();
   for (auto& d : P.kd) {
@@ -390,6 +446,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     d.chunk = std::min(d.L, 4096);
     d.nchunks = d.L / d.chunk;
   }
+  plan_tc(P);
   P.part_total = 0;
   for (auto& d : P.kd) {
     d.part_off = P.part_total;

@@ -68,7 +68,7 @@ def test_tap_xhat_and_scalogram(jt):
     x = torch.from_numpy(X).cuda()
     xh = plan.debug_tap(0, x).cpu().numpy().view(np.complex64).reshape(len(X), s.N_pad)
     u1 = plan.debug_tap(1, x).cpu().numpy().reshape(len(X), -1)
-    y2 = plan.debug_tap(2, x).cpu().numpy().view(np.complex64).reshape(len(X), -1)
+    y2 = plan.debug_tap(2, x).cpu().numpy().reshape(len(X), -1)
     yp = plan.debug_tap(3, x).cpu().numpy().reshape(len(X), s.n1, -1)
     for b in range(len(X)):
         x64 = X[b].astype(np.float64)
@@ -85,10 +85,11 @@ def test_tap_xhat_and_scalogram(jt):
         rows_o, rows_g, off = [], [], 0
         for a in s.alphas:
             ref2 = Y2[a]
-            g2 = y2[b, off:off + ref2.size].reshape(ref2.shape)
+            pl = y2[b, off:off + 2 * ref2.size].reshape(2 * ref2.shape[0], ref2.shape[1])
+            g2 = pl[0::2] + 1j * pl[1::2]            # planar rows: re, im
             rows_o += list(ref2)
             rows_g += list(g2)
-            off += ref2.size
+            off += 2 * ref2.size
         e = path_errors(rows_g, rows_o)
         assert e.max() <= 1e-5, (float(e.max()), int(np.argmax(e)))
         assert np.abs(yp[b] - Yphi).max() <= 1e-5 * np.abs(Yphi).max()
@@ -145,6 +146,21 @@ def test_c3_full_size_sampled_paths(jt):
     for b in (0, 2):
         O.set_workers(8)
         _check_signal(plan, out[b], X[b].astype(np.float64), prm, paths=sample)
+
+
+@pytest.mark.parametrize("kw", [C1, dict(N=2 ** 13, J=8, Q=16, J_fr=4, T=2 ** 13, F=16, average_fr=False),
+                                dict(N=2 ** 16, J=12, Q=16, J_fr=5, T=2 ** 13, F=4)], ids=["c1", "c2", "c3"])
+def test_kd_tensor_core_matches_simt(jt, kw, monkeypatch):
+    # the tcgen05 3xTF32 contraction against the FP32 SIMT one on the same inputs
+    import torch
+    X = signals.notes(2, N=kw["N"], seed0=77) if kw["N"] >= 2 ** 13 else _c1_inputs()
+    x = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    monkeypatch.setenv("JTFS_KD", "simt")
+    a = jt.Plan(**kw).forward(x).cpu().numpy().astype(np.float64)
+    monkeypatch.setenv("JTFS_KD", "tc")
+    b = jt.Plan(**kw).forward(x).cpu().numpy().astype(np.float64)
+    for i in range(len(X)):
+        assert np.linalg.norm(a[i] - b[i]) <= 1e-5 * np.linalg.norm(a[i])
 
 
 def test_determinism_and_batch_independence(jt):
