@@ -278,9 +278,6 @@ jtfs_status jtfs_plan_create(const jtfs_params* params, jtfs_plan_t* out) {
     return fail(JTFS_ERR_INVALID_ARG, err);
   }
   jtfs::Plan& P = h->P;
-  // micro-batch: keep one micro-batch's workspace around <= 4 GiB
-  const size_t per = jtfs::ws_layout(P, 1).total;
-  P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ((size_t)4 << 30) / std::max<size_t>(per, 1)));
   if (params->device >= 0) {
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);

@@ -138,8 +138,18 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
 
 __device__ __forceinline__ float sqrt_fast(float x) {
   float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
+}
+// packed FP32x2 FMA (FFMA2): d = a * (s, s) + c
+__device__ __forceinline__ float2 ffma2(float2 a, float s, float2 c) {
+  unsigned long long r, ua, us, uc;
+  ua = *reinterpret_cast<unsigned long long*>(&a);
+  uc = *reinterpret_cast<unsigned long long*>(&c);
+  const float2 ss = make_float2(s, s);
+  us = *reinterpret_cast<const unsigned long long*>(&ss);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ua), "l"(us), "l"(uc));
+  return *reinterpret_cast<float2*>(&r);
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -169,8 +179,10 @@ template <int NF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_kd_tc(const __grid_constant__ CUtensorMap tmAhi, const __grid_constant__ CUtensorMap tmAlo,
             const __grid_constant__ CUtensorMap tmY, TcParams p) {
-  extern __shared__ unsigned char smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B align by offsetting the __shared__ array itself (keeps the shared
+  // address space visible to the compiler: LDS/STS instead of generic LD/ST)
+  uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   float* Yhi = reinterpret_cast<float*>(base);
   float* Ylo = reinterpret_cast<float*>(base + p.ybytes);
   uint8_t* Ast = base + 2 * p.ybytes;
@@ -342,9 +354,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 8192; ++i) p.dbg[8192 + 2048 + i] = reinterpret_cast<const float*>(Ast)[i];
             }
           }
-          float part[NF];
+          float2 part[NF / 2];
 #pragma unroll
-          for (int m = 0; m < NF; ++m) part[m] = 0.f;
+          for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
+          // re lane (i < 16) takes the even columns, im lane (i + 16) the odd ones
+          const float2* wcol = reinterpret_cast<const float2*>(Wt) + (im ? NF / 2 : 0);
           for (int c0 = 0; c0 < p.Nt; c0 += 16) {
             uint32_t v[16];
             tmem_ld16(tb + c0, v);
@@ -353,17 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 8; ++j) {
               const float a = __uint_as_float(v[2 * j]), bb = __uint_as_float(v[2 * j + 1]);
               const float recv = __shfl_xor_sync(0xffffffffu, im ? a : bb, 16);
-              const float re = im ? recv : a;
-              const float iv = im ? bb : recv;
-              const float mag = sqrt_fast(fmaf(re, re, iv * iv));
-              const float4* w4 = reinterpret_cast<const float4*>(Wt + (c0 + 2 * j + (im ? 1 : 0)) * NF);
+              const float own = im ? bb : a;
+              const float mag = sqrt_fast(fmaf(own, own, recv * recv));
+              const float4* w4 = reinterpret_cast<const float4*>(wcol + (c0 + 2 * j) * (NF / 2));
 #pragma unroll
               for (int m4 = 0; m4 < NF / 4; ++m4) {
                 const float4 w = w4[m4];
-                part[4 * m4 + 0] = fmaf(w.x, mag, part[4 * m4 + 0]);
-                part[4 * m4 + 1] = fmaf(w.y, mag, part[4 * m4 + 1]);
-                part[4 * m4 + 2] = fmaf(w.z, mag, part[4 * m4 + 2]);
-                part[4 * m4 + 3] = fmaf(w.w, mag, part[4 * m4 + 3]);
+                part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mag, part[2 * m4 + 0]);
+                part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mag, part[2 * m4 + 1]);
               }
             }
           }
@@ -371,11 +382,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty + ab);
 #pragma unroll
-          for (int m = 0; m < NF; ++m) part[m] += __shfl_xor_sync(0xffffffffu, part[m], 16);
+          for (int m = 0; m < NF / 2; ++m) {
+            part[m].x += __shfl_xor_sync(0xffffffffu, part[m].x, 16);
+            part[m].y += __shfl_xor_sync(0xffffffffu, part[m].y, 16);
+          }
           if (!im) {
-            float* a = acc + (mb * 64 + rloc) * NF;
+            float2* a = reinterpret_cast<float2*>(acc + (mb * 64 + rloc) * NF);
 #pragma unroll
-            for (int m = 0; m < NF; ++m) a[m] += part[m];
+            for (int m = 0; m < NF / 2; ++m) a[m] = make_float2(a[m].x + part[m].x, a[m].y + part[m].y);
           }
         }
       }
@@ -459,6 +473,16 @@ void plan_tc(Plan& P) {
     d.tc_Nt = Nt;
     d.tc_ybytes = (Nt / 32) * d.tc_colstride;
     while (d.tc_S < 4 && tc_smem(d, NF, P.tc_n_mblk) + 32768 <= budget) ++d.tc_S;
+    // time chunk per work unit: the largest power of two <= 4096 that still gives
+    // about 4 units per SM for a full micro-batch (partials are per chunk)
+    {
+      int64_t target = (int64_t)P.mb * P.tc_n_mpart * d.L / (4 * 148);
+      int ch = 4096;
+      while (ch > Nt && ch > target) ch /= 2;
+      d.chunk = std::min(ch, d.L);
+      if (d.chunk < Nt) d.chunk = Nt;
+      d.nchunks = d.L / d.chunk;
+    }
     d.tc_tpu = d.chunk / Nt;
     if (d.L < 32 || d.chunk % Nt) P.kd_impl = 0;  // tiles need >= 32 time columns
   }

@@ -443,8 +443,14 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       for (int m : nz) acc += ph[m] * unit_root((int64_t)m * t, d.L).real();
       P.g.push_back((float)(acc / d.L));
     }
-    d.chunk = std::min(d.L, 4096);
+    d.chunk = std::min(d.L, 4096);   // refined by plan_tc (work units per launch)
     d.nchunks = d.L / d.chunk;
+  }
+  // micro-batch: keep one micro-batch's workspace around <= 4 GiB (partials are small)
+  P.part_total = 0;
+  {
+    const size_t per = ws_layout(P, 1).total;
+    P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ((size_t)4 << 30) / std::max<size_t>(per, 1)));
   }
   plan_tc(P);
   P.part_total = 0;
