@@ -196,6 +196,7 @@ def main():
     clocks = clk.stop()
     plan.profile_enable(False)
     prof = plan.profile_read(reset=True)
+    kd_alpha_ms = plan.profile_read_kd(reset=True)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -253,6 +254,7 @@ def main():
             "clocks": clocks,
             "stages_ms": {k: round(v[0], 3) for k, v in prof.items()},
             "stage_share": stage_share,
+            "kd_ms_per_alpha": [round(v, 3) for v in kd_alpha_ms],
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(1)

@@ -204,6 +204,10 @@ JTFS_API jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, i
 JTFS_API jtfs_status jtfs_profile_enable(jtfs_plan_t plan, int32_t enable);
 JTFS_API jtfs_status jtfs_profile_read(jtfs_plan_t plan, double* stage_ms, int64_t* stage_launches,
                                        int32_t cap, int32_t reset);
+/* Per-alpha breakdown of stage 4 (KD) recorded while profiling is enabled:
+ * ms[i] = summed milliseconds of the KD launches of the i-th active alpha
+ * (layout.n_alpha entries).  Synchronises; reset != 0 clears. */
+JTFS_API jtfs_status jtfs_profile_read_kd(jtfs_plan_t plan, double* ms, int32_t cap, int32_t reset);
 
 JTFS_API const char* jtfs_status_string(jtfs_status s);
 JTFS_API const char* jtfs_last_error(void);

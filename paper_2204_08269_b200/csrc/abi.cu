@@ -66,8 +66,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   } while (0)
   UP(P.d_bandvals, P.bandvals.data(), P.bandvals.size() * 4);
   UP(P.d_A, P.A.data(), P.A.size() * 4);
-  UP(P.d_A2hi, P.A2hi.data(), P.A2hi.size() * 4);
-  UP(P.d_A2lo, P.A2lo.data(), P.A2lo.size() * 4);
+  UP(P.d_A2, P.A2.data(), P.A2.size() * 4);
   UP(P.d_g, P.g.data(), P.g.size() * 4);
   UP(P.d_W, P.W.data(), P.W.size() * 4);
   UP(P.d_hphi, P.hphi.data(), P.hphi.size() * 4);
@@ -503,6 +502,32 @@ jtfs_status jtfs_profile_read(jtfs_plan_t plan, double* stage_ms, int64_t* stage
       P.prof_events[s].clear();
       P.launches[s] = 0;
     }
+  }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_profile_read_kd(jtfs_plan_t plan, double* ms, int32_t cap, int32_t reset) {
+  if (!plan || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  jtfs::Plan& P = plan->P;
+  for (size_t a = 0; a < P.kd.size(); ++a) {
+    double t = 0;
+    if (a < P.prof_kd.size())
+      for (auto& pr : P.prof_kd[a]) {
+        float x = 0;
+        cudaError_t e = cudaEventSynchronize((cudaEvent_t)pr.second);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&x, (cudaEvent_t)pr.first, (cudaEvent_t)pr.second);
+        if (e != cudaSuccess) return cuda_fail(e, "profile events");
+        t += x;
+      }
+    if ((int)a < cap && ms) ms[a] = t;
+  }
+  if (reset) {
+    for (auto& v : P.prof_kd)
+      for (auto& pr : v) {
+        cudaEventDestroy((cudaEvent_t)pr.first);
+        cudaEventDestroy((cudaEvent_t)pr.second);
+      }
+    P.prof_kd.clear();
   }
   return JTFS_OK;
 }

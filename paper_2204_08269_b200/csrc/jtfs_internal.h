@@ -62,7 +62,7 @@ struct AlphaKD {
   // tensor-core (tcgen05) tiling, see kernels_tc.cu
   int tc_K8 = 0, tc_Kst = 0, tc_nkc = 0, tc_nbox = 0, tc_BR = 0, tc_colstride = 0;
   int tc_Nt = 0, tc_ybytes = 0, tc_S = 2, tc_tpu = 1;
-  int64_t tc_a2_off = 0;  // float offset of A''_alpha [2 Mpad][Kst] in the A2 tables
+  int64_t tc_a2_off = 0;  // float offset of A''_alpha's 16 KiB chunk records in A2
 };
 
 struct TmapBlob {
@@ -108,7 +108,7 @@ struct Plan {
   std::vector<FoldGroup> u1_groups;      // first-order IFFT rows grouped by L1
   std::vector<FoldGroup> y2_groups;      // second-order rows grouped by L_alpha
   std::vector<float> A;                  // complex interleaved A_alpha^T tables (SIMT KD)
-  std::vector<float> A2hi, A2lo;         // real-embedded A''_alpha, 3xTF32 split (tcgen05 KD)
+  std::vector<float> A2;                 // real-embedded A''_alpha, 3xTF32 split, pre-tiled/swizzled (tcgen05 KD)
   std::vector<float> g;                  // time pooling taps per alpha
   std::vector<float> W;                  // lambda pooling matrices per filter
   std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
@@ -121,9 +121,7 @@ struct Plan {
   int device = -1;
   float* d_bandvals = nullptr;
   float* d_A = nullptr;
-  float* d_A2hi = nullptr;
-  float* d_A2lo = nullptr;
-  std::vector<TmapBlob> tc_maps;  // CUtensorMap of A''_hi / A''_lo per alpha
+  float* d_A2 = nullptr;
   float* d_g = nullptr;
   float* d_W = nullptr;
   float* d_hphi = nullptr;
@@ -144,6 +142,7 @@ struct Plan {
   bool prof = false;
   std::vector<std::pair<void*, void*>> prof_events[6];  // cudaEvent_t pairs per stage
   int64_t launches[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<std::vector<std::pair<void*, void*>>> prof_kd;  // per active alpha
 };
 
 // plan.cpp

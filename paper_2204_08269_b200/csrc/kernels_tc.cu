@@ -12,13 +12,14 @@
 // mantissa bits cleared, lo = x - hi exactly) keeps ~fp32 accuracy.
 //
 // CTA = 10 warps, persistent over work units (signal, time chunk, M-part):
-//   warp 0      TMA producer: Y'' tile (MN-major, SWIZZLE_128B, loaded once per
-//               tile and reused by every M-block) + A'' K-chunks (K-major,
-//               SWIZZLE_128B, streamed from L2 through an S-stage ring)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..9  epilogue, two sets of 4 (one per TMEM accumulator buffer):
-//               tcgen05.ld -> re/im pairing by shuffle -> |Z| -> phi_T pooling at
-//               the retained frames -> per-row smem accumulators -> global partials.
+//   warp 8      TMA producer: Y'' tile (MN-major, SWIZZLE_128B_BASE32B, loaded
+//               once per tile and reused by every M-block) + A'' K-records of 16
+//               (K-major, SWIZZLE_64B, pre-tiled; 2 per 32 KiB stage of an S-ring)
+//   warp 9      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 0..7  epilogue, two sets of 4; set s owns TMEM buffer s and the M-blocks
+//               mb = s, s+2, ...: tcgen05.ld -> re/im pairing by shuffle -> |Z| ->
+//               phi_T pooling at the retained frames (packed FFMA2) -> per-row
+//               accumulators in registers -> global partials at the end of a unit.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -71,13 +72,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---- TMA ----
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
   asm volatile(
@@ -85,6 +79,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "[%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// ---- bulk copy (non-tensor TMA): contiguous global -> smem, completes on an mbarrier ----
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 // ---- tcgen05 ----
@@ -114,12 +116,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor (sm_100 version bit), lbo / sbo in bytes.
-//  A, K-major, SWIZZLE_128B (layout 2): 8-row x 128 B atoms, sbo = 1024, lbo unused.
+//  A, K-major, SWIZZLE_64B (layout 4): 8-row x 64 B atoms, sbo = 512, lbo unused.
 //  B, MN-major tf32, SWIZZLE_128B_BASE32B (layout 1, Swizzle<2,5,2>): 4-row x 128 B
 //  atoms (32 MN elements), lbo = stride between 32-element MN groups, sbo = 512
 //  between 4-row K atoms.  (Plain SWIZZLE_128B MN-major tf32 reads as zeros on
 //  sm_100a -- found with tools/tc_unit.cu.)
-constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128Base32B = 1;
+constexpr uint32_t kLayoutSW128Base32B = 1, kLayoutSW64 = 4;
+constexpr int kRec = 16384;    // one A'' K-record: 128 rows x 16 fp32, hi + lo (SWIZZLE_64B images)
+constexpr int kStage = 32768;  // one pipeline stage: up to two consecutive K-records
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -152,11 +156,23 @@ __device__ __forceinline__ float2 ffma2(float2 a, float s, float2 c) {
   return *reinterpret_cast<float2*>(&r);
 }
 
+// one elected lane of a converged warp (operands stay warp-uniform -> UR registers)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 %%rx;\n\t.reg .pred %%px;\n\t"
+      "elect.sync %%rx|%%px, %1;\n\t"
+      "@%%px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 struct TcParams {
   int K8;        // K' = 2K rounded up to 8: rows of Y'' used
-  int nkc;       // 32-wide K chunks of A''
+  int nkc;       // 16-wide K chunks of A''
   int Nt;        // time columns per tile (32..256)
   int BR, nbox;  // TMA box rows, boxes per 32-column group
   int colstride; // bytes between 32-column groups of the Y'' tile
@@ -167,18 +183,20 @@ struct TcParams {
   int n_mpart, n_mblk;  // M-parts and 64-complex-row M-blocks per part
   int L, D, frame0, nframes, Mpad;
   int nsig;
+  int expmode;     // measurement only (JTFS_TC_EXPMODE): 1 skip epilogue math, 2 skip TMEM loads too
+  const float* A;  // A''_alpha pre-tiled 16 KiB chunk records [2 Mpad / 128][nkc]
   const float* g;  // phi_T taps g_alpha[L]
   float* part;
   int64_t part_off, part_stride;
-  float* dbg;      // debug dump (JTFS_TC_DEBUG) or nullptr
 };
 
 constexpr int kThreads = 320;
+// warp roles: 0..7 epilogue, 8 TMA producer, 9 MMA issuer (highest warp id: the
+// issue arbiter favours high warp ids, so the single MMA thread is never starved)
+constexpr int kProdWarp = 8, kMmaWarp = 9;
 
-template <int NF>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_kd_tc(const __grid_constant__ CUtensorMap tmAhi, const __grid_constant__ CUtensorMap tmAlo,
-            const __grid_constant__ CUtensorMap tmY, TcParams p) {
+template <int NF, int MAXSLOT>
+__global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ CUtensorMap tmY, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
@@ -186,9 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* Yhi = reinterpret_cast<float*>(base);
   float* Ylo = reinterpret_cast<float*>(base + p.ybytes);
   uint8_t* Ast = base + 2 * p.ybytes;
-  float* Wt = reinterpret_cast<float*>(Ast + p.S * 32768);
-  float* acc = Wt + p.Nt * NF;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(acc + p.n_mblk * 64 * NF);
+  float* Wt = reinterpret_cast<float*>(Ast + p.S * kStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Wt + p.Nt * NF);
   uint64_t* y_full = bars + 0;
   uint64_t* y_ready = bars + 1;
   uint64_t* y_empty = bars + 2;
@@ -213,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -225,11 +242,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int units = p.nsig * p.nchunks * p.n_mpart;
   const int ngroups = p.Nt / 32;
+  const int nst = (p.nkc + 1) / 2;  // A'' stages (<= 2 records of 16 K-columns) per M-block
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      uint32_t tile_cnt = 0, a_cnt = 0;
+    // Bulk copies issued by one thread complete one after another (~600 cycles
+    // each, measured with tools/bulk_bw.cu), so kIssuers lanes issue in parallel:
+    // A'' stage j goes through lane j % kIssuers; the Y'' boxes are spread too.
+    // Issuer lanes must divide S so that every ring slot is always served by the
+    // same lane (parity waits cannot tell laps apart).
+    const int kIssuers = (p.S % 4 == 0) ? 4 : (p.S % 3 == 0) ? 3 : (p.S % 2 == 0) ? 2 : 1;
+    if (lane < kIssuers) {
+      uint32_t tile_cnt = 0, j = 0, s = 0, ph = 0;
       const uint32_t ytx = (uint32_t)(ngroups * p.nbox * p.BR * 128);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int mpart = u % p.n_mpart;
@@ -237,83 +261,118 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = u / (p.n_mpart * p.nchunks);
         for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
           mbar_wait(y_empty, (tile_cnt + 1) & 1);
-          mbar_expect_tx(y_full, ytx);
           const int t0 = (chunk * p.tpu + tile) * p.Nt;
-          for (int cg = 0; cg < ngroups; ++cg)
-            for (int bx = 0; bx < p.nbox; ++bx)
+          if (p.expmode >= 4) {  // measurement only: no Y'' load
+            if (lane == 0) mbar_arrive(y_full);
+          } else {
+            if (lane == 0) mbar_expect_tx(y_full, ytx);
+            __syncwarp((1u << kIssuers) - 1);
+            for (int i = lane; i < ngroups * p.nbox; i += kIssuers) {
+              const int cg = i / p.nbox, bx = i % p.nbox;
               tma_load_3d(reinterpret_cast<uint8_t*>(Yhi) + cg * p.colstride + bx * p.BR * 128, &tmY, y_full,
                           t0 + cg * 32, bx * p.BR, b);
+            }
+          }
           for (int mb = 0; mb < p.n_mblk; ++mb) {
-            const int row0 = (mpart * p.n_mblk + mb) * 128;
-            for (int kc = 0; kc < p.nkc; ++kc, ++a_cnt) {
-              const int s = a_cnt % p.S;
-              const uint32_t k = a_cnt / p.S;
-              mbar_wait(a_empty + s, (k + 1) & 1);
-              mbar_expect_tx(a_full + s, 32768);
-              tma_load_2d(Ast + s * 32768, &tmAhi, a_full + s, kc * 32, row0);
-              tma_load_2d(Ast + s * 32768 + 16384, &tmAlo, a_full + s, kc * 32, row0);
+            const float* arec = p.A + (size_t)(mpart * p.n_mblk + mb) * p.nkc * (kRec / 4);
+            for (int st = 0; st < nst; ++st) {
+              if ((int)(j % kIssuers) == lane) {
+                mbar_wait(a_empty + s, ph ^ 1);
+                if (p.expmode >= 3) {  // measurement only: no A'' load
+                  mbar_arrive(a_full + s);
+                } else {
+                  const uint32_t bytes = (uint32_t)(min(2, p.nkc - 2 * st) * kRec);
+                  mbar_expect_tx(a_full + s, bytes);
+                  bulk_load(Ast + s * kStage, arec + (size_t)(2 * st) * (kRec / 4), bytes, a_full + s);
+                }
+              }
+              ++j;
+              if (++s == (uint32_t)p.S) {
+                s = 0;
+                ph ^= 1;
+              }
             }
           }
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      uint32_t tile_cnt = 0, a_cnt = 0, mb_cnt = 0;
+  } else if (warp == kMmaWarp) {
+    // ===================== MMA issuer (warp-wide loop, one elected lane issues) =====================
+    {
+      uint32_t tile_cnt = 0, s = 0, ph = 0;
+      uint32_t use0 = 0, use1 = 0;  // per-accumulator-buffer use counters
       const uint32_t idesc = idesc_tf32(p.Nt);
-      const uint32_t yhi = smem_u32(Yhi), ylo = smem_u32(Ylo), ast = smem_u32(Ast);
       const int ksteps = p.K8 / 8;
+      // descriptor templates; per MMA only the 14-bit start-address field changes
+      const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 512, kLayoutSW64);
+      const uint64_t dYh0 = sdesc(smem_u32(Yhi), p.colstride, 512, kLayoutSW128Base32B);
+      const uint64_t dYl0 = sdesc(smem_u32(Ylo), p.colstride, 512, kLayoutSW128Base32B);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
           mbar_wait(y_ready, tile_cnt & 1);
           tc_fence_after();
-          for (int mb = 0; mb < p.n_mblk; ++mb, ++mb_cnt) {
-            const int ab = mb_cnt & 1;
-            mbar_wait(acc_empty + ab, ((mb_cnt >> 1) + 1) & 1);
+          for (int mb = 0; mb < p.n_mblk; ++mb) {
+            const int ab = mb & 1;  // M-block parity fixes the TMEM buffer and the epilogue set
+            const uint32_t use = ab ? use1++ : use0++;
+            mbar_wait(acc_empty + ab, (use + 1) & 1);
             tc_fence_after();
             const uint32_t d = tmem_base + (uint32_t)(ab * p.Nt);
-            for (int kc = 0; kc < p.nkc; ++kc, ++a_cnt) {
-              const int s = a_cnt % p.S;
-              mbar_wait(a_full + s, (a_cnt / p.S) & 1);
+            for (int st = 0; st < nst; ++st) {
+              mbar_wait(a_full + s, ph);
               tc_fence_after();
-              const uint32_t ah = ast + s * 32768, al = ah + 16384;
-              for (int ks = 0; ks < 4; ++ks) {
-                const int kstep = kc * 4 + ks;
-                if (kstep >= ksteps) break;
-                const uint64_t dah = sdesc(ah + ks * 32, 16, 1024, kLayoutSW128);
-                const uint64_t dal = sdesc(al + ks * 32, 16, 1024, kLayoutSW128);
-                const uint64_t dbh = sdesc(yhi + kstep * 1024, p.colstride, 512, kLayoutSW128Base32B);
-                const uint64_t dbl = sdesc(ylo + kstep * 1024, p.colstride, 512, kLayoutSW128Base32B);
-                mma_tf32(d, dah, dbh, idesc, kstep > 0 ? 1u : 0u);
-                mma_tf32(d, dah, dbl, idesc, 1u);
-                mma_tf32(d, dal, dbh, idesc, 1u);
+              if (elect_one()) {
+                const uint64_t dst = dA0 + (uint64_t)((s * kStage) >> 4);
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                  const uint64_t ah = dst + (uint64_t)((r * kRec) >> 4);
+                  const uint64_t al = ah + (uint64_t)((kRec / 2) >> 4);
+#pragma unroll
+                  for (int ks = 0; ks < 2; ++ks) {
+                    const int kstep = 4 * st + 2 * r + ks;
+                    if (kstep < ksteps) {
+                      const uint64_t ko = (uint64_t)((ks * 32) >> 4), yo = (uint64_t)((kstep * 1024) >> 4);
+                      mma_tf32(d, ah + ko, dYh0 + yo, idesc, kstep > 0 ? 1u : 0u);
+                      mma_tf32(d, ah + ko, dYl0 + yo, idesc, 1u);
+                      mma_tf32(d, al + ko, dYh0 + yo, idesc, 1u);
+                    }
+                  }
+                }
+                mma_commit(a_empty + s);
               }
-              mma_commit(a_empty + s);
+              __syncwarp();
+              if (++s == (uint32_t)p.S) {
+                s = 0;
+                ph ^= 1;
+              }
             }
-            mma_commit(acc_full + ab);
+            if (elect_one()) mma_commit(acc_full + ab);
+            __syncwarp();
           }
-          mma_commit(y_empty);
+          if (elect_one()) mma_commit(y_empty);
+          __syncwarp();
         }
       }
     }
   } else {
-    // ===================== epilogue (warps 2..9) =====================
-    const int etid = threadIdx.x - 64;       // 0..255
-    const int eset = (warp - 2) >> 2;        // TMEM accumulator buffer handled
+    // ===================== epilogue (warps 0..7) =====================
+    const int etid = threadIdx.x;            // 0..255
+    const int eset = warp >> 2;              // TMEM accumulator buffer handled
     const int q = warp & 3;                  // TMEM lane quarter (warp_id % 4)
     const bool im = lane >= 16;
     const int rloc = q * 16 + (lane & 15);   // complex row inside an M-block
-    uint32_t tile_cnt = 0, mb_cnt = 0;
+    uint32_t tile_cnt = 0, use = 0;
     const int yfloats = ngroups * p.colstride / 4;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int mpart = u % p.n_mpart;
       const int chunk = (u / p.n_mpart) % p.nchunks;
       const int b = u / (p.n_mpart * p.nchunks);
+      float2 accr[MAXSLOT][NF / 2];  // pooled partials of my rows (M-blocks eset, eset+2, ...)
+#pragma unroll
+      for (int k = 0; k < MAXSLOT; ++k)
+#pragma unroll
+        for (int m = 0; m < NF / 2; ++m) accr[k][m] = make_float2(0.f, 0.f);
       for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
-        named_bar(1, 256);  // every epilogue warp is done with the previous tile (W, acc)
-        if (tile == 0)
-          for (int i = etid; i < p.n_mblk * 64 * NF; i += 256) acc[i] = 0.f;
+        named_bar(1, 256);  // every epilogue warp is done with the previous tile's W
         mbar_wait(y_full, tile_cnt & 1);
         // 3xTF32 split of the Y'' tile, in place (elementwise: layout-agnostic)
         for (int i = etid; i < yfloats; i += 256) {
@@ -322,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           Yhi[i] = h;
           Ylo[i] = v - h;
         }
-        // phi_T pooling taps of this tile: Wt[c][m] = g[((frame0 + m) D - t) mod L]
+        // phi_T pooling taps of this tile, stored [c][NF/2 re-lane pairs | NF/2 im-lane pairs]
         const int t0 = (chunk * p.tpu + tile) * p.Nt;
         for (int i = etid; i < p.Nt * NF; i += 256) {
           const int c = i / NF, m = i % NF;
@@ -336,33 +395,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(1, 256);
-        if (p.dbg && blockIdx.x == 0 && tile_cnt == 0)
-          for (int i = etid; i < 8192 && i < yfloats; i += 256) p.dbg[i] = Yhi[i];
         if (etid == 0) mbar_arrive(y_ready);
-        for (int mb = 0; mb < p.n_mblk; ++mb, ++mb_cnt) {
-          const int ab = mb_cnt & 1;
-          if (ab != eset) continue;
-          mbar_wait(acc_full + ab, (mb_cnt >> 1) & 1);
+        for (int mb = eset; mb < p.n_mblk; mb += 2, ++use) {
+          const int ab = eset;
+          mbar_wait(acc_full + ab, use & 1);
           tc_fence_after();
           const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * p.Nt);
-          if (p.dbg && blockIdx.x == 0 && mb_cnt == 0) {
-            uint32_t v[16];
-            tmem_ld16(tb, v);
-            tmem_wait_ld();
-            for (int j = 0; j < 16; ++j) p.dbg[8192 + (q * 32 + lane) * 16 + j] = __uint_as_float(v[j]);
-            if (lane == 0 && q == 0) {
-              for (int i = 0; i < 8192; ++i) p.dbg[8192 + 2048 + i] = reinterpret_cast<const float*>(Ast)[i];
-            }
-          }
           float2 part[NF / 2];
 #pragma unroll
           for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
           // re lane (i < 16) takes the even columns, im lane (i + 16) the odd ones
           const float2* wcol = reinterpret_cast<const float2*>(Wt) + (im ? NF / 2 : 0);
           for (int c0 = 0; c0 < p.Nt; c0 += 16) {
+            if (p.expmode >= 2) break;
             uint32_t v[16];
             tmem_ld16(tb + c0, v);
             tmem_wait_ld();
+            if (p.expmode == 1) {
+              part[0].x += __uint_as_float(v[0] ^ v[15]);
+              continue;
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float a = __uint_as_float(v[2 * j]), bb = __uint_as_float(v[2 * j + 1]);
@@ -386,26 +438,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             part[m].x += __shfl_xor_sync(0xffffffffu, part[m].x, 16);
             part[m].y += __shfl_xor_sync(0xffffffffu, part[m].y, 16);
           }
-          if (!im) {
-            float2* a = reinterpret_cast<float2*>(acc + (mb * 64 + rloc) * NF);
+          const int slot = mb >> 1;
 #pragma unroll
-            for (int m = 0; m < NF / 2; ++m) a[m] = make_float2(a[m].x + part[m].x, a[m].y + part[m].y);
-          }
+          for (int k = 0; k < MAXSLOT; ++k)
+            if (k == slot) {
+#pragma unroll
+              for (int m = 0; m < NF / 2; ++m)
+                accr[k][m] = make_float2(accr[k][m].x + part[m].x, accr[k][m].y + part[m].y);
+            }
         }
       }
-      // unit done: write the M-part's pooled partials of this time chunk
-      named_bar(1, 256);
-      float* dst = p.part + (int64_t)b * p.part_stride + p.part_off +
-                   ((int64_t)chunk * p.Mpad + (int64_t)mpart * p.n_mblk * 64) * p.nframes;
-      for (int i = etid; i < p.n_mblk * 64 * p.nframes; i += 256) {
-        const int r = i / p.nframes, m = i % p.nframes;
-        dst[i] = acc[r * NF + m];
+      // unit done: my rows' pooled partials of this time chunk -> global
+      if (!im) {
+        float* dst = p.part + (int64_t)b * p.part_stride + p.part_off +
+                     ((int64_t)chunk * p.Mpad + (int64_t)mpart * p.n_mblk * 64) * p.nframes;
+#pragma unroll
+        for (int k = 0; k < MAXSLOT; ++k) {
+          const int mb = 2 * k + eset;
+          if (mb < p.n_mblk) {
+            float* d = dst + (int64_t)(mb * 64 + rloc) * p.nframes;
+#pragma unroll
+            for (int m = 0; m < NF / 2; ++m) {
+              if (2 * m < p.nframes) d[2 * m] = accr[k][m].x;
+              if (2 * m + 1 < p.nframes) d[2 * m + 1] = accr[k][m].y;
+            }
+          }
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
@@ -443,36 +507,45 @@ bool encode(CUtensorMap* m, void* base, int rank, const cuuint64_t* dims, const 
             swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-size_t tc_smem(const AlphaKD& d, int nf, int n_mblk) {
-  return 1024 + 2 * (size_t)d.tc_ybytes + (size_t)d.tc_S * 32768 + (size_t)d.tc_Nt * nf * 4 +
-         (size_t)n_mblk * 64 * nf * 4 + 8 * (7 + 2 * d.tc_S) + 16;
+size_t tc_smem(const AlphaKD& d, int nf) {
+  return 1024 + 2 * (size_t)d.tc_ybytes + (size_t)d.tc_S * tc::kStage + (size_t)d.tc_Nt * nf * 4 +
+         8 * (7 + 2 * d.tc_S) + 16;
 }
 int nf_of(int nframes) { return nframes <= 8 ? 8 : nframes <= 16 ? 16 : 32; }
 }  // namespace
 
-// choose the per-alpha tensor-core tiling (called by build_plan)
+// choose the per-alpha tensor-core tiling (called by build_plan): the widest
+// Y'' tile (Nt, power of two <= 256) that leaves room for >= 3 A'' stages, then as
+// many 16 KiB A'' stages as fit (<= 8)
 void plan_tc(Plan& P) {
   const int NF = nf_of(P.n_frames);
   const size_t budget = 227 * 1024;
   P.tc_n_mblk = P.Mpad / 64 / P.tc_n_mpart;
+  // tuning overrides (measurement only): largest tile width / number of A'' stages
+  const char* e_nt = std::getenv("JTFS_TC_NTMAX");
+  const char* e_s = std::getenv("JTFS_TC_SMAX");
+  const int nt_max = e_nt ? std::max(32, std::atoi(e_nt)) : 256;
+  const int s_max = e_s ? std::max(2, std::min(6, std::atoi(e_s))) : 6;
   for (auto& d : P.kd) {
     const int K2 = 2 * d.K;
     d.tc_K8 = (K2 + 7) / 8 * 8;
-    d.tc_Kst = (K2 + 31) / 32 * 32;
-    d.tc_nkc = d.tc_Kst / 32;
+    d.tc_Kst = (K2 + 15) / 16 * 16;
+    d.tc_nkc = d.tc_Kst / 16;
     d.tc_nbox = (d.tc_K8 + 127) / 128;
     d.tc_BR = (d.tc_K8 + d.tc_nbox * 8 - 1) / (d.tc_nbox * 8) * 8;
     d.tc_colstride = d.tc_nbox * d.tc_BR * 128;
-    const size_t fixed = 1024 + (size_t)P.tc_n_mblk * 64 * NF * 4 + 256;
-    int Nt = std::min(256, d.L);
-    d.tc_S = 2;
+    int Nt = std::min(nt_max, d.L);
     for (; Nt > 32; Nt /= 2) {
-      const size_t y = 2 * (size_t)(Nt / 32) * d.tc_colstride;
-      if (fixed + y + 2 * 32768 + (size_t)Nt * NF * 4 <= budget) break;
+      d.tc_Nt = Nt;
+      d.tc_ybytes = (Nt / 32) * d.tc_colstride;
+      d.tc_S = 2;
+      if (tc_smem(d, NF) <= budget) break;
     }
     d.tc_Nt = Nt;
     d.tc_ybytes = (Nt / 32) * d.tc_colstride;
-    while (d.tc_S < 4 && tc_smem(d, NF, P.tc_n_mblk) + 32768 <= budget) ++d.tc_S;
+    d.tc_S = 2;
+    while (d.tc_S < s_max && tc_smem(d, NF) + tc::kStage <= budget) ++d.tc_S;
+    if (d.tc_S == 5) d.tc_S = 4;  // issuer lanes must divide S (kernels_tc.cu producer)
     // time chunk per work unit: the largest power of two <= 4096 that still gives
     // about 4 units per SM for a full micro-batch (partials are per chunk)
     {
@@ -484,40 +557,25 @@ void plan_tc(Plan& P) {
       d.nchunks = d.L / d.chunk;
     }
     d.tc_tpu = d.chunk / Nt;
-    if (d.L < 32 || d.chunk % Nt) P.kd_impl = 0;  // tiles need >= 32 time columns
+    if (d.L < 32 || d.chunk % Nt || tc_smem(d, NF) > budget) P.kd_impl = 0;
   }
 }
 
 cudaError_t tc_setup_device(Plan& P) {
   const int NF = nf_of(P.n_frames);
   size_t mx = 0;
-  for (auto& d : P.kd) mx = std::max(mx, tc_smem(d, NF, P.tc_n_mblk));
+  for (auto& d : P.kd) mx = std::max(mx, tc_smem(d, NF));
   cudaError_t e = cudaSuccess;
-  if (NF == 8) e = cudaFuncSetAttribute(tc::k_kd_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  else if (NF == 16) e = cudaFuncSetAttribute(tc::k_kd_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  else e = cudaFuncSetAttribute(tc::k_kd_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  if (NF == 8) e = cudaFuncSetAttribute(tc::k_kd_tc<8, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  else if (NF == 16)
+    e = cudaFuncSetAttribute(tc::k_kd_tc<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  else e = cudaFuncSetAttribute(tc::k_kd_tc<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
   if (e != cudaSuccess) return e;
-  // A'' tensor maps (constant per plan)
-  P.tc_maps.resize(P.kd.size() * 2);
-  for (size_t i = 0; i < P.kd.size(); ++i) {
-    const auto& d = P.kd[i];
-    cuuint64_t dims[2] = {(cuuint64_t)d.tc_Kst, (cuuint64_t)(2 * P.Mpad)};
-    cuuint64_t strides[1] = {(cuuint64_t)d.tc_Kst * 4};
-    cuuint32_t box[2] = {32, 128};
-    if (!encode(reinterpret_cast<CUtensorMap*>(P.tc_maps[2 * i].b), P.d_A2hi + d.tc_a2_off, 2, dims, strides, box,
-                CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode(reinterpret_cast<CUtensorMap*>(P.tc_maps[2 * i + 1].b), P.d_A2lo + d.tc_a2_off, 2, dims, strides,
-                box, CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
-  }
   return cudaSuccess;
 }
 
-int launch_kd_tc(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, int* err) {
+int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, int* err) {
   const int NF = nf_of(P.n_frames);
-  static float* dbg = nullptr;
-  const bool debug = std::getenv("JTFS_TC_DEBUG") != nullptr;
-  if (debug && !dbg) cudaMalloc(&dbg, 65536 * 4);
   int sms = 148;
   {
     int dev = 0;
@@ -537,7 +595,7 @@ int launch_kd_tc(const Plan& P, const float* y2, int nsig, float* part, cudaStre
     }
     tc::TcParams p{};
     p.K8 = d.tc_K8;
-    p.nkc = (d.tc_K8 + 31) / 32;
+    p.nkc = (d.tc_K8 + 15) / 16;
     p.Nt = d.tc_Nt;
     p.BR = d.tc_BR;
     p.nbox = d.tc_nbox;
@@ -554,29 +612,30 @@ int launch_kd_tc(const Plan& P, const float* y2, int nsig, float* part, cudaStre
     p.nframes = P.n_frames;
     p.Mpad = P.Mpad;
     p.nsig = nsig;
+    p.A = P.d_A2 + d.tc_a2_off;
+    {
+      const char* e = std::getenv("JTFS_TC_EXPMODE");
+      p.expmode = e ? std::atoi(e) : 0;
+    }
     p.g = P.d_g + d.g_off;
     p.part = part;
     p.part_off = d.part_off;
     p.part_stride = P.part_total;
-    p.dbg = (debug && i == 0) ? dbg : nullptr;
     const int units = nsig * d.nchunks * P.tc_n_mpart;
     const int grid = std::min(units, sms);
-    const size_t sm = tc_smem(d, NF, P.tc_n_mblk);
-    const CUtensorMap* mA = reinterpret_cast<const CUtensorMap*>(P.tc_maps[2 * i].b);
-    const CUtensorMap* mL = reinterpret_cast<const CUtensorMap*>(P.tc_maps[2 * i + 1].b);
-    if (NF == 8) tc::k_kd_tc<8><<<grid, tc::kThreads, sm, st>>>(*mA, *mL, tmY, p);
-    else if (NF == 16) tc::k_kd_tc<16><<<grid, tc::kThreads, sm, st>>>(*mA, *mL, tmY, p);
-    else tc::k_kd_tc<32><<<grid, tc::kThreads, sm, st>>>(*mA, *mL, tmY, p);
-    if (debug && i == 0) {
-      std::vector<float> h(65536);
-      cudaStreamSynchronize(st);
-      cudaMemcpy(h.data(), dbg, 65536 * 4, cudaMemcpyDeviceToHost);
-      FILE* f = std::fopen(std::getenv("JTFS_TC_DEBUG"), "wb");
-      if (f) {
-        std::fwrite(h.data(), 4, h.size(), f);
-        std::fclose(f);
-      }
+    const size_t sm = tc_smem(d, NF);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (P.prof) {
+      if (P.prof_kd.size() < P.kd.size()) P.prof_kd.resize(P.kd.size());
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
+      P.prof_kd[i].push_back({(void*)e0, (void*)e1});
     }
+    if (NF == 8) tc::k_kd_tc<8, 9><<<grid, tc::kThreads, sm, st>>>(tmY, p);
+    else if (NF == 16) tc::k_kd_tc<16, 4><<<grid, tc::kThreads, sm, st>>>(tmY, p);
+    else tc::k_kd_tc<32, 2><<<grid, tc::kThreads, sm, st>>>(tmY, p);
+    if (P.prof) cudaEventRecord(e1, st);
   }
   *err = 0;
   return (int)P.kd.size();

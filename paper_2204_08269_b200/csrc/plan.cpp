@@ -342,8 +342,10 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   {
     // M-blocks of 64 complex rows, split into M-parts so that one part's pooled
     // row accumulators fit the tcgen05 kernel's shared memory (<= 36 KiB)
+    // M-blocks per part: 2 * MAXSLOT register-resident row accumulators per
+    // epilogue thread in kernels_tc.cu (NF 8: 9 slots, 16: 4, 32: 2)
     const int n_frames_pad = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
-    const int max_mblk = 144 / n_frames_pad;
+    const int max_mblk = n_frames_pad == 8 ? 18 : n_frames_pad == 16 ? 8 : 4;
     const int mblocks = (P.M + 63) / 64;
     P.tc_n_mpart = (mblocks + max_mblk - 1) / max_mblk;
     P.tc_n_mblk = (mblocks + P.tc_n_mpart - 1) / P.tc_n_mpart;
@@ -389,14 +391,16 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   // real-embedded A''_alpha for the tensor cores: row (mb*128 + q*32 + i) is
   // Re (i < 16) or Im (i >= 16) of complex row mb*64 + q*16 + i%16 (one TMEM lane
   // quarter per q); column 2l / 2l+1 multiplies Re / Im Y2[l]; 3xTF32 hi/lo split.
-  P.A2hi.clear();
-  P.A2lo.clear();
+  // Stored pre-tiled for one cp.async.bulk per pipeline stage: for every
+  // (128-row block, 16-column K chunk) a 16 KiB record [hi 8 KiB | lo 8 KiB], each
+  // half in the UMMA K-major SWIZZLE_64B image (8-row x 64 B atoms, Swizzle<2,4,3>).
+  P.A2.clear();
   for (auto& d : P.kd) {
-    const int Kst = (2 * d.K + 31) / 32 * 32;
-    d.tc_a2_off = (int64_t)P.A2hi.size();
-    const size_t base = P.A2hi.size();
-    P.A2hi.resize(base + (size_t)2 * P.Mpad * Kst, 0.f);
-    P.A2lo.resize(base + (size_t)2 * P.Mpad * Kst, 0.f);
+    const int nkc = (2 * d.K + 15) / 16;
+    const int nblk = 2 * P.Mpad / 128;
+    d.tc_a2_off = (int64_t)P.A2.size();
+    const size_t base = P.A2.size();
+    P.A2.resize(base + (size_t)nblk * nkc * 4096, 0.f);
     std::vector<int> row_f(P.Mpad, -1), row_i(P.Mpad, 0);
     for (size_t fi = 0; fi < P.fr.size(); ++fi)
       for (int i = 0; i < P.fr[fi].nrows; ++i) {
@@ -411,8 +415,16 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       std::memcpy(&hi, &u, 4);
       lo = (float)(v - (double)hi);
     };
-    for (int R = 0; R < 2 * P.Mpad; ++R) {
-      const int mb = R / 128, l = R % 128, q = l / 32, i = l % 32;
+    auto put = [&](int blk, int R, int col, float hi, float lo) {
+      const int kc = col / 16, kk = col % 16;
+      const uint32_t o = (uint32_t)((R / 8) * 512 + (R % 8) * 64 + kk * 4);
+      const uint32_t sw = o ^ (((o >> 7) & 3u) << 4);
+      const size_t rec = base + ((size_t)blk * nkc + kc) * 4096;
+      P.A2[rec + sw / 4] = hi;
+      P.A2[rec + 2048 + sw / 4] = lo;
+    };
+    for (int Rg = 0; Rg < 2 * P.Mpad; ++Rg) {
+      const int mb = Rg / 128, l = Rg % 128, q = l / 32, i = l % 32;
       const int r = mb * 64 + q * 16 + (i & 15);
       const bool re = i < 16;
       if (row_f[r] < 0) continue;
@@ -423,9 +435,11 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
         const auto a = htap[row_f[r]][idx];
         const double c0 = re ? a.real() : a.imag();   // multiplies Re Y
         const double c1 = re ? -a.imag() : a.real();  // multiplies Im Y
-        const size_t o = base + (size_t)R * Kst + 2 * lam;
-        split(c0, P.A2hi[o], P.A2lo[o]);
-        split(c1, P.A2hi[o + 1], P.A2lo[o + 1]);
+        float hi, lo;
+        split(c0, hi, lo);
+        put(mb, l, 2 * lam, hi, lo);
+        split(c1, hi, lo);
+        put(mb, l, 2 * lam + 1, hi, lo);
       }
     }
   }

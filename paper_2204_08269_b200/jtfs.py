@@ -31,7 +31,7 @@ EXPORTS = [
     "jtfs_plan", "jtfs_plan_create", "jtfs_plan_destroy", "jtfs_layout", "jtfs_paths",
     "jtfs_lambda_xi", "jtfs_workspace_size", "jtfs_forward", "jtfs_forward_host",
     "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_cost", "jtfs_profile_enable",
-    "jtfs_profile_read", "jtfs_status_string", "jtfs_last_error",
+    "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -70,6 +70,7 @@ _lib.jtfs_debug_filter.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int3
 _lib.jtfs_cost.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32]
 _lib.jtfs_profile_enable.argtypes = [_P, C.c_int32]
 _lib.jtfs_profile_read.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32, C.c_int32]
+_lib.jtfs_profile_read_kd.argtypes = [_P, C.POINTER(C.c_double), C.c_int32, C.c_int32]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -186,6 +187,13 @@ class Plan:
         nl = (C.c_int64 * 6)()
         _check(_lib.jtfs_profile_read(self._h, ms, nl, 6, int(reset)), "jtfs_profile_read")
         return {STAGES[i]: (ms[i], nl[i]) for i in range(6)}
+
+    def profile_read_kd(self, reset: bool = True):
+        """Per-alpha KD milliseconds since the last reset."""
+        n = self.layout.n_alpha
+        ms = (C.c_double * max(n, 1))()
+        _check(_lib.jtfs_profile_read_kd(self._h, ms, n, int(reset)), "jtfs_profile_read_kd")
+        return [ms[i] for i in range(n)]
 
     # ---- compute (torch tensors on the plan's device) ----
     def workspace(self, batch: int):

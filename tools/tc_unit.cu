@@ -23,6 +23,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 
 __device__ __forceinline__ uint32_t swz(uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
 __device__ __forceinline__ uint32_t swz32(uint32_t off) { return off ^ (((off >> 7) & 3u) << 5); }
+__device__ __forceinline__ uint32_t swz64(uint32_t off) { return off ^ (((off >> 7) & 3u) << 4); }
 
 // mode 0: A K-major SW128, B MN-major SW128 (the KD layout)
 // mode 1: A K-major SW128, B K-major SW128
@@ -35,10 +36,18 @@ __global__ void k_test(const float* A, const float* B, float* D, int mode, int K
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x;
-  for (int i = tid; i < 128 * 32; i += blockDim.x) {
-    const int m = i / 32, k = i % 32;
-    const uint32_t off = (m / 8) * 1024 + (m % 8) * 128 + k * 4;
-    *(float*)(As + swz(off)) = (k < K) ? A[m * K + k] : 0.f;
+  if (mode == 3) {  // A K-major SWIZZLE_64B: 16-float (64 B) rows, 8-row atoms of 512 B, K chunks of 16
+    for (int i = tid; i < 128 * 32; i += blockDim.x) {
+      const int m = i / 32, k = i % 32;
+      const uint32_t off = (k / 16) * (128 * 64) + (m / 8) * 512 + (m % 8) * 64 + (k % 16) * 4;
+      *(float*)(As + swz64(off)) = (k < K) ? A[m * K + k] : 0.f;
+    }
+  } else {
+    for (int i = tid; i < 128 * 32; i += blockDim.x) {
+      const int m = i / 32, k = i % 32;
+      const uint32_t off = (m / 8) * 1024 + (m % 8) * 128 + k * 4;
+      *(float*)(As + swz(off)) = (k < K) ? A[m * K + k] : 0.f;
+    }
   }
   const int KR = (K + 7) / 8 * 8;
   for (int i = tid; i < KR * N; i += blockDim.x) {
@@ -47,7 +56,7 @@ __global__ void k_test(const float* A, const float* B, float* D, int mode, int K
     if (mode == 0) {
       const uint32_t off = (n / 32) * (KR * 128) + k * 128 + (n % 32) * 4;
       *(float*)(Bs + swz(off)) = v;
-    } else if (mode == 2) {
+    } else if (mode == 2 || mode == 3) {
       const uint32_t off = (n / 32) * (KR * 128) + k * 128 + (n % 32) * 4;
       *(float*)(Bs + swz32(off)) = v;
     } else {
@@ -72,9 +81,10 @@ __global__ void k_test(const float* A, const float* B, float* D, int mode, int K
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((mode != 1 ? 1u : 0u) << 16) |
                            ((uint32_t)(N >> 3) << 17) | (8u << 24);
     for (int ks = 0; ks < KR / 8; ++ks) {
-      uint64_t da = sdesc(smem_u32(As) + ks * 32, 16, 1024, 2);
+      uint64_t da = mode == 3 ? sdesc(smem_u32(As) + (ks / 2) * (128 * 64) + (ks % 2) * 32, 16, 512, 4)
+                              : sdesc(smem_u32(As) + ks * 32, 16, 1024, 2);
       uint64_t db = mode == 0   ? sdesc(smem_u32(Bs) + ks * 1024, KR * 128, 1024, 2)
-                    : mode == 2 ? sdesc(smem_u32(Bs) + ks * 1024, KR * 128, 512, 1)
+                    : mode >= 2 ? sdesc(smem_u32(Bs) + ks * 1024, KR * 128, 512, 1)
                                 : sdesc(smem_u32(Bs) + ks * 32, 16, 1024, 2);
       uint32_t acc = ks > 0;
       asm volatile(
@@ -114,7 +124,7 @@ __global__ void k_test(const float* A, const float* B, float* D, int mode, int K
 
 int main() {
   constexpr int N = 64;
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 4; ++mode)
     for (int K : {8, 24}) {
       std::vector<float> A(128 * K), B(K * N), D(128 * N), R(128 * N, 0.f);
       for (int i = 0; i < 128 * K; ++i) A[i] = (float)((i * 7 + 3) % 11 - 5);
