@@ -71,6 +71,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// wait + accumulate the waited cycles into acc (instrumentation)
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long long& acc) {
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  acc += clock64() - t0;
+}
+
 // ---- TMA ----
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
@@ -111,6 +118,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       "%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -184,6 +201,7 @@ struct TcParams {
   int L, D, frame0, nframes, Mpad;
   int nsig;
   int expmode;     // measurement only (JTFS_TC_EXPMODE): 1 skip epilogue math, 2 skip TMEM loads too
+  unsigned long long* prof;  // measurement only (JTFS_TC_PROF): per-role wait-cycle counters or nullptr
   const float* A;  // A''_alpha pre-tiled 16 KiB chunk records [2 Mpad / 128][nkc]
   const float* g;  // phi_T taps g_alpha[L]
   float* part;
@@ -301,6 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
     {
       uint32_t tile_cnt = 0, s = 0, ph = 0;
       uint32_t use0 = 0, use1 = 0;  // per-accumulator-buffer use counters
+      long long w_y = 0, w_acc = 0, w_a = 0;
+      const long long t_start = clock64();
       const uint32_t idesc = idesc_tf32(p.Nt);
       const int ksteps = p.K8 / 8;
       // descriptor templates; per MMA only the 14-bit start-address field changes
@@ -309,16 +329,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
       const uint64_t dYl0 = sdesc(smem_u32(Ylo), p.colstride, 512, kLayoutSW128Base32B);
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
-          mbar_wait(y_ready, tile_cnt & 1);
+          mbar_wait_t(y_ready, tile_cnt & 1, w_y);
           tc_fence_after();
           for (int mb = 0; mb < p.n_mblk; ++mb) {
             const int ab = mb & 1;  // M-block parity fixes the TMEM buffer and the epilogue set
             const uint32_t use = ab ? use1++ : use0++;
-            mbar_wait(acc_empty + ab, (use + 1) & 1);
+            mbar_wait_t(acc_empty + ab, (use + 1) & 1, w_acc);
             tc_fence_after();
             const uint32_t d = tmem_base + (uint32_t)(ab * p.Nt);
             for (int st = 0; st < nst; ++st) {
-              mbar_wait(a_full + s, ph);
+              mbar_wait_t(a_full + s, ph, w_a);
               tc_fence_after();
               if (elect_one()) {
                 const uint64_t dst = dA0 + (uint64_t)((s * kStage) >> 4);
@@ -352,6 +372,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
           __syncwarp();
         }
       }
+      if (p.prof && lane == 0) {
+        atomicAdd(p.prof + 0, (unsigned long long)(clock64() - t_start));
+        atomicAdd(p.prof + 1, (unsigned long long)w_y);
+        atomicAdd(p.prof + 2, (unsigned long long)w_acc);
+        atomicAdd(p.prof + 3, (unsigned long long)w_a);
+      }
     }
   } else {
     // ===================== epilogue (warps 0..7) =====================
@@ -362,6 +388,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
     const int rloc = q * 16 + (lane & 15);   // complex row inside an M-block
     uint32_t tile_cnt = 0, use = 0;
     const int yfloats = ngroups * p.colstride / 4;
+    long long e_bar = 0, e_y = 0, e_split = 0, e_acc = 0, e_math = 0;
+    const long long e_start = clock64();
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int mpart = u % p.n_mpart;
       const int chunk = (u / p.n_mpart) % p.nchunks;
@@ -372,8 +400,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
 #pragma unroll
         for (int m = 0; m < NF / 2; ++m) accr[k][m] = make_float2(0.f, 0.f);
       for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
+        long long tb0 = clock64();
         named_bar(1, 256);  // every epilogue warp is done with the previous tile's W
-        mbar_wait(y_full, tile_cnt & 1);
+        e_bar += clock64() - tb0;
+        mbar_wait_t(y_full, tile_cnt & 1, e_y);
+        tb0 = clock64();
         // 3xTF32 split of the Y'' tile, in place (elementwise: layout-agnostic)
         for (int i = etid; i < yfloats; i += 256) {
           const float v = Yhi[i];
@@ -395,10 +426,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar(1, 256);
+        e_split += clock64() - tb0;
         if (etid == 0) mbar_arrive(y_ready);
         for (int mb = eset; mb < p.n_mblk; mb += 2, ++use) {
           const int ab = eset;
-          mbar_wait(acc_full + ab, use & 1);
+          mbar_wait_t(acc_full + ab, use & 1, e_acc);
+          const long long tm0 = clock64();
           tc_fence_after();
           const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * p.Nt);
           float2 part[NF / 2];
@@ -406,17 +439,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
           for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
           // re lane (i < 16) takes the even columns, im lane (i + 16) the odd ones
           const float2* wcol = reinterpret_cast<const float2*>(Wt) + (im ? NF / 2 : 0);
-          for (int c0 = 0; c0 < p.Nt; c0 += 16) {
+          for (int c0 = 0; c0 < p.Nt; c0 += 32) {
             if (p.expmode >= 2) break;
-            uint32_t v[16];
-            tmem_ld16(tb + c0, v);
+            uint32_t v[32];
+            tmem_ld32(tb + c0, v);
             tmem_wait_ld();
             if (p.expmode == 1) {
-              part[0].x += __uint_as_float(v[0] ^ v[15]);
+              part[0].x += __uint_as_float(v[0] ^ v[31]);
               continue;
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 16; ++j) {
               const float a = __uint_as_float(v[2 * j]), bb = __uint_as_float(v[2 * j + 1]);
               const float recv = __shfl_xor_sync(0xffffffffu, im ? a : bb, 16);
               const float own = im ? bb : a;
@@ -433,6 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty + ab);
+          e_math += clock64() - tm0;
 #pragma unroll
           for (int m = 0; m < NF / 2; ++m) {
             part[m].x += __shfl_xor_sync(0xffffffffu, part[m].x, 16);
@@ -465,6 +499,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
           }
         }
       }
+    }
+    if (p.prof && lane == 0) {
+      atomicAdd(p.prof + 4, (unsigned long long)(clock64() - e_start));
+      atomicAdd(p.prof + 5, (unsigned long long)e_bar);
+      atomicAdd(p.prof + 6, (unsigned long long)e_y);
+      atomicAdd(p.prof + 7, (unsigned long long)e_split);
+      atomicAdd(p.prof + 8, (unsigned long long)e_acc);
+      atomicAdd(p.prof + 9, (unsigned long long)e_math);
     }
   }
   tc_fence_before();
@@ -617,6 +659,11 @@ int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t s
       const char* e = std::getenv("JTFS_TC_EXPMODE");
       p.expmode = e ? std::atoi(e) : 0;
     }
+    static unsigned long long* prof = nullptr;
+    const bool do_prof = std::getenv("JTFS_TC_PROF") != nullptr;
+    if (do_prof && !prof) cudaMalloc(&prof, 16 * 8);
+    if (do_prof) cudaMemsetAsync(prof, 0, 16 * 8, st);
+    p.prof = do_prof ? prof : nullptr;
     p.g = P.d_g + d.g_off;
     p.part = part;
     p.part_off = d.part_off;
@@ -636,6 +683,17 @@ int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t s
     else if (NF == 16) tc::k_kd_tc<16, 4><<<grid, tc::kThreads, sm, st>>>(tmY, p);
     else tc::k_kd_tc<32, 2><<<grid, tc::kThreads, sm, st>>>(tmY, p);
     if (P.prof) cudaEventRecord(e1, st);
+    if (do_prof) {
+      unsigned long long h[16];
+      cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const double nm = (double)grid, ne = (double)grid * 8;
+      std::fprintf(stderr,
+                   "KDPROF alpha %zu Nt %d S %d | mma: total %.0f wait_y %.0f wait_acc %.0f wait_a %.0f | "
+                   "epi: total %.0f bar %.0f wait_y %.0f split %.0f wait_acc %.0f math %.0f (kcycles/CTA)\n",
+                   i, d.tc_Nt, d.tc_S, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
+                   h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3, h[8] / ne / 1e3, h[9] / ne / 1e3);
+    }
   }
   *err = 0;
   return (int)P.kd.size();
