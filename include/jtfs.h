@@ -187,7 +187,10 @@ JTFS_API jtfs_status jtfs_debug_filter(jtfs_plan_t plan, int32_t bank, int32_t i
  * 2 per frame per element).  flops[s]: the cheapest exact formulation of the
  * stage's arithmetic (for KD the FFT-along-lambda form); bytes[s]: the stage's
  * unavoidable HBM traffic (input + output of the whole path are charged to
- * KA / KS / KE).  Host query. */
+ * KA / KS / KE).  With cap >= 7, flops[6] is the tensor-core work KD actually
+ * executes per signal (real-embedded 3xTF32 contraction: 3 x 2 x (2M)(2K)L
+ * summed over alpha) and bytes[6] the A''/Y'' bytes KD stages into shared
+ * memory per signal.  Host query. */
 JTFS_API jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap);
 
 /* Stage profiling (tracing).  When enabled, jtfs_forward records a CUDA event

@@ -462,9 +462,19 @@ jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* x, int64_
 
 jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap) {
   if (!plan || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
-  double f[6], b[6];
+  double f[7], b[7];
   jtfs::stage_cost(plan->P, f, b);
-  for (int i = 0; i < std::min(cap, 6); ++i) {
+  // executed tensor work of the tcgen05 KD
+  const jtfs::Plan& P = plan->P;
+  f[6] = 0;
+  b[6] = 0;
+  for (const auto& d : P.kd) {
+    const double K8 = d.tc_K8, L = d.L, M2 = 2.0 * P.Mpad;
+    f[6] += 3.0 * 2.0 * M2 * K8 * L;
+    const double tiles = L / std::max(d.tc_Nt, 1);
+    b[6] += tiles * P.tc_n_mpart * (P.tc_n_mblk * (double)d.tc_nkc * 16384.0 + d.tc_ybytes);
+  }
+  for (int i = 0; i < std::min(cap, 7); ++i) {
     if (flops) flops[i] = f[i];
     if (bytes) bytes[i] = b[i];
   }

@@ -67,6 +67,12 @@ __device__ __forceinline__ CT rot16(CT a, int j) {
   return CxT<CT>::make(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
 }
 
+// Shared-memory index padding: one pad element after every 16 (breaks the bank
+// conflicts of the stride-R writes of the early Stockham passes).
+__host__ __device__ constexpr int padx(int e) { return e + (e >> 4); }
+// padded row stride for rows of length L (odd when >= 16, for column gathers)
+__host__ __device__ constexpr int pad_row(int L) { return L < 16 ? L : L + (L >> 4) + 1; }
+
 __host__ __device__ constexpr int bitrev(int v, int bits) {
   int r = 0;
   for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
@@ -98,16 +104,17 @@ __device__ __forceinline__ void dft_reg(CT (&v)[R]) {
   for (int r = 0; r < R; ++r) v[r] = t[r];
 }
 
-// One Stockham pass of radix R over G rows of length L held in smem s[g*LS + e].
+// One Stockham pass of radix R over G rows of length L held in smem s[g*LS + padx(e)].
+// W: the length-L twiddle table exp(-2 pi i t / L), t < L, staged in shared memory.
 template <int LOG2L, int R, int G, int NT, int DIR, int LS, class CT>
-__device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* __restrict__ W, int log2Ntw) {
+__device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* W) {
   constexpr int L = 1 << LOG2L;
   constexpr int LR = L / R;
   constexpr int NBF = G * LR;
   constexpr int BPT = (NBF + NT - 1) / NT;
   constexpr int LOG2R = ilog2c(R);
   const int Ns = 1 << log2Ns;
-  const int twshift = log2Ntw - (log2Ns + LOG2R);
+  const int twshift = LOG2L - (log2Ns + LOG2R);
   CT v[BPT][R];
   int base[BPT];
 #pragma unroll
@@ -118,44 +125,61 @@ __device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* __res
       const int g = bf / LR, j = bf % LR;
       const CT* row = s + g * LS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[i][r] = row[j + r * LR];
+      for (int r = 0; r < R; ++r) v[i][r] = row[padx(j + r * LR)];
       const int k = j & (Ns - 1);
       if (Ns > 1) {
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], twiddle<DIR>(W, (r * k) << twshift));
+        for (int r = 1; r < R; ++r) {
+          const CT w = W[(r * k) << twshift];
+          v[i][r] = cmul(v[i][r], DIR < 0 ? w : CxT<CT>::make(w.x, -w.y));
+        }
       }
       dft_reg<R, DIR>(v[i]);
-      base[i] = g * LS + (j - k) * R + k;
+      base[i] = g * LS + (j - k) * R + k;  // row start + unpadded offset of r = 0
     }
   }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < BPT; ++i) {
     if (base[i] >= 0) {
+      const int g = (threadIdx.x + i * NT) / LR;
+      const int e0 = base[i] - g * LS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) s[base[i] + r * Ns] = v[i][r];
+      for (int r = 0; r < R; ++r) s[g * LS + padx(e0 + r * Ns)] = v[i][r];
     }
   }
   __syncthreads();
 }
 
-// Full FFT of G rows in smem (caller has __syncthreads()'d after filling s).
-template <int LOG2L, int G, int NT, int DIR, int LS = (1 << LOG2L), class CT>
-__device__ __forceinline__ void fft_smem(CT* s, const CT* __restrict__ W, int log2Ntw) {
+// Stage the length-L twiddle table (contiguous in global memory) into shared memory.
+template <int LOG2L, int NT, class CT>
+__device__ __forceinline__ void stage_twiddles(CT* Ws, const CT* __restrict__ Wg) {
+#pragma unroll 4
+  for (int t = threadIdx.x; t < (1 << LOG2L); t += NT) Ws[t] = __ldg(Wg + t);
+}
+
+// Full FFT of G rows in smem (caller has __syncthreads()'d after filling s and the
+// shared twiddle table Ws of length L).
+template <int LOG2L, int G, int NT, int DIR, int LS = pad_row(1 << LOG2L), class CT>
+__device__ __forceinline__ void fft_smem(CT* s, const CT* Ws) {
   constexpr int REM = LOG2L % 3;
   int log2Ns = 0;
   if constexpr (REM != 0) {
-    stockham_pass<LOG2L, (1 << REM), G, NT, DIR, LS>(s, 0, W, log2Ntw);
+    stockham_pass<LOG2L, (1 << REM), G, NT, DIR, LS>(s, 0, Ws);
     log2Ns = REM;
   }
   if constexpr (LOG2L >= 3) {
 #pragma unroll 1
     for (int p = 0; p < LOG2L / 3; ++p) {
-      stockham_pass<LOG2L, 8, G, NT, DIR, LS>(s, log2Ns, W, log2Ntw);
+      stockham_pass<LOG2L, 8, G, NT, DIR, LS>(s, log2Ns, Ws);
       log2Ns += 3;
     }
   }
 }
+
+// offset of the length-L table inside the concatenated per-length twiddle tables
+// (lengths 2, 4, ..., 2^k stored back to back: offset(L) = L - 2)
+__host__ __device__ constexpr int tw_offset(int log2L) { return (1 << log2L) - 2; }
 
 }  // namespace dev
 }  // namespace jtfs

@@ -113,7 +113,7 @@ struct Plan {
   std::vector<float> W;                  // lambda pooling matrices per filter
   std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
                                          // then [N_fr] real phi_F taps, then [NPT] real phi_T taps
-  std::vector<float> twiddle;            // complex exp(-2 pi i t / N_tw), t < N_tw
+  std::vector<float> twiddle;            // per-length tables exp(-2 pi i t / L), L = 2..N_tw, at offset L - 2
   std::vector<double> twiddle64;         // the same in fp64 (KA)
   int N_tw = 0;
 

@@ -27,16 +27,25 @@ namespace dev {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ float2 fold_value(const float2* __restrict__ src, const FoldRow& d,
                                              const float* __restrict__ bandvals, int i, int L) {
-  float2 acc = make_float2(0.f, 0.f);
+  // first alias t0 = (i - m0) mod L handled without a loop (the common case has at
+  // most one alias, so the loads of several bins can be in flight together)
   int t = (i - d.m0) % L;
   if (t < 0) t += L;
-  for (; t < d.len; t += L) {
+  float2 acc = make_float2(0.f, 0.f);
+  if (t < d.len) {
     int p = d.m0 + t;
     if (p >= d.Lsrc) p -= d.Lsrc;
     const float2 x = src[d.src_off + p];
     const float f = __ldg(bandvals + d.band_off + t);
-    acc.x = fmaf(x.x, f, acc.x);
-    acc.y = fmaf(x.y, f, acc.y);
+    acc = make_float2(x.x * f, x.y * f);
+    for (t += L; t < d.len; t += L) {
+      p = d.m0 + t;
+      if (p >= d.Lsrc) p -= d.Lsrc;
+      const float2 y = src[d.src_off + p];
+      const float g = __ldg(bandvals + d.band_off + t);
+      acc.x = fmaf(y.x, g, acc.x);
+      acc.y = fmaf(y.y, g, acc.y);
+    }
   }
   return acc;
 }
@@ -112,22 +121,33 @@ struct ProbRealFwd {  // U1 (real) -> U1hat
 // single-CTA FFT of G rows per block
 // ---------------------------------------------------------------------------------
 template <int LOG2L, int G, int NT, int DIR, class P>
-__global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typename P::CT* __restrict__ W,
-                                                 int log2Ntw) {
+__global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typename P::CT* __restrict__ Wtab) {
   using CT = typename P::CT;
-  constexpr int L = 1 << LOG2L;
+  constexpr int L = 1 << LOG2L, LS = pad_row(L), EPT = G * L / NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* smem = reinterpret_cast<CT*>(smem_raw);
+  CT* Ws = smem + G * LS;
+  stage_twiddles<LOG2L, NT>(Ws, Wtab + tw_offset(LOG2L));
   const int rho0 = blockIdx.x * G;
-  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
-    const int g = idx / L, e = idx % L;
-    smem[idx] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : CxT<CT>::make(0, 0);
+  {
+    CT v[EPT];  // all global loads of this thread in flight together
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      v[i] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : CxT<CT>::make(0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      smem[g * LS + padx(e)] = v[i];
+    }
   }
   __syncthreads();
-  fft_smem<LOG2L, G, NT, DIR>(smem, W, log2Ntw);
-  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
-    const int g = idx / L, e = idx % L;
-    if (rho0 + g < nrows) prob.store(rho0 + g, e, smem[idx]);
+  fft_smem<LOG2L, G, NT, DIR, LS>(smem, Ws);
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+    if (rho0 + g < nrows) prob.store(rho0 + g, e, smem[g * LS + padx(e)]);
   }
 }
 
@@ -135,42 +155,50 @@ __global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typena
 template <int LOG2L, int G, int NT>
 __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restrict__ u1hat,
                                                  float* __restrict__ u1dbg, int nrows,
-                                                 const float2* __restrict__ W, int log2Ntw) {
-  constexpr int L = 1 << LOG2L;
+                                                 const float2* __restrict__ Wtab) {
+  constexpr int L = 1 << LOG2L, LS = pad_row(L), EPT = G * L / NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* smem = reinterpret_cast<float2*>(smem_raw);
+  float2* Ws = smem + G * LS;
+  stage_twiddles<LOG2L, NT>(Ws, Wtab + tw_offset(LOG2L));
   const int rho0 = blockIdx.x * G;
-  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
-    const int g = idx / L, e = idx % L;
-    smem[idx] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
-  }
-  __syncthreads();
-  fft_smem<LOG2L, G, NT, +1>(smem, W, log2Ntw);
-  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
-    const int g = idx / L;
-    const int rho = min(rho0 + g, nrows - 1);
-    const float sc = prob.rows[rho % prob.nrows].scale;
-    const float2 v = smem[idx];
-    smem[idx] = make_float2(sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc, 0.f);
-  }
-  __syncthreads();
-  if (u1dbg) {
-    for (int idx = threadIdx.x; idx < G * L; idx += NT) {
-      const int g = idx / L, e = idx % L;
-      const int rho = rho0 + g;
-      if (rho < nrows) {
-        const int b = rho / prob.nrows, r = rho % prob.nrows;
-        u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = smem[idx].x;
-      }
+  {
+    float2 v[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      v[i] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      smem[g * LS + padx(e)] = v[i];
     }
   }
-  fft_smem<LOG2L, G, NT, -1>(smem, W, log2Ntw);
-  for (int idx = threadIdx.x; idx < G * L; idx += NT) {
-    const int g = idx / L, e = idx % L;
+  __syncthreads();
+  fft_smem<LOG2L, G, NT, +1, LS>(smem, Ws);
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+    const int rho = min(rho0 + g, nrows - 1);
+    const float sc = prob.rows[rho % prob.nrows].scale;
+    const float2 v = smem[g * LS + padx(e)];
+    const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc;
+    smem[g * LS + padx(e)] = make_float2(u, 0.f);
+    if (u1dbg && rho0 + g < nrows) {
+      const int b = (rho0 + g) / prob.nrows, r = (rho0 + g) % prob.nrows;
+      u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = u;
+    }
+  }
+  __syncthreads();
+  fft_smem<LOG2L, G, NT, -1, LS>(smem, Ws);
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
     const int rho = rho0 + g;
     if (rho < nrows) {
       const int b = rho / prob.nrows, r = rho % prob.nrows;
-      u1hat[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = smem[idx];
+      u1hat[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = smem[g * LS + padx(e)];
     }
   }
 }
@@ -181,50 +209,82 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
 // ---------------------------------------------------------------------------------
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
 __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restrict__ tmp,
-                                               const typename P::CT* __restrict__ W, int log2Ntw) {
+                                               const typename P::CT* __restrict__ Wtab) {
   using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
-  constexpr int LS = La + 1;
+  constexpr int LS = pad_row(La), EPT = G * La / NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* smem = reinterpret_cast<CT*>(smem_raw);
+  CT* Ws = smem + G * LS;
+  stage_twiddles<LOG2A, NT>(Ws, Wtab + tw_offset(LOG2A));
+  const CT* WL = Wtab + tw_offset(LOG2A + LOG2B);  // exp(-2 pi i t / L) for the inter-pass twiddle
   constexpr int CPB = Lb / G;  // column groups per big row
   const int rho = blockIdx.x / CPB;
   const int nb0 = (blockIdx.x % CPB) * G;
-  for (int idx = threadIdx.x; idx < G * La; idx += NT) {
-    const int g = idx % G, na = idx / G;
-    smem[g * LS + na] = prob.load(rho, na * Lb + nb0 + g);
+  {
+    CT v[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx % G, na = idx / G;
+      v[i] = prob.load(rho, na * Lb + nb0 + g);
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx % G, na = idx / G;
+      smem[g * LS + padx(na)] = v[i];
+    }
   }
   __syncthreads();
-  fft_smem<LOG2A, G, NT, DIR, LS>(smem, W, log2Ntw);
+  fft_smem<LOG2A, G, NT, DIR, LS>(smem, Ws);
   CT* out = tmp + (int64_t)rho * L;
-  for (int idx = threadIdx.x; idx < G * La; idx += NT) {
-    const int g = idx % G, ka = idx / G;
-    const int u = (ka * (nb0 + g)) << (log2Ntw - (LOG2A + LOG2B));
-    out[ka * Lb + nb0 + g] = cmul(smem[g * LS + ka], twiddle<DIR>(W, u));
+  {
+    CT w[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx % G, ka = idx / G;
+      w[i] = twiddle<DIR>(WL, ka * (nb0 + g));
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx % G, ka = idx / G;
+      out[ka * Lb + nb0 + g] = cmul(smem[g * LS + padx(ka)], w[i]);
+    }
   }
 }
 
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
 __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __restrict__ tmp,
-                                               const typename P::CT* __restrict__ W, int log2Ntw) {
+                                               const typename P::CT* __restrict__ Wtab) {
   using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
-  constexpr int LS = Lb + 1;
+  constexpr int LS = pad_row(Lb), EPT = G * Lb / NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* smem = reinterpret_cast<CT*>(smem_raw);
+  CT* Ws = smem + G * LS;
+  stage_twiddles<LOG2B, NT>(Ws, Wtab + tw_offset(LOG2B));
   constexpr int RPB = La / G;
   const int rho = blockIdx.x / RPB;
   const int ka0 = (blockIdx.x % RPB) * G;
   const CT* in = tmp + (int64_t)rho * L;
-  for (int idx = threadIdx.x; idx < G * Lb; idx += NT) {
-    const int g = idx / Lb, e = idx % Lb;
-    smem[g * LS + e] = in[(ka0 + g) * Lb + e];
+  {
+    CT v[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / Lb, e = idx % Lb;
+      v[i] = in[(ka0 + g) * Lb + e];
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / Lb, e = idx % Lb;
+      smem[g * LS + padx(e)] = v[i];
+    }
   }
   __syncthreads();
-  fft_smem<LOG2B, G, NT, DIR, LS>(smem, W, log2Ntw);
-  for (int idx = threadIdx.x; idx < G * Lb; idx += NT) {
-    const int g = idx % G, kb = idx / G;
-    prob.store(rho, ka0 + g + La * kb, smem[g * LS + kb]);
+  fft_smem<LOG2B, G, NT, DIR, LS>(smem, Ws);
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int idx = threadIdx.x + i * NT, g = idx % G, kb = idx / G;
+    prob.store(rho, ka0 + g + La * kb, smem[g * LS + padx(kb)]);
   }
 }
 
@@ -530,27 +590,37 @@ template <int LOG2L>
 constexpr int rows_NT() { return (rows_G<LOG2L>() << LOG2L) / 8 < 32 ? 32 : (rows_G<LOG2L>() << LOG2L) / 8; }
 
 template <int LOG2L, int DIR, class P>
-void launch_rows(const P& prob, int nrows, const typename P::CT* W, int log2Ntw, cudaStream_t st) {
+void launch_rows(const P& prob, int nrows, const typename P::CT* W, int, cudaStream_t st) {
   constexpr int G = rows_G<LOG2L>();
   constexpr int NT = rows_NT<LOG2L>();
   const int grid = (nrows + G - 1) / G;
-  const size_t sm = (size_t)G * (1 << LOG2L) * sizeof(typename P::CT);
-  k_fft_rows<LOG2L, G, NT, DIR, P><<<grid, NT, sm, st>>>(prob, nrows, W, log2Ntw);
+  const size_t sm = ((size_t)G * pad_row(1 << LOG2L) + (1 << LOG2L)) * sizeof(typename P::CT);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_rows<LOG2L, G, NT, DIR, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  k_fft_rows<LOG2L, G, NT, DIR, P><<<grid, NT, sm, st>>>(prob, nrows, W);
 }
 
 template <int LOG2L>
-void launch_u1_fused(const ProbFold& prob, float2* u1hat, float* u1dbg, int nrows, const float2* W,
-                     int log2Ntw, cudaStream_t st) {
+void launch_u1_fused(const ProbFold& prob, float2* u1hat, float* u1dbg, int nrows, const float2* W, int,
+                     cudaStream_t st) {
   constexpr int G = rows_G<LOG2L>();
   constexpr int NT = rows_NT<LOG2L>();
   const int grid = (nrows + G - 1) / G;
-  const size_t sm = (size_t)G * (1 << LOG2L) * sizeof(float2);
-  k_u1_fused<LOG2L, G, NT><<<grid, NT, sm, st>>>(prob, u1hat, u1dbg, nrows, W, log2Ntw);
+  const size_t sm = ((size_t)G * pad_row(1 << LOG2L) + (1 << LOG2L)) * sizeof(float2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_u1_fused<LOG2L, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  k_u1_fused<LOG2L, G, NT><<<grid, NT, sm, st>>>(prob, u1hat, u1dbg, nrows, W);
 }
 
 template <int LOG2L, int DIR, class PA, class PB>
-void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, const typename PA::CT* W,
-                 int log2Ntw, cudaStream_t st) {
+void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, const typename PA::CT* W, int,
+                 cudaStream_t st) {
   using CT = typename PA::CT;
   constexpr int ELEMS = sizeof(CT) == 8 ? 4096 : 2048;  // 32 KiB of smem per CTA
   constexpr int LOG2A = (LOG2L + 1) / 2, LOG2B = LOG2L / 2;
@@ -559,9 +629,9 @@ void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, con
   constexpr int NT = ELEMS / 8;
   static_assert(GA >= 1 && GB >= 1 && GA <= Lb && GB <= La, "four-step tile");
   k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA>
-      <<<nbig * (Lb / GA), NT, (size_t)GA * (La + 1) * sizeof(CT), st>>>(pa, tmp, W, log2Ntw);
+      <<<nbig * (Lb / GA), NT, ((size_t)GA * pad_row(La) + La) * sizeof(CT), st>>>(pa, tmp, W);
   k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB>
-      <<<nbig * (La / GB), NT, (size_t)GB * (Lb + 1) * sizeof(CT), st>>>(pb, tmp, W, log2Ntw);
+      <<<nbig * (La / GB), NT, ((size_t)GB * pad_row(Lb) + Lb) * sizeof(CT), st>>>(pb, tmp, W);
 }
 
 template <class F>
@@ -628,7 +698,7 @@ int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int
   p.yphi = yphi;
   p.out = out;
   p.bandvals = P.d_bandvals;
-  p.W = (const float2*)P.d_twiddle;
+  p.W = (const float2*)P.d_twiddle + dev::tw_offset(ilog2_exact(P.N_tw));
   p.log2Ntw = ilog2_exact(P.N_tw);
   p.n1 = P.n1;
   p.NPT = P.NPT;

@@ -510,15 +510,24 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   P.path_filter.push_back(-1);
 
   // ---- twiddles exp(-2 pi i t / N_tw) ----
+  // per-length twiddle tables exp(-2 pi i t / L), t < L, for L = 2, 4, ..., N_pad,
+  // stored back to back (offset(L) = L - 2); plus the full-length table at the end
+  // for the scattered-index users (KS inverse DFT of NPT bins)
   P.N_tw = P.N_pad;
-  P.twiddle.resize((size_t)P.N_tw * 2);
-  P.twiddle64.resize((size_t)P.N_tw * 2);
-  for (int t = 0; t < P.N_tw; ++t) {
-    const auto w = unit_root(-(int64_t)t, P.N_tw);
-    P.twiddle[2 * t] = (float)w.real();
-    P.twiddle[2 * t + 1] = (float)w.imag();
-    P.twiddle64[2 * t] = w.real();
-    P.twiddle64[2 * t + 1] = w.imag();
+  const int lgN = ilog2_exact(P.N_tw);
+  const size_t nper = (size_t)2 * P.N_tw - 2;
+  P.twiddle.assign(2 * nper, 0.f);
+  P.twiddle64.assign(2 * nper, 0.0);
+  for (int lg = 1; lg <= lgN; ++lg) {
+    const int L = 1 << lg;
+    for (int t = 0; t < L; ++t) {
+      const auto w = unit_root(-(int64_t)t, L);
+      const size_t o = (size_t)(L - 2 + t);
+      P.twiddle[2 * o] = (float)w.real();
+      P.twiddle[2 * o + 1] = (float)w.imag();
+      P.twiddle64[2 * o] = w.real();
+      P.twiddle64[2 * o + 1] = w.imag();
+    }
   }
   return "";
 }

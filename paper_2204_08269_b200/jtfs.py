@@ -172,10 +172,12 @@ class Plan:
 
     def cost(self):
         """{stage: (algorithmic flops, bytes)} per signal (jtfs_cost)."""
-        f = (C.c_double * 6)()
-        b = (C.c_double * 6)()
-        _check(_lib.jtfs_cost(self._h, f, b, 6), "jtfs_cost")
-        return {STAGES[i]: (f[i], b[i]) for i in range(6)}
+        f = (C.c_double * 7)()
+        b = (C.c_double * 7)()
+        _check(_lib.jtfs_cost(self._h, f, b, 7), "jtfs_cost")
+        out = {STAGES[i]: (f[i], b[i]) for i in range(6)}
+        out["KD_tensor_executed"] = (f[6], b[6])
+        return out
 
     # ---- tracing ----
     def profile_enable(self, on: bool = True):
