@@ -66,7 +66,9 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   } while (0)
   UP(P.d_bandvals, P.bandvals.data(), P.bandvals.size() * 4);
   UP(P.d_A, P.A.data(), P.A.size() * 4);
-  UP(P.d_A2, P.A2.data(), P.A2.size() * 4);
+  UP(P.d_A16, P.A16.data(), P.A16.size() * 2);
+  UP(P.d_Ainv, P.Ainv.data(), P.Ainv.size() * 4);
+  UP(P.d_wtab, P.wtab.data(), P.wtab.size() * 4);
   UP(P.d_g, P.g.data(), P.g.size() * 4);
   UP(P.d_W, P.W.data(), P.W.size() * 4);
   UP(P.d_hphi, P.hphi.data(), P.hphi.size() * 4);
@@ -82,7 +84,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   UP(P.d_band_L1, P.band_phiT_L1.data(), P.band_phiT_L1.size() * sizeof(Band));
   {
     std::vector<DevAlpha> da;
-    for (const auto& d : P.kd) da.push_back(DevAlpha{d.nchunks, 0, d.part_off});
+    for (const auto& d : P.kd) da.push_back(DevAlpha{d.nslices, 0, d.part_off});
     UP(P.d_alphas, da.data(), da.size() * sizeof(DevAlpha));
   }
   {
@@ -116,7 +118,8 @@ jtfs_status upload_plan(jtfs::Plan& P) {
 
 struct WsPtrs {
   float2 *xhat, *tmp, *u1hat;
-  float *u1, *yphi, *y2, *part;
+  float *u1, *yphi, *y2, *ys, *part;
+  uint16_t* y16;
   int* flag;
 };
 
@@ -130,6 +133,8 @@ WsPtrs carve(const jtfs::Plan& P, void* ws, int64_t mb) {
   w.u1hat = (float2*)c; c += L.u1hat;
   w.yphi = (float*)c; c += L.yphi;
   w.y2 = (float*)c; c += L.y2;
+  w.y16 = (uint16_t*)c; c += L.y16;
+  w.ys = (float*)c; c += L.ys;
   w.part = (float*)c; c += L.part;
   w.flag = (int*)c;
   return w;
@@ -193,7 +198,7 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   {
     StageScope s(P, 4, st);
     int err = 0;
-    s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, nb, w.part, st, &err) : launch_kd(P, w.y2, nb, w.part, st));
+    s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, w.y16, w.ys, nb, w.part, st, &err) : launch_kd(P, w.y2, nb, w.part, st));
     if (err) return "tcgen05 KD: cuTensorMapEncodeTiled failed for the Y2 tensor map";
     if (std::getenv("JTFS_DEBUG_SYNC")) {
       cudaError_t e = cudaStreamSynchronize(st);
@@ -464,15 +469,16 @@ jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t ca
   if (!plan || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
   double f[7], b[7];
   jtfs::stage_cost(plan->P, f, b);
-  // executed tensor work of the tcgen05 KD
+  // executed tensor work of the tcgen05 KD (fp16 split: 3 products, re and im
+  // accumulators, K' padded to 16) and the bytes it stages through shared memory
   const jtfs::Plan& P = plan->P;
   f[6] = 0;
   b[6] = 0;
   for (const auto& d : P.kd) {
-    const double K8 = d.tc_K8, L = d.L, M2 = 2.0 * P.Mpad;
-    f[6] += 3.0 * 2.0 * M2 * K8 * L;
+    const double K16 = d.tc_K16, L = d.L, M = P.Mpad;
+    f[6] += 3.0 * 2.0 * 2.0 * M * K16 * L;
     const double tiles = L / std::max(d.tc_Nt, 1);
-    b[6] += tiles * P.tc_n_mpart * (P.tc_n_mblk * (double)d.tc_nkc * 16384.0 + d.tc_ybytes);
+    b[6] += tiles * P.tc_n_mpart * (P.tc_n_mblk * (double)d.tc_nkc * 16384.0 + 4.0 * d.tc_K16 * d.tc_Nt);
   }
   for (int i = 0; i < std::min(cap, 7); ++i) {
     if (flops) flops[i] = f[i];

@@ -59,10 +59,20 @@ struct AlphaKD {
   int chunk;        // time columns per KD work unit
   int nchunks;      // L / chunk
   int64_t part_off; // float offset of partials [nchunks][Mpad][n_frames] in one signal
-  // tensor-core (tcgen05) tiling, see kernels_tc.cu
-  int tc_K8 = 0, tc_Kst = 0, tc_nkc = 0, tc_nbox = 0, tc_BR = 0, tc_colstride = 0;
-  int tc_Nt = 0, tc_ybytes = 0, tc_S = 2, tc_tpu = 1;
-  int64_t tc_a2_off = 0;  // float offset of A''_alpha's 16 KiB chunk records in A2
+  // tensor-core (tcgen05 kind::f16, fp16 two-term split) tiling, see kernels_tc.cu
+  int tc_K2 = 0;        // K' = 2K real contraction length (planar Y rows)
+  int tc_K16 = 0;       // K' rounded up to the MMA K-step (16)
+  int tc_nkc = 0;       // 16-wide K chunks (A records per M-block)
+  int tc_nbr = 1, tc_BRk = 0;  // TMA row boxes / rows per box of the fp16 B tile
+  int tc_Nt = 0;        // time columns per tile (64 or 128)
+  int tc_NBB = 2;       // fp16 B-operand tile buffers
+  int tc_S = 2, tc_tpu = 1;
+  int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16
+  int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
+  int64_t y16_off = 0;  // fp16 offset of Y16_alpha [hi|lo][K16][L] in one signal's Y16 buffer (KY output)
+  int64_t ys_off = 0;   // float offset of the per-tile inverse Y scales (L / 64 slots) in one signal's ys
+  int64_t wtab_off = 0; // float offset of the phi_T taps table [L][NF] in wtab
+  int nslices = 0;      // KD partial slices per signal and alpha (time chunks x epilogue sets)
 };
 
 struct TmapBlob {
@@ -93,7 +103,7 @@ struct Plan {
   std::vector<AlphaKD> kd;       // active alphas in bank order
   int64_t y2_total = 0;          // complex elements of Y2 per signal
   int M = 0, Mpad = 0;           // joint-stage rows per alpha
-  int tc_n_mpart = 1, tc_n_mblk = 1;  // M-parts per KD work unit, 64-row M-blocks per part
+  int tc_n_mpart = 1, tc_n_mblk = 1;  // M-parts per KD work unit, 128-row M-blocks per part
   int kd_impl = 1;               // 1: tcgen05 (default), 0: SIMT (JTFS_KD=simt, validation)
   std::vector<FrFilter> fr;      // frequential filters: theta=-1 (beta), theta=+1 (beta), phi_F
   std::vector<jtfs_path_t> paths;
@@ -108,7 +118,10 @@ struct Plan {
   std::vector<FoldGroup> u1_groups;      // first-order IFFT rows grouped by L1
   std::vector<FoldGroup> y2_groups;      // second-order rows grouped by L_alpha
   std::vector<float> A;                  // complex interleaved A_alpha^T tables (SIMT KD)
-  std::vector<float> A2;                 // real-embedded A''_alpha, 3xTF32 split, pre-tiled/swizzled (tcgen05 KD)
+  std::vector<uint16_t> A16;             // A''_alpha re/im, row-scaled fp16 hi/lo, pre-tiled/swizzled (tcgen05 KD)
+  std::vector<float> Ainv;               // per alpha and row: 1 / (power-of-two row scale of A16)
+  std::vector<float> wtab;               // per alpha: phi_T taps per time column and frame [L][NF]
+  int64_t y16_total = 0, ys_total = 0;   // per signal: fp16 elements of Y16, per-tile scale slots
   std::vector<float> g;                  // time pooling taps per alpha
   std::vector<float> W;                  // lambda pooling matrices per filter
   std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
@@ -121,7 +134,9 @@ struct Plan {
   int device = -1;
   float* d_bandvals = nullptr;
   float* d_A = nullptr;
-  float* d_A2 = nullptr;
+  uint16_t* d_A16 = nullptr;
+  float* d_Ainv = nullptr;
+  float* d_wtab = nullptr;
   float* d_g = nullptr;
   float* d_W = nullptr;
   float* d_hphi = nullptr;
@@ -151,7 +166,7 @@ int ilog2_exact(int64_t v);  // -1 if not a power of two
 
 // workspace layout (per micro-batch of mb signals), in bytes
 struct WsLayout {
-  size_t xhat, tmp, u1, u1hat, yphi, y2, part, flag, total;
+  size_t xhat, tmp, u1, u1hat, yphi, y2, y16, ys, part, flag, total;
 };
 WsLayout ws_layout(const Plan& p, int64_t mb);
 

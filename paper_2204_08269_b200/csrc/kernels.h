@@ -56,7 +56,7 @@ int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_
 size_t ke_smem_bytes(const Plan& P);
 int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
 cudaError_t ke_set_smem(const Plan& P);
-int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, int* err);
+int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st, int* err);
 cudaError_t tc_setup_device(Plan& P);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 

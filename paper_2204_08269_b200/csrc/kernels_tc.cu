@@ -3,24 +3,37 @@
 // joint wavelet) fused with the complex modulus and phi_T pooling of
 // Eq. (3).
 //
-// Per active alpha, the exact frequential operator is the complex matrix
-// A[M][K] (plan.cpp).  Real embedding (rows re/im interleaved per TMEM quarter):
-//   D[128 lanes x Nt] += A''[128 x K'] * Y''[K' x Nt],   K' = 2K,
-//   Y'' rows 2l / 2l+1 = Re / Im Y2_alpha[l]  (KC writes Y2 planar),
-//   A'' row (lane q*32 + i): i < 16 -> Re, i >= 16 -> Im of complex row q*16 + i%16.
-// 3xTF32: D = A_hi Y_hi + A_hi Y_lo + A_lo Y_hi (hi = fp32 with the low 13
-// mantissa bits cleared, lo = x - hi exactly) keeps ~fp32 accuracy.
+// Per active alpha, the exact frequential operator is the complex matrix A[M][K]
+// (plan.cpp).  With Y'' the planar Y2_alpha tile (rows 2l / 2l+1 = Re / Im Y2[l],
+// K' = 2K rows, Nt time columns), two real products per 128-row M-block
+//   D_re[128 x Nt] = A_re''[128 x K'] Y'',   D_im[128 x Nt] = A_im''[128 x K'] Y''
+// give Re Z and Im Z of the same complex row in the same TMEM lane (columns
+// [0, Nt) and [Nt, 2Nt) of the block's accumulator), so the epilogue needs no
+// cross-lane exchange: |Z| = sqrt(D_re^2 + D_im^2) lane-locally.
 //
-// CTA = 10 warps, persistent over work units (signal, time chunk, M-part):
-//   warp 8      TMA producer: Y'' tile (MN-major, SWIZZLE_128B_BASE32B, loaded
-//               once per tile and reused by every M-block) + A'' K-records of 16
-//               (K-major, SWIZZLE_64B, pre-tiled; 2 per 32 KiB stage of an S-ring)
-//   warp 9      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 0..7  epilogue, two sets of 4; set s owns TMEM buffer s and the M-blocks
-//               mb = s, s+2, ...: tcgen05.ld -> re/im pairing by shuffle -> |Z| ->
-//               phi_T pooling at the retained frames (packed FFMA2) -> per-row
-//               accumulators in registers -> global partials at the end of a unit.
+// Arithmetic: kind::f16 with a two-term fp16 split of both operands,
+//   x s = hi + lo,  hi = rn16(x s),  lo = rn16(x s - hi),
+//   D = A_hi Y_hi + A_hi Y_lo + A_lo Y_hi   (fp32 accumulation in TMEM),
+// relative error ~2^-21 per product, like fp32 (precision budget).
+// The scales are powers of two (exact): s_m per A row (max |A''_m| s_m in
+// [2^13, 2^14), plan.cpp), s_Y per Y'' tile (max |Y''| s_Y in [2^13, 2^14), KY
+// below); |Z| = |D| / (s_m s_Y), applied to the pooled partials.
+//
+// KY (k_ky): Y2_alpha fp32 tiles -> s_Y and the fp16 hi / lo planes [2][K16][L].
+// KD (k_kd_tc): CTA = 11 warps (TMEM 512 columns), persistent over work units
+// (signal, time chunk, M-part), tiles of Nt columns inside a unit:
+//   warp 10     B producer: TMA of the fp16 hi / lo tile (MN-major SWIZZLE_128B,
+//               exactly the UMMA B image) + bulk copy of the tile's phi_T taps
+//   warp 8      A producer: A'' K-records (pre-tiled fp16 SWIZZLE_32B images, 16 KiB
+//               each, 2 per 32 KiB stage of an S-ring), lane s serves ring slot s
+//   warp 9      TMEM allocator + tcgen05.mma issuer (one elected lane)
+//   warps 0..7  epilogue, two sets of 4 warps; both sets take every M-block, set s
+//               the columns [s Nt/2, (s+1) Nt/2): tcgen05.ld (re, im) -> |Z| -> phi_T
+//               pooling at the retained frames (packed FFMA2) -> per-row
+//               accumulators in registers -> global partials [slice][Mpad][frames]
+//               at the end of a unit (slice = 2 chunk + set; KE sums the slices).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -88,6 +101,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // ---- bulk copy (non-tensor TMA): contiguous global -> smem, completes on an mbarrier ----
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -100,12 +122,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -131,15 +153,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// ties the loaded registers to a point after tcgen05.wait::ld (volatile asm order), so
+// the compiler cannot hoist their uses above the wait
+__device__ __forceinline__ void reg_fence16(uint32_t (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(v[i]));
+}
+__device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(v[i]));
+}
 
 // UMMA shared-memory descriptor (sm_100 version bit), lbo / sbo in bytes.
-//  A, K-major, SWIZZLE_64B (layout 4): 8-row x 64 B atoms, sbo = 512, lbo unused.
-//  B, MN-major tf32, SWIZZLE_128B_BASE32B (layout 1, Swizzle<2,5,2>): 4-row x 128 B
-//  atoms (32 MN elements), lbo = stride between 32-element MN groups, sbo = 512
-//  between 4-row K atoms.  (Plain SWIZZLE_128B MN-major tf32 reads as zeros on
-//  sm_100a -- found with tools/tc_unit.cu.)
-constexpr uint32_t kLayoutSW128Base32B = 1, kLayoutSW64 = 4;
-constexpr int kRec = 16384;    // one A'' K-record: 128 rows x 16 fp32, hi + lo (SWIZZLE_64B images)
+//  A, K-major fp16, SWIZZLE_32B (layout 6): 8-row x 32 B atoms, sbo = 256, lbo unused.
+//  B, MN-major fp16, SWIZZLE_128B (layout 2): 8 K-rows x 128 B atoms (64 MN
+//  elements), lbo = stride between 64-element MN groups, sbo = 1024 between 8-row
+//  K groups.  (Both verified bit-exact with tools/tc_unit16.cu.)
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW32 = 6;
+constexpr int kRec = 16384;    // one A'' K-record: 128 rows x 16 fp16 x {re_hi, re_lo, im_hi, im_lo}
+constexpr int kImg = 4096;     // one 128 x 16 fp16 image inside a record
 constexpr int kStage = 32768;  // one pipeline stage: up to two consecutive K-records
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
@@ -151,9 +183,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return d;
 }
 
-// instruction descriptor: kind::tf32, D f32, A K-major, B MN-major, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(n >> 3) << 17) |
+// instruction descriptor: kind::f16, D f32, A/B fp16, A K-major, B MN-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(128 >> 4) << 24);
 }
 
@@ -187,60 +219,188 @@ __device__ __forceinline__ bool elect_one() {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+
+// epilogue of 16 time columns of one M-block: |Z| from the lane's re / im
+// accumulators (packed FP32x2 squares), phi_T pooling into the NF frame partials
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  const unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
+  const unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ua), "l"(ub));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  const unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
+  const unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
+  const unsigned long long uc = *reinterpret_cast<unsigned long long*>(&c);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ua), "l"(ub), "l"(uc));
+  return *reinterpret_cast<float2*>(&r);
+}
+template <int NF>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&vr)[16], const uint32_t (&vi)[16], const float* wt,
+                                          float2 (&part)[NF / 2]) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 re = make_float2(__uint_as_float(vr[j]), __uint_as_float(vr[j + 1]));
+    const float2 im = make_float2(__uint_as_float(vi[j]), __uint_as_float(vi[j + 1]));
+    const float2 sq = ffma2v(im, im, fmul2(re, re));
+    const float mag[2] = {sqrt_fast(sq.x), sqrt_fast(sq.y)};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4* w4 = reinterpret_cast<const float4*>(wt + (j + h) * NF);
+#pragma unroll
+      for (int m4 = 0; m4 < NF / 4; ++m4) {
+        const float4 w = w4[m4];
+        part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mag[h], part[2 * m4 + 0]);
+        part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mag[h], part[2 * m4 + 1]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// KY: one CTA per (signal, tile): max |Y''| over the K' x Nt tile -> s_Y (power of
+// two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y - hi) into the
+// planes [hi | lo][K16][L] (rows >= K' zero), 1 / s_Y into ys[tile].
+// ---------------------------------------------------------------------------------
+struct KYParams {
+  const float* y2;     // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
+  int64_t y2_stride;
+  __half* y16;         // Y16 of signal 0 at alpha's offset; signal stride y16_stride halves
+  int64_t y16_stride;
+  float* ys;           // per-tile inverse scales of signal 0 at alpha's offset; stride ys_stride
+  int64_t ys_stride;
+  int K2, K16, L, Nt, ntiles;
+};
+
+__global__ void __launch_bounds__(256) k_ky(KYParams p) {
+  __shared__ uint32_t red[8];
+  const int b = blockIdx.x / p.ntiles, tile = blockIdx.x % p.ntiles;
+  const int t0 = tile * p.Nt;
+  const float* Y = p.y2 + (int64_t)b * p.y2_stride + t0;
+  const int nq = p.Nt / 4;
+  float mx = 0.f;
+  for (int i = threadIdx.x; i < p.K2 * nq; i += 256) {
+    const int k = i / nq, c = 4 * (i % nq);
+    const float4 v = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)k * p.L + c));
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  const uint32_t w = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+  __syncthreads();
+  uint32_t mbits = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mbits = max(mbits, red[i]);
+  int E = (int)(mbits >> 23) - 127;
+  E = max(E, -100);
+  const float s = __uint_as_float((uint32_t)(13 - E + 127) << 23);
+  if (threadIdx.x == 0) p.ys[(int64_t)b * p.ys_stride + tile] = __uint_as_float((uint32_t)(E - 13 + 127) << 23);
+  __half* hi = p.y16 + (int64_t)b * p.y16_stride + t0;
+  __half* lo = hi + (int64_t)p.K16 * p.L;
+  const int nh = p.Nt / 2;
+  for (int i = threadIdx.x; i < p.K16 * nh; i += 256) {
+    const int k = i / nh, c = 2 * (i % nh);
+    float2 v = make_float2(0.f, 0.f);
+    if (k < p.K2) v = __ldg(reinterpret_cast<const float2*>(Y + (int64_t)k * p.L + c));
+    v.x *= s;
+    v.y *= s;
+    const __half2 h = __floats2half2_rn(v.x, v.y);
+    const float2 hf = __half22float2(h);
+    *reinterpret_cast<__half2*>(hi + (int64_t)k * p.L + c) = h;
+    *reinterpret_cast<__half2*>(lo + (int64_t)k * p.L + c) = __floats2half2_rn(v.x - hf.x, v.y - hf.y);
+  }
+}
+
 struct TcParams {
-  int K8;        // K' = 2K rounded up to 8: rows of Y'' used
-  int nkc;       // 16-wide K chunks of A''
-  int Nt;        // time columns per tile (32..256)
-  int BR, nbox;  // TMA box rows, boxes per 32-column group
-  int colstride; // bytes between 32-column groups of the Y'' tile
-  int ybytes;    // bytes of one Y'' tile buffer (hi or lo)
-  int S;         // A ring stages
-  int tpu;       // tiles per work unit
-  int nchunks;   // time chunks per signal (L / (Nt * tpu))
-  int n_mpart, n_mblk;  // M-parts and 64-complex-row M-blocks per part
-  int L, D, frame0, nframes, Mpad;
+  int K16;         // B tile rows (K' rounded up to 16)
+  int nkc;         // 16-wide K chunks
+  int Nt;          // time columns per tile (64 or 128)
+  int BRk, nbr;    // B TMA box rows, row boxes per plane
+  int NBB;         // fp16 B tile buffers (1 or 2)
+  int nbuf;        // TMEM accumulator buffers (512 / (2 Nt))
+  int S;           // A ring stages
+  int tpu;         // tiles per work unit
+  int nchunks;     // time chunks per signal (L / (Nt * tpu))
+  int n_mpart, n_mblk;  // M-parts and 128-row M-blocks per part
+  int L, nframes, Mpad;
   int nsig;
-  int expmode;     // measurement only (JTFS_TC_EXPMODE): 1 skip epilogue math, 2 skip TMEM loads too
   unsigned long long* prof;  // measurement only (JTFS_TC_PROF): per-role wait-cycle counters or nullptr
-  const float* A;  // A''_alpha pre-tiled 16 KiB chunk records [2 Mpad / 128][nkc]
-  const float* g;  // phi_T taps g_alpha[L]
+  const uint16_t* A;   // A''_alpha records [Mpad / 128][nkc] x 16 KiB
+  const float* ainv;   // 1 / s_m per row [Mpad]
+  const float* wtab;   // phi_T taps [L][NF]
+  const float* ys;     // 1 / s_Y per (signal, tile): ys[b * ys_stride + tile]
+  int64_t ys_stride;
   float* part;
   int64_t part_off, part_stride;
 };
 
-constexpr int kThreads = 320;
-// warp roles: 0..7 epilogue, 8 TMA producer, 9 MMA issuer (highest warp id: the
-// issue arbiter favours high warp ids, so the single MMA thread is never starved)
-constexpr int kProdWarp = 8, kMmaWarp = 9;
+constexpr int kThreads = 352;
+// warp roles: 0..7 epilogue, 8 A producer, 9 MMA issuer, 10 B producer
+constexpr int kProdWarp = 8, kMmaWarp = 9, kBWarp = 10;
+
+// shared-memory carve-up (host and device agree through this function)
+struct SmemLayout {
+  uint32_t bhi[2], blo[2], ast, wt, bars, total;
+};
+__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int NF) {
+  SmemLayout l{};
+  auto up = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
+  uint32_t o = 0;
+  const uint32_t bsz = (uint32_t)(K16 * Nt * 2);  // one fp16 K16 x Nt image
+  for (int i = 0; i < 2; ++i) {
+    if (i < NBB) {
+      l.bhi[i] = o;
+      o = up(o + bsz, 1024);
+      l.blo[i] = o;
+      o = up(o + bsz, 1024);
+    } else {
+      l.bhi[i] = l.bhi[0];
+      l.blo[i] = l.blo[0];
+    }
+  }
+  l.ast = o;
+  o += (uint32_t)S * kStage;
+  l.wt = o;  // [2][Nt][NF]
+  o += (uint32_t)(2 * Nt * NF * 4);
+  l.bars = up(o, 8);
+  o = l.bars + 8 * (4 + 4 + 8 + 2 * S) + 16;
+  l.total = o + 1024;  // + alignment slack of the dynamic smem base
+  return l;
+}
 
 template <int NF, int MAXSLOT>
-__global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ CUtensorMap tmY, TcParams p) {
+__global__ void __launch_bounds__(kThreads, 1)
+    k_kd_tc(const __grid_constant__ CUtensorMap tmB, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  float* Yhi = reinterpret_cast<float*>(base);
-  float* Ylo = reinterpret_cast<float*>(base + p.ybytes);
-  uint8_t* Ast = base + 2 * p.ybytes;
-  float* Wt = reinterpret_cast<float*>(Ast + p.S * kStage);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Wt + p.Nt * NF);
-  uint64_t* y_full = bars + 0;
-  uint64_t* y_ready = bars + 1;
-  uint64_t* y_empty = bars + 2;
-  uint64_t* acc_full = bars + 3;   // [2]
-  uint64_t* acc_empty = bars + 5;  // [2]
-  uint64_t* a_full = bars + 7;     // [S]
-  uint64_t* a_empty = bars + 7 + p.S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * p.S);
+  const SmemLayout lay = smem_layout(p.K16, p.Nt, p.NBB, p.S, NF);
+  uint8_t* Ast = base + lay.ast;
+  float* Wt = reinterpret_cast<float*>(base + lay.wt);  // [2][Nt][NF]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + lay.bars);
+  uint64_t* b_full = bars + 0;      // [2] B tile landed
+  uint64_t* b_empty = bars + 2;     // [2] MMA done with the B tile
+  uint64_t* w_full = bars + 4;      // [2] taps landed
+  uint64_t* w_empty = bars + 6;     // [2] epilogue done with the taps
+  uint64_t* acc_full = bars + 8;    // [4]
+  uint64_t* acc_empty = bars + 12;  // [4]
+  uint64_t* a_full = bars + 16;     // [S]
+  uint64_t* a_empty = bars + 16 + p.S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * p.S);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(y_full, 1);
-    mbar_init(y_ready, 1);
-    mbar_init(y_empty, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(b_full + i, 1);
+      mbar_init(b_empty + i, 1);
+      mbar_init(w_full + i, 1);
+      mbar_init(w_empty + i, 8);
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(acc_full + i, 1);
-      mbar_init(acc_empty + i, 4);
+      mbar_init(acc_empty + i, 8);
     }
     for (int i = 0; i < p.S; ++i) {
       mbar_init(a_full + i, 1);
@@ -259,56 +419,59 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
   const uint32_t tmem_base = *tmem_slot;
 
   const int units = p.nsig * p.nchunks * p.n_mpart;
-  const int ngroups = p.Nt / 32;
   const int nst = (p.nkc + 1) / 2;  // A'' stages (<= 2 records of 16 K-columns) per M-block
+  // the CTA's tile sequence: unit u = blockIdx.x + i * gridDim.x, tile 0..tpu-1
+  const int my_units = (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int my_tiles = my_units * p.tpu;
 
-  if (warp == kProdWarp) {
-    // ===================== TMA producer =====================
+  if (warp == kBWarp) {
+    // ===================== B producer: fp16 hi / lo tile + taps =====================
+    if (lane == 0) {
+      const uint32_t btx = (uint32_t)(2 * p.K16 * p.Nt * 2);
+      const uint32_t wbytes = (uint32_t)(p.Nt * NF * 4);
+      for (int gt = 0; gt < my_tiles; ++gt) {
+        const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
+        const int chunk = (u / p.n_mpart) % p.nchunks, b = u / (p.n_mpart * p.nchunks);
+        const int t0 = (chunk * p.tpu + gt % p.tpu) * p.Nt;
+        const int wi = gt & 1, bi = gt % p.NBB;
+        mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
+        mbar_expect_tx(w_full + wi, wbytes);
+        bulk_load(Wt + wi * p.Nt * NF, p.wtab + (size_t)t0 * NF, wbytes, w_full + wi);
+        mbar_wait(b_empty + bi, (uint32_t)((gt / p.NBB) + 1) & 1u);
+        mbar_expect_tx(b_full + bi, btx);
+        for (int h = 0; h < 2; ++h) {
+          uint8_t* dst = base + (h ? lay.blo[bi] : lay.bhi[bi]);
+          for (int cg = 0; cg < p.Nt / 64; ++cg)
+            for (int rb = 0; rb < p.nbr; ++rb)
+              tma_load_4d(dst + cg * (p.K16 * 128) + rb * (p.BRk * 128), &tmB, b_full + bi, t0 + cg * 64,
+                          rb * p.BRk, h, b);
+        }
+      }
+    }
+  } else if (warp == kProdWarp) {
+    // ===================== A producer =====================
     // Bulk copies issued by one thread complete one after another (~600 cycles
-    // each, measured with tools/bulk_bw.cu), so kIssuers lanes issue in parallel:
-    // A'' stage j goes through lane j % kIssuers; the Y'' boxes are spread too.
-    // Issuer lanes must divide S so that every ring slot is always served by the
-    // same lane (parity waits cannot tell laps apart).
-    const int kIssuers = (p.S % 4 == 0) ? 4 : (p.S % 3 == 0) ? 3 : (p.S % 2 == 0) ? 2 : 1;
-    if (lane < kIssuers) {
-      uint32_t tile_cnt = 0, j = 0, s = 0, ph = 0;
-      const uint32_t ytx = (uint32_t)(ngroups * p.nbox * p.BR * 128);
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    // each, measured with tools/bulk_bw.cu), so lane s serves ring slot s (S lanes
+    // issue in parallel; a slot is always served by the same lane, which keeps its
+    // parity waits unambiguous).
+    if (lane < p.S) {
+      uint32_t j = 0, s = 0, ph = 0;
+      for (int gt = 0; gt < my_tiles; ++gt) {
+        const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
         const int mpart = u % p.n_mpart;
-        const int chunk = (u / p.n_mpart) % p.nchunks;
-        const int b = u / (p.n_mpart * p.nchunks);
-        for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
-          mbar_wait(y_empty, (tile_cnt + 1) & 1);
-          const int t0 = (chunk * p.tpu + tile) * p.Nt;
-          if (p.expmode >= 4) {  // measurement only: no Y'' load
-            if (lane == 0) mbar_arrive(y_full);
-          } else {
-            if (lane == 0) mbar_expect_tx(y_full, ytx);
-            __syncwarp((1u << kIssuers) - 1);
-            for (int i = lane; i < ngroups * p.nbox; i += kIssuers) {
-              const int cg = i / p.nbox, bx = i % p.nbox;
-              tma_load_3d(reinterpret_cast<uint8_t*>(Yhi) + cg * p.colstride + bx * p.BR * 128, &tmY, y_full,
-                          t0 + cg * 32, bx * p.BR, b);
+        for (int mb = 0; mb < p.n_mblk; ++mb) {
+          const uint16_t* arec = p.A + (size_t)(mpart * p.n_mblk + mb) * p.nkc * (kRec / 2);
+          for (int st = 0; st < nst; ++st) {
+            if ((int)s == lane) {
+              mbar_wait(a_empty + s, ph ^ 1);
+              const uint32_t bytes = (uint32_t)(min(2, p.nkc - 2 * st) * kRec);
+              mbar_expect_tx(a_full + s, bytes);
+              bulk_load(Ast + s * kStage, arec + (size_t)(2 * st) * (kRec / 2), bytes, a_full + s);
             }
-          }
-          for (int mb = 0; mb < p.n_mblk; ++mb) {
-            const float* arec = p.A + (size_t)(mpart * p.n_mblk + mb) * p.nkc * (kRec / 4);
-            for (int st = 0; st < nst; ++st) {
-              if ((int)(j % kIssuers) == lane) {
-                mbar_wait(a_empty + s, ph ^ 1);
-                if (p.expmode >= 3) {  // measurement only: no A'' load
-                  mbar_arrive(a_full + s);
-                } else {
-                  const uint32_t bytes = (uint32_t)(min(2, p.nkc - 2 * st) * kRec);
-                  mbar_expect_tx(a_full + s, bytes);
-                  bulk_load(Ast + s * kStage, arec + (size_t)(2 * st) * (kRec / 4), bytes, a_full + s);
-                }
-              }
-              ++j;
-              if (++s == (uint32_t)p.S) {
-                s = 0;
-                ph ^= 1;
-              }
+            ++j;
+            if (++s == (uint32_t)p.S) {
+              s = 0;
+              ph ^= 1;
             }
           }
         }
@@ -316,185 +479,138 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (warp-wide loop, one elected lane issues) =====================
-    {
-      uint32_t tile_cnt = 0, s = 0, ph = 0;
-      uint32_t use0 = 0, use1 = 0;  // per-accumulator-buffer use counters
-      long long w_y = 0, w_acc = 0, w_a = 0;
-      const long long t_start = clock64();
-      const uint32_t idesc = idesc_tf32(p.Nt);
-      const int ksteps = p.K8 / 8;
-      // descriptor templates; per MMA only the 14-bit start-address field changes
-      const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 512, kLayoutSW64);
-      const uint64_t dYh0 = sdesc(smem_u32(Yhi), p.colstride, 512, kLayoutSW128Base32B);
-      const uint64_t dYl0 = sdesc(smem_u32(Ylo), p.colstride, 512, kLayoutSW128Base32B);
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
-          mbar_wait_t(y_ready, tile_cnt & 1, w_y);
+    uint32_t s = 0, ph = 0, cnt = 0;
+    long long w_b = 0, w_acc = 0, w_a = 0;
+    const long long t_start = clock64();
+    const uint32_t idesc = idesc_f16(p.Nt);
+    const uint32_t colstride = (uint32_t)(p.K16 * 128);
+    const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 256, kLayoutSW32);
+    for (int gt = 0; gt < my_tiles; ++gt) {
+      const int bi = gt % p.NBB;
+      mbar_wait_t(b_full + bi, (uint32_t)(gt / p.NBB) & 1u, w_b);
+      tc_fence_after();
+      const uint64_t dBh = sdesc(smem_u32(base + lay.bhi[bi]), colstride, 1024, kLayoutSW128);
+      const uint64_t dBl = sdesc(smem_u32(base + lay.blo[bi]), colstride, 1024, kLayoutSW128);
+      for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
+        const uint32_t ab = cnt % (uint32_t)p.nbuf, use = cnt / (uint32_t)p.nbuf;
+        mbar_wait_t(acc_empty + ab, (use + 1) & 1, w_acc);
+        tc_fence_after();
+        const uint32_t d_re = tmem_base + ab * 2u * (uint32_t)p.Nt;
+        const uint32_t d_im = d_re + (uint32_t)p.Nt;
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait_t(a_full + s, ph, w_a);
           tc_fence_after();
-          for (int mb = 0; mb < p.n_mblk; ++mb) {
-            const int ab = mb & 1;  // M-block parity fixes the TMEM buffer and the epilogue set
-            const uint32_t use = ab ? use1++ : use0++;
-            mbar_wait_t(acc_empty + ab, (use + 1) & 1, w_acc);
-            tc_fence_after();
-            const uint32_t d = tmem_base + (uint32_t)(ab * p.Nt);
-            for (int st = 0; st < nst; ++st) {
-              mbar_wait_t(a_full + s, ph, w_a);
-              tc_fence_after();
-              if (elect_one()) {
-                const uint64_t dst = dA0 + (uint64_t)((s * kStage) >> 4);
+          if (elect_one()) {
+            const uint64_t dst = dA0 + (uint64_t)((s * kStage) >> 4);
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                  const uint64_t ah = dst + (uint64_t)((r * kRec) >> 4);
-                  const uint64_t al = ah + (uint64_t)((kRec / 2) >> 4);
-#pragma unroll
-                  for (int ks = 0; ks < 2; ++ks) {
-                    const int kstep = 4 * st + 2 * r + ks;
-                    if (kstep < ksteps) {
-                      const uint64_t ko = (uint64_t)((ks * 32) >> 4), yo = (uint64_t)((kstep * 1024) >> 4);
-                      mma_tf32(d, ah + ko, dYh0 + yo, idesc, kstep > 0 ? 1u : 0u);
-                      mma_tf32(d, ah + ko, dYl0 + yo, idesc, 1u);
-                      mma_tf32(d, al + ko, dYh0 + yo, idesc, 1u);
-                    }
-                  }
-                }
-                mma_commit(a_empty + s);
-              }
-              __syncwarp();
-              if (++s == (uint32_t)p.S) {
-                s = 0;
-                ph ^= 1;
+            for (int r = 0; r < 2; ++r) {
+              const int kc = 2 * st + r;
+              if (kc < p.nkc) {
+                const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
+                const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
+                const uint32_t acc0 = kc > 0 ? 1u : 0u;
+                mma_f16(d_re, a + (0 * kImg >> 4), dBh + yo, idesc, acc0);
+                mma_f16(d_re, a + (0 * kImg >> 4), dBl + yo, idesc, 1u);
+                mma_f16(d_re, a + (1 * kImg >> 4), dBh + yo, idesc, 1u);
+                mma_f16(d_im, a + (2 * kImg >> 4), dBh + yo, idesc, acc0);
+                mma_f16(d_im, a + (2 * kImg >> 4), dBl + yo, idesc, 1u);
+                mma_f16(d_im, a + (3 * kImg >> 4), dBh + yo, idesc, 1u);
               }
             }
-            if (elect_one()) mma_commit(acc_full + ab);
-            __syncwarp();
+            mma_commit(a_empty + s);
           }
-          if (elect_one()) mma_commit(y_empty);
           __syncwarp();
+          if (++s == (uint32_t)p.S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
+        if (elect_one()) mma_commit(acc_full + ab);
+        __syncwarp();
       }
-      if (p.prof && lane == 0) {
-        atomicAdd(p.prof + 0, (unsigned long long)(clock64() - t_start));
-        atomicAdd(p.prof + 1, (unsigned long long)w_y);
-        atomicAdd(p.prof + 2, (unsigned long long)w_acc);
-        atomicAdd(p.prof + 3, (unsigned long long)w_a);
-      }
+      if (elect_one()) mma_commit(b_empty + bi);
+      __syncwarp();
+    }
+    if (p.prof && lane == 0) {
+      atomicAdd(p.prof + 0, (unsigned long long)(clock64() - t_start));
+      atomicAdd(p.prof + 1, (unsigned long long)w_b);
+      atomicAdd(p.prof + 2, (unsigned long long)w_acc);
+      atomicAdd(p.prof + 3, (unsigned long long)w_a);
     }
   } else {
     // ===================== epilogue (warps 0..7) =====================
-    const int etid = threadIdx.x;            // 0..255
-    const int eset = warp >> 2;              // TMEM accumulator buffer handled
-    const int q = warp & 3;                  // TMEM lane quarter (warp_id % 4)
-    const bool im = lane >= 16;
-    const int rloc = q * 16 + (lane & 15);   // complex row inside an M-block
-    uint32_t tile_cnt = 0, use = 0;
-    const int yfloats = ngroups * p.colstride / 4;
-    long long e_bar = 0, e_y = 0, e_split = 0, e_acc = 0, e_math = 0;
+    const int eset = warp >> 2;  // column half
+    const int q = warp & 3;      // TMEM lane quarter (warp_id % 4)
+    const int cbeg = eset * (p.Nt / 2);
+    long long e_w = 0, e_acc = 0, e_math = 0;
     const long long e_start = clock64();
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    uint32_t cnt = 0;
+    float2 accr[MAXSLOT][NF / 2];  // pooled partials of my rows (one per M-block of the part)
+    for (int gt = 0; gt < my_tiles; ++gt) {
+      const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
       const int mpart = u % p.n_mpart;
-      const int chunk = (u / p.n_mpart) % p.nchunks;
-      const int b = u / (p.n_mpart * p.nchunks);
-      float2 accr[MAXSLOT][NF / 2];  // pooled partials of my rows (M-blocks eset, eset+2, ...)
+      const int chunk = (u / p.n_mpart) % p.nchunks, b = u / (p.n_mpart * p.nchunks);
+      const int tile = gt % p.tpu;
+      if (tile == 0) {
 #pragma unroll
-      for (int k = 0; k < MAXSLOT; ++k)
+        for (int k = 0; k < MAXSLOT; ++k)
 #pragma unroll
-        for (int m = 0; m < NF / 2; ++m) accr[k][m] = make_float2(0.f, 0.f);
-      for (int tile = 0; tile < p.tpu; ++tile, ++tile_cnt) {
-        long long tb0 = clock64();
-        named_bar(1, 256);  // every epilogue warp is done with the previous tile's W
-        e_bar += clock64() - tb0;
-        mbar_wait_t(y_full, tile_cnt & 1, e_y);
-        tb0 = clock64();
-        // 3xTF32 split of the Y'' tile, in place (elementwise: layout-agnostic)
-        for (int i = etid; i < yfloats; i += 256) {
-          const float v = Yhi[i];
-          const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-          Yhi[i] = h;
-          Ylo[i] = v - h;
-        }
-        // phi_T pooling taps of this tile, stored [c][NF/2 re-lane pairs | NF/2 im-lane pairs]
-        const int t0 = (chunk * p.tpu + tile) * p.Nt;
-        for (int i = etid; i < p.Nt * NF; i += 256) {
-          const int c = i / NF, m = i % NF;
-          float w = 0.f;
-          if (m < p.nframes) {
-            int t = ((p.frame0 + m) * p.D - (t0 + c)) % p.L;
-            if (t < 0) t += p.L;
-            w = __ldg(p.g + t);
-          }
-          Wt[i] = w;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        named_bar(1, 256);
-        e_split += clock64() - tb0;
-        if (etid == 0) mbar_arrive(y_ready);
-        for (int mb = eset; mb < p.n_mblk; mb += 2, ++use) {
-          const int ab = eset;
-          mbar_wait_t(acc_full + ab, use & 1, e_acc);
-          const long long tm0 = clock64();
-          tc_fence_after();
-          const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * p.Nt);
-          float2 part[NF / 2];
-#pragma unroll
-          for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
-          // re lane (i < 16) takes the even columns, im lane (i + 16) the odd ones
-          const float2* wcol = reinterpret_cast<const float2*>(Wt) + (im ? NF / 2 : 0);
-          for (int c0 = 0; c0 < p.Nt; c0 += 32) {
-            if (p.expmode >= 2) break;
-            uint32_t v[32];
-            tmem_ld32(tb + c0, v);
-            tmem_wait_ld();
-            if (p.expmode == 1) {
-              part[0].x += __uint_as_float(v[0] ^ v[31]);
-              continue;
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float a = __uint_as_float(v[2 * j]), bb = __uint_as_float(v[2 * j + 1]);
-              const float recv = __shfl_xor_sync(0xffffffffu, im ? a : bb, 16);
-              const float own = im ? bb : a;
-              const float mag = sqrt_fast(fmaf(own, own, recv * recv));
-              const float4* w4 = reinterpret_cast<const float4*>(wcol + (c0 + 2 * j) * (NF / 2));
-#pragma unroll
-              for (int m4 = 0; m4 < NF / 4; ++m4) {
-                const float4 w = w4[m4];
-                part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mag, part[2 * m4 + 0]);
-                part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mag, part[2 * m4 + 1]);
-              }
-            }
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(acc_empty + ab);
-          e_math += clock64() - tm0;
-#pragma unroll
-          for (int m = 0; m < NF / 2; ++m) {
-            part[m].x += __shfl_xor_sync(0xffffffffu, part[m].x, 16);
-            part[m].y += __shfl_xor_sync(0xffffffffu, part[m].y, 16);
-          }
-          const int slot = mb >> 1;
-#pragma unroll
-          for (int k = 0; k < MAXSLOT; ++k)
-            if (k == slot) {
-#pragma unroll
-              for (int m = 0; m < NF / 2; ++m)
-                accr[k][m] = make_float2(accr[k][m].x + part[m].x, accr[k][m].y + part[m].y);
-            }
-        }
+          for (int m = 0; m < NF / 2; ++m) accr[k][m] = make_float2(0.f, 0.f);
       }
-      // unit done: my rows' pooled partials of this time chunk -> global
-      if (!im) {
+      const int wi = gt & 1;
+      mbar_wait_t(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
+      const float inv = __ldg(p.ys + (int64_t)b * p.ys_stride + chunk * p.tpu + tile);
+      const float* wt = Wt + wi * p.Nt * NF + cbeg * NF;
+#pragma unroll 1
+      for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
+        const uint32_t ab = cnt % (uint32_t)p.nbuf;
+        mbar_wait_t(acc_full + ab, (cnt / (uint32_t)p.nbuf) & 1u, e_acc);
+        const long long tm0 = clock64();
+        tc_fence_after();
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ab * 2u * (uint32_t)p.Nt + (uint32_t)cbeg;
+        float2 part[NF / 2];
+#pragma unroll
+        for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
+        const int half = p.Nt / 2;
+        for (int c0 = 0; c0 < half; c0 += 16) {
+          uint32_t vr[16], vi[16];
+          tmem_ld16(tb + c0, vr);
+          tmem_ld16(tb + p.Nt + c0, vi);
+          tmem_wait_ld();
+          reg_fence16(vr);
+          reg_fence16(vi);
+          if (c0 + 16 >= half) {  // last read of this buffer: hand it back to the MMA
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty + ab);
+          }
+          epi_chunk<NF>(vr, vi, wt + c0 * NF, part);
+        }
+        e_math += clock64() - tm0;
+#pragma unroll
+        for (int k = 0; k < MAXSLOT; ++k)
+          if (k == mb) {
+#pragma unroll
+            for (int m = 0; m < NF / 2; ++m)
+              accr[k][m] = make_float2(fmaf(part[m].x, inv, accr[k][m].x), fmaf(part[m].y, inv, accr[k][m].y));
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(w_empty + wi);  // this warp is done with the tile's taps
+      if (tile == p.tpu - 1) {
+        // unit done: my rows' pooled partials of this (time chunk, column half) slice
         float* dst = p.part + (int64_t)b * p.part_stride + p.part_off +
-                     ((int64_t)chunk * p.Mpad + (int64_t)mpart * p.n_mblk * 64) * p.nframes;
+                     (int64_t)(2 * chunk + eset) * p.Mpad * p.nframes;
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k) {
-          const int mb = 2 * k + eset;
-          if (mb < p.n_mblk) {
-            float* d = dst + (int64_t)(mb * 64 + rloc) * p.nframes;
+          if (k < p.n_mblk) {
+            const int row = (mpart * p.n_mblk + k) * 128 + q * 32 + lane;
+            const float ia = __ldg(p.ainv + row);
+            float* d = dst + (int64_t)row * p.nframes;
 #pragma unroll
             for (int m = 0; m < NF / 2; ++m) {
-              if (2 * m < p.nframes) d[2 * m] = accr[k][m].x;
-              if (2 * m + 1 < p.nframes) d[2 * m + 1] = accr[k][m].y;
+              if (2 * m < p.nframes) d[2 * m] = accr[k][m].x * ia;
+              if (2 * m + 1 < p.nframes) d[2 * m + 1] = accr[k][m].y * ia;
             }
           }
         }
@@ -502,11 +618,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_kd_tc(const __grid_constant__ C
     }
     if (p.prof && lane == 0) {
       atomicAdd(p.prof + 4, (unsigned long long)(clock64() - e_start));
-      atomicAdd(p.prof + 5, (unsigned long long)e_bar);
-      atomicAdd(p.prof + 6, (unsigned long long)e_y);
-      atomicAdd(p.prof + 7, (unsigned long long)e_split);
-      atomicAdd(p.prof + 8, (unsigned long long)e_acc);
-      atomicAdd(p.prof + 9, (unsigned long long)e_math);
+      atomicAdd(p.prof + 5, (unsigned long long)e_w);
+      atomicAdd(p.prof + 6, (unsigned long long)e_acc);
+      atomicAdd(p.prof + 7, (unsigned long long)e_math);
     }
   }
   tc_fence_before();
@@ -540,66 +654,63 @@ PFN_encodeTiled get_encoder() {
   return fn;
 }
 
-bool encode(CUtensorMap* m, void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-            const cuuint32_t* box, CUtensorMapSwizzle swz) {
+bool encode(CUtensorMap* m, CUtensorMapDataType dt, void* base, int rank, const cuuint64_t* dims,
+            const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle swz) {
   PFN_encodeTiled fn = get_encoder();
   if (!fn) return false;
-  cuuint32_t es[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, dt, rank, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-size_t tc_smem(const AlphaKD& d, int nf) {
-  return 1024 + 2 * (size_t)d.tc_ybytes + (size_t)d.tc_S * tc::kStage + (size_t)d.tc_Nt * nf * 4 +
-         8 * (7 + 2 * d.tc_S) + 16;
-}
 int nf_of(int nframes) { return nframes <= 8 ? 8 : nframes <= 16 ? 16 : 32; }
+size_t tc_smem(const AlphaKD& d, int nf) {
+  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, d.tc_S, nf).total;
+}
 }  // namespace
 
-// choose the per-alpha tensor-core tiling (called by build_plan): the widest
-// Y'' tile (Nt, power of two <= 256) that leaves room for >= 3 A'' stages, then as
-// many 16 KiB A'' stages as fit (<= 8)
+// choose the per-alpha tensor-core tiling (called by build_plan): the first of
+// (Nt, B buffers, min stages) = (128, 2, 3), (128, 1, 3), (128, 2, 2), (128, 1, 2),
+// (64, 2, 3), (64, 1, 2) that fits, then as many A'' stages as fit (<= 6)
 void plan_tc(Plan& P) {
   const int NF = nf_of(P.n_frames);
   const size_t budget = 227 * 1024;
-  P.tc_n_mblk = P.Mpad / 64 / P.tc_n_mpart;
+  P.tc_n_mblk = P.Mpad / 128 / P.tc_n_mpart;
   // tuning overrides (measurement only): largest tile width / number of A'' stages
   const char* e_nt = std::getenv("JTFS_TC_NTMAX");
   const char* e_s = std::getenv("JTFS_TC_SMAX");
-  const int nt_max = e_nt ? std::max(32, std::atoi(e_nt)) : 256;
+  const int nt_max = e_nt ? std::max(64, std::atoi(e_nt)) : 128;
   const int s_max = e_s ? std::max(2, std::min(6, std::atoi(e_s))) : 6;
   for (auto& d : P.kd) {
-    const int K2 = 2 * d.K;
-    d.tc_K8 = (K2 + 7) / 8 * 8;
-    d.tc_Kst = (K2 + 15) / 16 * 16;
-    d.tc_nkc = d.tc_Kst / 16;
-    d.tc_nbox = (d.tc_K8 + 127) / 128;
-    d.tc_BR = (d.tc_K8 + d.tc_nbox * 8 - 1) / (d.tc_nbox * 8) * 8;
-    d.tc_colstride = d.tc_nbox * d.tc_BR * 128;
-    int Nt = std::min(nt_max, d.L);
-    for (; Nt > 32; Nt /= 2) {
-      d.tc_Nt = Nt;
-      d.tc_ybytes = (Nt / 32) * d.tc_colstride;
-      d.tc_S = 2;
-      if (tc_smem(d, NF) <= budget) break;
+    d.tc_K2 = 2 * d.K;
+    d.tc_K16 = (d.tc_K2 + 15) / 16 * 16;
+    d.tc_nkc = d.tc_K16 / 16;
+    d.tc_nbr = (d.tc_K16 + 255) / 256;
+    d.tc_BRk = (d.tc_K16 / d.tc_nbr + 7) / 8 * 8;
+    bool ok = false;
+    const int cand[6][3] = {{128, 2, 3}, {128, 1, 3}, {128, 2, 2}, {128, 1, 2}, {64, 2, 3}, {64, 1, 2}};
+    for (const auto& c : cand) {
+      if (c[0] > nt_max || c[0] > d.L) continue;
+      d.tc_Nt = c[0];
+      d.tc_NBB = c[1];
+      d.tc_S = c[2];
+      if (tc_smem(d, NF) > budget) continue;
+      while (d.tc_S < s_max && tc_smem(d, NF) + tc::kStage <= budget) ++d.tc_S;
+      ok = true;
+      break;
     }
-    d.tc_Nt = Nt;
-    d.tc_ybytes = (Nt / 32) * d.tc_colstride;
-    d.tc_S = 2;
-    while (d.tc_S < s_max && tc_smem(d, NF) + tc::kStage <= budget) ++d.tc_S;
-    if (d.tc_S == 5) d.tc_S = 4;  // issuer lanes must divide S (kernels_tc.cu producer)
     // time chunk per work unit: the largest power of two <= 4096 that still gives
     // about 4 units per SM for a full micro-batch (partials are per chunk)
-    {
+    if (ok) {
       int64_t target = (int64_t)P.mb * P.tc_n_mpart * d.L / (4 * 148);
       int ch = 4096;
-      while (ch > Nt && ch > target) ch /= 2;
+      while (ch > d.tc_Nt && ch > target) ch /= 2;
       d.chunk = std::min(ch, d.L);
-      if (d.chunk < Nt) d.chunk = Nt;
+      if (d.chunk < d.tc_Nt) d.chunk = d.tc_Nt;
       d.nchunks = d.L / d.chunk;
+      d.tc_tpu = d.chunk / d.tc_Nt;
     }
-    d.tc_tpu = d.chunk / Nt;
-    if (d.L < 32 || d.chunk % Nt || tc_smem(d, NF) > budget) P.kd_impl = 0;
+    if (!ok || d.L < 64 || d.chunk % d.tc_Nt || d.tc_nbr * d.tc_BRk < d.tc_K16) P.kd_impl = 0;
   }
 }
 
@@ -612,11 +723,11 @@ cudaError_t tc_setup_device(Plan& P) {
   else if (NF == 16)
     e = cudaFuncSetAttribute(tc::k_kd_tc<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
   else e = cudaFuncSetAttribute(tc::k_kd_tc<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  if (e != cudaSuccess) return e;
-  return cudaSuccess;
+  return e;
 }
 
-int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, int* err) {
+int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st,
+                 int* err) {
   const int NF = nf_of(P.n_frames);
   int sms = 148;
   {
@@ -624,47 +735,62 @@ int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t s
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  int launches = 0;
   for (size_t i = 0; i < P.kd.size(); ++i) {
     const auto& d = P.kd[i];
-    CUtensorMap tmY;
-    cuuint64_t dims[3] = {(cuuint64_t)d.L, (cuuint64_t)(2 * d.K), (cuuint64_t)nsig};
-    cuuint64_t strides[2] = {(cuuint64_t)d.L * 4, (cuuint64_t)(2 * P.y2_total) * 4};
-    cuuint32_t box[3] = {32, (cuuint32_t)d.tc_BR, 1};
-    if (!encode(&tmY, const_cast<float*>(y2) + 2 * d.y2_off, 3, dims, strides, box,
-                CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) {
+    // ---- KY: fp16 split of the Y'' tiles ----
+    {
+      tc::KYParams q{};
+      q.y2 = y2 + 2 * d.y2_off;
+      q.y2_stride = 2 * P.y2_total;
+      q.y16 = reinterpret_cast<__half*>(y16) + d.y16_off;
+      q.y16_stride = P.y16_total;
+      q.ys = ys + d.ys_off;
+      q.ys_stride = P.ys_total;
+      q.K2 = d.tc_K2;
+      q.K16 = d.tc_K16;
+      q.L = d.L;
+      q.Nt = d.tc_Nt;
+      q.ntiles = d.L / d.tc_Nt;
+      tc::k_ky<<<nsig * q.ntiles, 256, 0, st>>>(q);
+      ++launches;
+    }
+    CUtensorMap tmB;
+    cuuint64_t dims[4] = {(cuuint64_t)d.L, (cuuint64_t)d.tc_K16, 2, (cuuint64_t)nsig};
+    cuuint64_t strides[3] = {(cuuint64_t)d.L * 2, (cuuint64_t)d.tc_K16 * d.L * 2, (cuuint64_t)P.y16_total * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)d.tc_BRk, 1, 1};
+    if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 4, dims, strides, box,
+                CU_TENSOR_MAP_SWIZZLE_128B)) {
       *err = 1;
-      return (int)i;
+      return launches;
     }
     tc::TcParams p{};
-    p.K8 = d.tc_K8;
-    p.nkc = (d.tc_K8 + 15) / 16;
+    p.K16 = d.tc_K16;
+    p.nkc = d.tc_nkc;
     p.Nt = d.tc_Nt;
-    p.BR = d.tc_BR;
-    p.nbox = d.tc_nbox;
-    p.colstride = d.tc_colstride;
-    p.ybytes = d.tc_ybytes;
+    p.BRk = d.tc_BRk;
+    p.nbr = d.tc_nbr;
+    p.NBB = d.tc_NBB;
+    p.nbuf = 512 / (2 * d.tc_Nt);
     p.S = d.tc_S;
     p.tpu = d.tc_tpu;
     p.nchunks = d.nchunks;
     p.n_mpart = P.tc_n_mpart;
     p.n_mblk = P.tc_n_mblk;
     p.L = d.L;
-    p.D = d.D;
-    p.frame0 = P.frame0;
     p.nframes = P.n_frames;
     p.Mpad = P.Mpad;
     p.nsig = nsig;
-    p.A = P.d_A2 + d.tc_a2_off;
-    {
-      const char* e = std::getenv("JTFS_TC_EXPMODE");
-      p.expmode = e ? std::atoi(e) : 0;
-    }
+    p.A = P.d_A16 + d.tc_a16_off;
+    p.ainv = P.d_Ainv + d.tc_ainv_off;
+    p.wtab = P.d_wtab + d.wtab_off;
+    p.ys = ys + d.ys_off;
+    p.ys_stride = P.ys_total;
     static unsigned long long* prof = nullptr;
     const bool do_prof = std::getenv("JTFS_TC_PROF") != nullptr;
     if (do_prof && !prof) cudaMalloc(&prof, 16 * 8);
     if (do_prof) cudaMemsetAsync(prof, 0, 16 * 8, st);
     p.prof = do_prof ? prof : nullptr;
-    p.g = P.d_g + d.g_off;
     p.part = part;
     p.part_off = d.part_off;
     p.part_stride = P.part_total;
@@ -679,9 +805,10 @@ int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t s
       cudaEventRecord(e0, st);
       P.prof_kd[i].push_back({(void*)e0, (void*)e1});
     }
-    if (NF == 8) tc::k_kd_tc<8, 9><<<grid, tc::kThreads, sm, st>>>(tmY, p);
-    else if (NF == 16) tc::k_kd_tc<16, 4><<<grid, tc::kThreads, sm, st>>>(tmY, p);
-    else tc::k_kd_tc<32, 2><<<grid, tc::kThreads, sm, st>>>(tmY, p);
+    if (NF == 8) tc::k_kd_tc<8, 9><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+    else if (NF == 16) tc::k_kd_tc<16, 4><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+    else tc::k_kd_tc<32, 2><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+    ++launches;
     if (P.prof) cudaEventRecord(e1, st);
     if (do_prof) {
       unsigned long long h[16];
@@ -689,14 +816,14 @@ int launch_kd_tc(Plan& P, const float* y2, int nsig, float* part, cudaStream_t s
       cudaStreamSynchronize(st);
       const double nm = (double)grid, ne = (double)grid * 8;
       std::fprintf(stderr,
-                   "KDPROF alpha %zu Nt %d S %d | mma: total %.0f wait_y %.0f wait_acc %.0f wait_a %.0f | "
-                   "epi: total %.0f bar %.0f wait_y %.0f split %.0f wait_acc %.0f math %.0f (kcycles/CTA)\n",
-                   i, d.tc_Nt, d.tc_S, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
-                   h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3, h[8] / ne / 1e3, h[9] / ne / 1e3);
+                   "KDPROF alpha %zu Nt %d NBB %d S %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
+                   "epi: total %.0f wait_w %.0f wait_acc %.0f math %.0f (kcycles/CTA)\n",
+                   i, d.tc_Nt, d.tc_NBB, d.tc_S, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
+                   h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3);
     }
   }
   *err = 0;
-  return (int)P.kd.size();
+  return launches;
 }
 
 }  // namespace jtfs

@@ -16,6 +16,35 @@
 namespace jtfs {
 
 namespace {
+// IEEE binary16 round-to-nearest-even of a double (host side, for the A'' tables)
+uint16_t half_rn(double v) {
+  const uint16_t sign = std::signbit(v) ? 0x8000 : 0;
+  double a = std::fabs(v);
+  if (a == 0) return sign;
+  if (a >= 65520.0) return sign | 0x7C00;  // overflow -> inf (never reached: |v| < 2^14)
+  int e = std::ilogb(a);
+  if (e < -14) {  // subnormal: units of 2^-24
+    const double q = std::nearbyint(a * 16777216.0);  // ties-to-even in the default mode
+    return sign | (uint16_t)q;                         // q == 1024 rolls into the first normal
+  }
+  double m = std::ldexp(a, -e) * 1024.0;  // [1024, 2048)
+  double q = std::nearbyint(m);
+  if (q == 2048.0) {
+    q = 1024.0;
+    ++e;
+  }
+  if (e > 15) return sign | 0x7C00;
+  return sign | (uint16_t)((e + 15) << 10) | (uint16_t)((int)q - 1024);
+}
+double half_to_double(uint16_t h) {
+  const int e = (h >> 10) & 31, f = h & 1023;
+  const double v = e == 0 ? std::ldexp((double)f, -24) : std::ldexp((double)(f + 1024), e - 25);
+  return (h & 0x8000) ? -v : v;
+}
+}  // namespace
+
+
+namespace {
 constexpr double kSigma0 = 0.1;             // sigma_phi = 0.1 / T        (R4)
 constexpr double kAlphaC = 5.0;             // critical-rate support rule (R5)
 constexpr double kEpsBand = 1e-9;           // spectral band truncation (relative to peak)
@@ -340,16 +369,15 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     P.M += f.nrows;
   }
   {
-    // M-blocks of 64 complex rows, split into M-parts so that one part's pooled
-    // row accumulators fit the tcgen05 kernel's shared memory (<= 36 KiB)
-    // M-blocks per part: 2 * MAXSLOT register-resident row accumulators per
-    // epilogue thread in kernels_tc.cu (NF 8: 9 slots, 16: 4, 32: 2)
+    // M-blocks of 128 complex rows (one TMEM lane each), split into M-parts so that
+    // one part's pooled row accumulators stay in the tcgen05 epilogue's registers:
+    // <= MAXSLOT M-blocks per part (kernels_tc.cu: NF 8: 9, 16: 4, 32: 2)
     const int n_frames_pad = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
-    const int max_mblk = n_frames_pad == 8 ? 18 : n_frames_pad == 16 ? 8 : 4;
-    const int mblocks = (P.M + 63) / 64;
+    int max_mblk = n_frames_pad == 8 ? 9 : n_frames_pad == 16 ? 4 : 2;
+    const int mblocks = (P.M + 127) / 128;
     P.tc_n_mpart = (mblocks + max_mblk - 1) / max_mblk;
     P.tc_n_mblk = (mblocks + P.tc_n_mpart - 1) / P.tc_n_mpart;
-    P.Mpad = P.tc_n_mblk * P.tc_n_mpart * 64;
+    P.Mpad = P.tc_n_mblk * P.tc_n_mpart * 128;
     const char* e = std::getenv("JTFS_KD");
     P.kd_impl = (e && std::strcmp(e, "simt") == 0) ? 0 : 1;
   }
@@ -388,58 +416,64 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       }
     }
   }
-  // real-embedded A''_alpha for the tensor cores: row (mb*128 + q*32 + i) is
-  // Re (i < 16) or Im (i >= 16) of complex row mb*64 + q*16 + i%16 (one TMEM lane
-  // quarter per q); column 2l / 2l+1 multiplies Re / Im Y2[l]; 3xTF32 hi/lo split.
-  // Stored pre-tiled for one cp.async.bulk per pipeline stage: for every
-  // (128-row block, 16-column K chunk) a 16 KiB record [hi 8 KiB | lo 8 KiB], each
-  // half in the UMMA K-major SWIZZLE_64B image (8-row x 64 B atoms, Swizzle<2,4,3>).
-  P.A2.clear();
+  // A''_alpha for the tensor cores (kernels_tc.cu): for complex row m and Y'' row
+  // k' = 2l + c (c = 0: Re Y2[l], c = 1: Im Y2[l]),
+  //   A_re''[m][2l] =  Re A[m][l],  A_re''[m][2l+1] = -Im A[m][l]   (Re Z = Ar Yr - Ai Yi)
+  //   A_im''[m][2l] =  Im A[m][l],  A_im''[m][2l+1] =  Re A[m][l]   (Im Z = Ai Yr + Ar Yi)
+  // Each row is scaled by a power of two s_m (max |entry| * s_m in [2^13, 2^14)) and
+  // split into fp16 hi = rn(a s_m), lo = rn(a s_m - hi); Ainv holds 1 / s_m.
+  // Stored pre-tiled for cp.async.bulk: per (128-row M-block, 16-wide K chunk) one
+  // 16 KiB record [re_hi | re_lo | im_hi | im_lo], each a 4 KiB UMMA K-major
+  // SWIZZLE_32B image (8-row x 32 B atoms, 16 B chunk index ^= row bit 2).
+  P.A16.clear();
+  P.Ainv.clear();
   for (auto& d : P.kd) {
-    const int nkc = (2 * d.K + 15) / 16;
-    const int nblk = 2 * P.Mpad / 128;
-    d.tc_a2_off = (int64_t)P.A2.size();
-    const size_t base = P.A2.size();
-    P.A2.resize(base + (size_t)nblk * nkc * 4096, 0.f);
+    const int K2 = 2 * d.K;
+    const int nkc = (K2 + 15) / 16;
+    const int nblk = P.Mpad / 128;
+    d.tc_a16_off = (int64_t)P.A16.size();
+    d.tc_ainv_off = (int64_t)P.Ainv.size();
+    const size_t base = P.A16.size();
+    P.A16.resize(base + (size_t)nblk * nkc * 8192, 0);
+    P.Ainv.resize(P.Ainv.size() + P.Mpad, 1.f);
     std::vector<int> row_f(P.Mpad, -1), row_i(P.Mpad, 0);
     for (size_t fi = 0; fi < P.fr.size(); ++fi)
       for (int i = 0; i < P.fr[fi].nrows; ++i) {
         row_f[P.fr[fi].row0 + i] = (int)fi;
         row_i[P.fr[fi].row0 + i] = i;
       }
-    auto split = [](double v, float& hi, float& lo) {
-      const float f = (float)v;
-      uint32_t u;
-      std::memcpy(&u, &f, 4);
-      u &= 0xFFFFE000u;
-      std::memcpy(&hi, &u, 4);
-      lo = (float)(v - (double)hi);
+    auto put = [&](int m, int img, int col, uint16_t h) {
+      const int mb = m / 128, r = m % 128, kc = col / 16, kk = col % 16;
+      const uint32_t o = (uint32_t)((r / 8) * 256 + (r % 8) * 32 + kk * 2);
+      const uint32_t sw = o ^ (((o >> 7) & 1u) << 4);
+      P.A16[base + ((size_t)mb * nkc + kc) * 8192 + (size_t)img * 2048 + sw / 2] = h;
     };
-    auto put = [&](int blk, int R, int col, float hi, float lo) {
-      const int kc = col / 16, kk = col % 16;
-      const uint32_t o = (uint32_t)((R / 8) * 512 + (R % 8) * 64 + kk * 4);
-      const uint32_t sw = o ^ (((o >> 7) & 3u) << 4);
-      const size_t rec = base + ((size_t)blk * nkc + kc) * 4096;
-      P.A2[rec + sw / 4] = hi;
-      P.A2[rec + 2048 + sw / 4] = lo;
-    };
-    for (int Rg = 0; Rg < 2 * P.Mpad; ++Rg) {
-      const int mb = Rg / 128, l = Rg % 128, q = l / 32, i = l % 32;
-      const int r = mb * 64 + q * 16 + (i & 15);
-      const bool re = i < 16;
-      if (row_f[r] < 0) continue;
-      const auto& f = P.fr[row_f[r]];
-      const int rp = f.rprime[row_i[r]];
+    std::vector<std::complex<double>> arow(d.K);
+    for (int m = 0; m < P.Mpad; ++m) {
+      if (row_f[m] < 0) continue;
+      const auto& f = P.fr[row_f[m]];
+      const int rp = f.rprime[row_i[m]];
+      double amax = 0;
       for (int lam = 0; lam < d.K; ++lam) {
         const int idx = (((rp << f.k) - lam) % P.N_fr + P.N_fr) % P.N_fr;
-        const auto a = htap[row_f[r]][idx];
-        const double c0 = re ? a.real() : a.imag();   // multiplies Re Y
-        const double c1 = re ? -a.imag() : a.real();  // multiplies Im Y
-        float hi, lo;
-        split(c0, hi, lo);
-        put(mb, l, 2 * lam, hi, lo);
-        split(c1, hi, lo);
-        put(mb, l, 2 * lam + 1, hi, lo);
+        arow[lam] = htap[row_f[m]][idx];
+        amax = std::max(amax, std::max(std::abs(arow[lam].real()), std::abs(arow[lam].imag())));
+      }
+      if (amax == 0) continue;
+      const int E = std::ilogb(amax);            // amax in [2^E, 2^(E+1))
+      const double s = std::ldexp(1.0, 13 - E);  // amax * s in [2^13, 2^14)
+      P.Ainv[d.tc_ainv_off + m] = (float)std::ldexp(1.0, E - 13);
+      for (int lam = 0; lam < d.K; ++lam) {
+        const double ar = arow[lam].real() * s, ai = arow[lam].imag() * s;
+        const double v[4] = {ar, -ai, ai, ar};  // re: (2l, 2l+1), im: (2l, 2l+1)
+        for (int t = 0; t < 4; ++t) {
+          const int img = (t / 2) * 2;            // 0: re, 2: im  (+1 for lo)
+          const int col = 2 * lam + (t % 2);
+          const uint16_t h = half_rn(v[t]);
+          const uint16_t l = half_rn(v[t] - half_to_double(h));
+          put(m, img, col, h);
+          put(m, img + 1, col, l);
+        }
       }
     }
   }
@@ -460,6 +494,33 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     d.chunk = std::min(d.L, 4096);   // refined by plan_tc (work units per launch)
     d.nchunks = d.L / d.chunk;
   }
+  // KY output (fp16 hi/lo planes, rows padded to 16), per-tile scale slots (tiles
+  // of >= 64 columns) and the phi_T taps table [L][NF] of the tensor-core KD
+  {
+    const int NF = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
+    P.y16_total = 0;
+    P.ys_total = 0;
+    P.wtab.clear();
+    for (auto& d : P.kd) {
+      const int K16 = (2 * d.K + 15) / 16 * 16;
+      d.y16_off = P.y16_total;
+      P.y16_total += (int64_t)2 * K16 * d.L;
+      d.ys_off = P.ys_total;
+      P.ys_total += std::max(1, d.L / 64);
+      d.wtab_off = (int64_t)P.wtab.size();
+      const float* g = P.g.data() + d.g_off;
+      for (int t = 0; t < d.L; ++t)
+        for (int m = 0; m < NF; ++m) {
+          float w = 0.f;
+          if (m < P.n_frames) {
+            int64_t i = ((int64_t)(P.frame0 + m) * d.D - t) % d.L;
+            if (i < 0) i += d.L;
+            w = g[i];
+          }
+          P.wtab.push_back(w);
+        }
+    }
+  }
   // micro-batch: keep one micro-batch's workspace around <= 4 GiB (partials are small)
   P.part_total = 0;
   {
@@ -469,8 +530,9 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   plan_tc(P);
   P.part_total = 0;
   for (auto& d : P.kd) {
+    d.nslices = d.nchunks * (P.kd_impl == 1 ? 2 : 1);  // tcgen05 KD: one slice per epilogue set
     d.part_off = P.part_total;
-    P.part_total += (int64_t)d.nchunks * P.Mpad * P.n_frames;
+    P.part_total += (int64_t)d.nslices * P.Mpad * P.n_frames;
   }
   // phi_t paths: psi_{beta,+1} taps (complex), phi_F taps (real), phi_T taps at rate T (real)
   P.hphi.clear();
@@ -547,9 +609,15 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   w.u1hat = al((size_t)mb * p.u1_total * 8);
   w.yphi = al((size_t)mb * p.n1 * p.NPT * 4);
   w.y2 = al((size_t)mb * p.y2_total * 8);
-  w.part = al((size_t)mb * p.part_total * 4);
+  w.y16 = al((size_t)mb * p.y16_total * 2);
+  w.ys = al((size_t)mb * p.ys_total * 4);
+  // partials: upper bound before plan_tc has fixed the slices (2 per time chunk)
+  int64_t part_total = p.part_total;
+  if (part_total == 0)
+    for (const auto& d : p.kd) part_total += (int64_t)2 * d.nchunks * p.Mpad * p.n_frames;
+  w.part = al((size_t)mb * part_total * 4);
   w.flag = 256;
-  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.part + w.flag;
+  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.flag;
   return w;
 }
 
