@@ -521,11 +521,15 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
         }
     }
   }
-  // micro-batch: keep one micro-batch's workspace around <= 4 GiB (partials are small)
+  // micro-batch: one micro-batch's workspace <= 16 GiB (HBM is 180 GB; larger
+  // micro-batches mean fewer launches and better-balanced KD grids).  The KD
+  // partials depend on the chunking plan_tc picks for this micro-batch; they are
+  // small next to Y2, so size first without them and shrink if needed.
+  const size_t ws_budget = (size_t)16 << 30;
   P.part_total = 0;
   {
     const size_t per = ws_layout(P, 1).total;
-    P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ((size_t)4 << 30) / std::max<size_t>(per, 1)));
+    P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ws_budget / std::max<size_t>(per, 1)));
   }
   plan_tc(P);
   P.part_total = 0;
@@ -534,6 +538,8 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     d.part_off = P.part_total;
     P.part_total += (int64_t)d.nslices * P.Mpad * P.n_frames;
   }
+  while (P.mb > 1 && ws_layout(P, P.mb).total > ws_budget) --P.mb;
+
   // phi_t paths: psi_{beta,+1} taps (complex), phi_F taps (real), phi_T taps at rate T (real)
   P.hphi.clear();
   for (int b = 0; b < nb; ++b)
@@ -611,11 +617,7 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   w.y2 = al((size_t)mb * p.y2_total * 8);
   w.y16 = al((size_t)mb * p.y16_total * 2);
   w.ys = al((size_t)mb * p.ys_total * 4);
-  // partials: upper bound before plan_tc has fixed the slices (2 per time chunk)
-  int64_t part_total = p.part_total;
-  if (part_total == 0)
-    for (const auto& d : p.kd) part_total += (int64_t)2 * d.nchunks * p.Mpad * p.n_frames;
-  w.part = al((size_t)mb * part_total * 4);
+  w.part = al((size_t)mb * p.part_total * 4);
   w.flag = 256;
   w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.flag;
   return w;
