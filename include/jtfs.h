@@ -49,6 +49,7 @@ typedef enum {
 
 /* flags */
 #define JTFS_CHECK_FINITE 1u   /* forward scans x for NaN/Inf first (one device sync) */
+#define JTFS_LATENCY 2u        /* size KD work units for one signal per forward (c4, path sharding) */
 
 /* pad modes (reading R6) */
 #define JTFS_PAD_REFLECT 0     /* numpy 'reflect' to N_pad = 2N, centred */
@@ -68,7 +69,7 @@ typedef struct jtfs_plan_s* jtfs_plan_t;  /* opaque; immutable after creation */
  *   average_fr  1: Eq. (3) (Phi_{T,F}); 0: Eq. (4) (Phi_T only)
  *   pad_mode    JTFS_PAD_REFLECT or JTFS_PAD_PERIODIC
  *   device      CUDA device ordinal; -1 = host-only plan (queries only, no forward)
- *   flags       JTFS_CHECK_FINITE
+ *   flags       JTFS_CHECK_FINITE | JTFS_LATENCY
  */
 typedef struct {
   int32_t N, J, Q, Q2, T, J_fr, Q_fr, F;
@@ -158,6 +159,49 @@ JTFS_API jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, in
                               float* out_host, float* x_dev, float* out_dev,
                               void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Path sharding of one forward over several GPUs (
+ * DESIGN.md §7).  The joint stage's frequential contraction + modulus + phi_T
+ * pooling (Eq. (3)) is a sum over time of per-(alpha, time chunk)
+ * contributions, so KD's work splits into units (alpha, time chunk) whose
+ * pooled partial slices are additive and disjoint.  A rank runs the replicated
+ * first stages (Eqs. (1)-(2): KA..KC, and S0/S1) plus KD for its own units;
+ * the ranks' partial buffers are summed (each slice is nonzero on exactly one
+ * rank, so the sum is exact), and one rank finishes Eq. (3)'s phi_F pooling and
+ * packing with jtfs_reduce_pack.  The result is byte-identical to jtfs_forward. */
+
+typedef struct {
+  int32_t alpha;   /* index of the active alpha (KD order = path order of jtfs_paths) */
+  int32_t chunk;   /* time chunk of that alpha */
+  int32_t col0;    /* first time column of the chunk on the alpha's grid */
+  int32_t ncols;   /* columns in the chunk */
+  double cost;     /* modelled relative cost (tensor + epilogue work), for load balancing */
+} jtfs_unit_t;
+
+/* The KD work units of one signal, alpha-major then chunk (unit id = position).
+ * Writes min(cap, n) units; *n_units = total.  Host query.  Plans created with
+ * JTFS_LATENCY use small chunks (many units for one signal). */
+JTFS_API jtfs_status jtfs_units(jtfs_plan_t plan, jtfs_unit_t* units, int32_t cap, int32_t* n_units);
+
+/* Floats of KD partials per signal (the buffer of jtfs_forward_units). */
+JTFS_API jtfs_status jtfs_partials_size(jtfs_plan_t plan, int64_t* floats_per_signal);
+
+/* Forward restricted to KD units unit_ids[0..n_units) (host array of unit ids,
+ * any order, no duplicates).  x: device fp32 [B][N]; partials: device fp32
+ * [B][partials_size], fully overwritten (slices of other units are zeroed);
+ * out: device fp32 [B][floats_per_signal] -- receives S0 and S1 only.  ws must
+ * be kept untouched until jtfs_reduce_pack (it holds the phi_T-averaged first
+ * order Y_phi).  B must not exceed the plan's micro-batch (JTFS_ERR_INVALID_ARG
+ * otherwise; c4 uses B = 1).  Asynchronous on `stream`. */
+JTFS_API jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B,
+                                        const int32_t* unit_ids, int32_t n_units, float* partials,
+                                        float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Eq. (3)/(4) completion from summed partials (device fp32 [B][partials_size])
+ * and the Y_phi left in ws by jtfs_forward_units on the same plan: phi_F pooling,
+ * phi-only paths and packing of S2 into out (S0/S1 already there).  Asynchronous. */
+JTFS_API jtfs_status jtfs_reduce_pack(jtfs_plan_t plan, const float* partials, int64_t B, float* out,
+                                      void* ws, size_t ws_bytes, void* stream);
+
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)
@@ -188,9 +232,9 @@ JTFS_API jtfs_status jtfs_debug_filter(jtfs_plan_t plan, int32_t bank, int32_t i
  * stage's arithmetic (for KD the FFT-along-lambda form); bytes[s]: the stage's
  * unavoidable HBM traffic (input + output of the whole path are charged to
  * KA / KS / KE).  With cap >= 7, flops[6] is the tensor-core work KD actually
- * executes per signal (real-embedded 3xTF32 contraction: 3 x 2 x (2M)(2K)L
- * summed over alpha) and bytes[6] the A''/Y'' bytes KD stages into shared
- * memory per signal.  Host query. */
+ * executes per signal (fp16 two-term split contraction: 3 products x (re, im)
+ * x 2 Mpad K16 L summed over alpha) and bytes[6] the A''/Y'' bytes KD stages
+ * into shared memory per signal.  Host query. */
 JTFS_API jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap);
 
 /* Stage profiling (tracing).  When enabled, jtfs_forward records a CUDA event

@@ -120,6 +120,7 @@ struct WsPtrs {
   float2 *xhat, *tmp, *u1hat;
   float *u1, *yphi, *y2, *ys, *part;
   uint16_t* y16;
+  int32_t* sel;
   int* flag;
 };
 
@@ -136,6 +137,7 @@ WsPtrs carve(const jtfs::Plan& P, void* ws, int64_t mb) {
   w.y16 = (uint16_t*)c; c += L.y16;
   w.ys = (float*)c; c += L.ys;
   w.part = (float*)c; c += L.part;
+  w.sel = (int32_t*)c; c += L.sel;
   w.flag = (int*)c;
   return w;
 }
@@ -179,8 +181,18 @@ struct StageScope {
 };
 
 // enqueue every stage for one micro-batch of nb signals; returns "" or an error
+// Options of jtfs_forward_units / jtfs_reduce_pack: KD restricted to a unit
+// selection and writing an external partials buffer; KE skipped or run alone.
+struct RunOpts {
+  const jtfs::UnitSel* sel = nullptr;
+  float* part = nullptr;  // KD partials target (default: the workspace's)
+  bool skip_ke = false;
+};
+
+void fill_ke_params(jtfs::Plan& P, jtfs::KEParams& kp, const float* part, const float* yphi, float* out);
+
 std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, const WsPtrs& w, bool keep_u1,
-                           int upto_stage, cudaStream_t st) {
+                           int upto_stage, cudaStream_t st, const RunOpts& o = RunOpts()) {
   using namespace jtfs;
   jtfs_layout_t lay;
   layout_of(P, &lay);
@@ -198,14 +210,26 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   {
     StageScope s(P, 4, st);
     int err = 0;
-    s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, w.y16, w.ys, nb, w.part, st, &err) : launch_kd(P, w.y2, nb, w.part, st));
+    float* part = o.part ? o.part : w.part;
+    s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, w.y16, w.ys, nb, part, st, &err, o.sel)
+                          : launch_kd(P, w.y2, nb, part, st, o.sel));
     if (err) return "tcgen05 KD: cuTensorMapEncodeTiled failed for the Y2 tensor map";
     if (std::getenv("JTFS_DEBUG_SYNC")) {
       cudaError_t e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return std::string("KD: ") + cudaGetErrorString(e);
     }
   }
+  if (o.skip_ke) return "";
   KEParams kp{};
+  fill_ke_params(P, kp, w.part, w.yphi, out);
+  { StageScope s(P, 5, st); s.done(launch_ke(P, kp, nb, st)); }
+  return "";
+}
+
+void fill_ke_params(jtfs::Plan& P, jtfs::KEParams& kp, const float* part, const float* yphi, float* out) {
+  using namespace jtfs;
+  jtfs_layout_t lay;
+  layout_of(P, &lay);
   kp.paths = (const DevPath*)P.d_paths;
   kp.filters = (const DevFilter*)P.d_fr;
   kp.alphas = (const DevAlpha*)P.d_alphas;
@@ -215,8 +239,8 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   kp.hpsi = (const float2*)P.d_hphi;
   kp.hphiF = P.d_hphi + (size_t)2 * nbeta * P.N_fr;
   kp.gT = kp.hphiF + P.N_fr;
-  kp.part = w.part;
-  kp.yphi = w.yphi;
+  kp.part = part;
+  kp.yphi = yphi;
   kp.out = out;
   kp.fps = lay.floats_per_signal;
   kp.off_s2 = lay.off_s2;
@@ -229,8 +253,6 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   kp.frame0 = P.frame0;
   kp.Mpad = P.Mpad;
   kp.k_phiphi = P.prm.average_fr ? P.log2F : 0;
-  { StageScope s(P, 5, st); s.done(launch_ke(P, kp, nb, st)); }
-  return "";
 }
 
 struct DeviceGuard {
@@ -414,6 +436,118 @@ jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B, 
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  return JTFS_OK;
+}
+
+// ---- path sharding (jtfs.h: jtfs_units / jtfs_forward_units / jtfs_reduce_pack) ----
+namespace {
+// unit table of one signal: alpha-major, chunk-minor
+void unit_table(const jtfs::Plan& P, std::vector<jtfs_unit_t>& u) {
+  u.clear();
+  for (size_t a = 0; a < P.kd.size(); ++a) {
+    const auto& d = P.kd[a];
+    // modelled cost: tensor work (3 products x re/im x K16 per complex output) +
+    // epilogue (modulus + pooling per complex output), per column of Mpad rows
+    const double k16 = (double)((2 * d.K + 15) / 16 * 16);
+    const double per_col = (double)P.Mpad * (6.0 * k16 / 8.0 + 24.0);
+    for (int c = 0; c < d.nchunks; ++c) {
+      jtfs_unit_t x{};
+      x.alpha = (int32_t)a;
+      x.chunk = c;
+      x.col0 = c * d.chunk;
+      x.ncols = d.chunk;
+      x.cost = per_col * d.chunk;
+      u.push_back(x);
+    }
+  }
+}
+}  // namespace
+
+jtfs_status jtfs_units(jtfs_plan_t plan, jtfs_unit_t* units, int32_t cap, int32_t* n_units) {
+  if (!plan || !n_units || cap < 0 || (cap > 0 && !units)) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  std::vector<jtfs_unit_t> u;
+  unit_table(plan->P, u);
+  *n_units = (int32_t)u.size();
+  for (int32_t i = 0; i < std::min<int32_t>(cap, (int32_t)u.size()); ++i) units[i] = u[i];
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_partials_size(jtfs_plan_t plan, int64_t* floats_per_signal) {
+  if (!plan || !floats_per_signal) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  *floats_per_signal = plan->P.part_total;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B, const int32_t* unit_ids,
+                               int32_t n_units, float* partials, float* out, void* ws, size_t ws_bytes,
+                               void* stream) {
+  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK) return s;
+  jtfs::Plan& P = plan->P;
+  if (B > P.mb) return fail(JTFS_ERR_INVALID_ARG, "forward_units: B exceeds the plan's micro-batch");
+  if (!partials || ((uintptr_t)partials & 15)) return fail(JTFS_ERR_INVALID_ARG, "partials NULL or misaligned");
+  if (n_units < 0 || (n_units > 0 && !unit_ids)) return fail(JTFS_ERR_INVALID_ARG, "bad unit list");
+  std::vector<jtfs_unit_t> table;
+  unit_table(P, table);
+  // per-alpha chunk lists, in ascending chunk order (the order does not change results)
+  std::vector<std::vector<int32_t>> per(P.kd.size());
+  std::vector<char> seen(table.size(), 0);
+  for (int32_t i = 0; i < n_units; ++i) {
+    const int32_t id = unit_ids[i];
+    if (id < 0 || id >= (int32_t)table.size()) return fail(JTFS_ERR_INVALID_ARG, "unit id out of range");
+    if (seen[id]) return fail(JTFS_ERR_INVALID_ARG, "duplicate unit id");
+    seen[id] = 1;
+    per[table[id].alpha].push_back(table[id].chunk);
+  }
+  jtfs::UnitSel sel;
+  std::vector<int32_t> flat;
+  for (auto& v : per) {
+    std::sort(v.begin(), v.end());
+    sel.off.push_back((int)flat.size());
+    sel.cnt.push_back((int)v.size());
+    flat.insert(flat.end(), v.begin(), v.end());
+  }
+  if (B == 0) return JTFS_OK;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  WsPtrs w = carve(P, ws, B);
+  cudaError_t e = cudaMemsetAsync(partials, 0, (size_t)B * P.part_total * 4, st);
+  if (e == cudaSuccess && !flat.empty())
+    e = cudaMemcpyAsync(w.sel, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host list is a local
+  if (e != cudaSuccess) return cuda_fail(e, "forward_units setup");
+  sel.d_sel = w.sel;
+  RunOpts o;
+  o.sel = &sel;
+  o.part = partials;
+  o.skip_ke = true;
+  const std::string err = run_microbatch(P, x, (int)B, out, w, false, 99, st, o);
+  if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_reduce_pack(jtfs_plan_t plan, const float* partials, int64_t B, float* out, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (!plan) return fail(JTFS_ERR_INVALID_ARG, "plan is NULL");
+  jtfs::Plan& P = plan->P;
+  if (P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");
+  if (B < 0 || B > P.mb) return fail(JTFS_ERR_INVALID_ARG, "reduce_pack: B out of range");
+  if (!partials || !out || !ws) return fail(JTFS_ERR_INVALID_ARG, "NULL buffer");
+  if (ws_bytes < jtfs::ws_layout(P, B).total) return fail(JTFS_ERR_WORKSPACE, "workspace too small");
+  if (B == 0) return JTFS_OK;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  WsPtrs w = carve(P, ws, B);
+  jtfs::KEParams kp{};
+  fill_ke_params(P, kp, partials, w.yphi, out);
+  {
+    StageScope sc(P, 5, st);
+    sc.done(jtfs::launch_ke(P, kp, (int)B, st));
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return JTFS_OK;
 }
 

@@ -383,8 +383,8 @@ __global__ void __launch_bounds__(256) k_kd_simt(KDParams p) {
   int u = blockIdx.x;
   const int mblk = u % nmb;
   u /= nmb;
-  const int ch = u % p.nchunks;
-  const int b = u / p.nchunks;
+  const int ch = p.chunk_sel ? p.chunk_sel[u % p.nsel] : u % p.nsel;
+  const int b = u / p.nsel;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const float* Y = p.y2 + (int64_t)b * p.y2_stride + p.y2_off;  // planar rows 2l (re), 2l+1 (im)
   const float2* A = p.A + mblk * 64;
@@ -739,9 +739,14 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2,
   return n;
 }
 
-int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st) {
-  for (const auto& d : P.kd) {
+int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, const UnitSel* sel) {
+  int n = 0;
+  for (size_t i = 0; i < P.kd.size(); ++i) {
+    const auto& d = P.kd[i];
     KDParams k{};
+    k.chunk_sel = sel ? sel->d_sel + sel->off[i] : nullptr;
+    k.nsel = sel ? sel->cnt[i] : d.nchunks;
+    if (k.nsel == 0) continue;
     k.A = (const float2*)P.d_A + d.a_off;
     k.y2 = y2;
     k.g = P.d_g + d.g_off;
@@ -759,12 +764,13 @@ int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_
     k.part_off = d.part_off;
     k.y2_stride = 2 * P.y2_total;
     k.part_stride = P.part_total;
-    const int grid = nsig * d.nchunks * (P.Mpad / 64);
+    const int grid = nsig * k.nsel * (P.Mpad / 64);
     if (P.n_frames <= 8) k_kd_simt<8><<<grid, 256, 0, st>>>(k);
     else if (P.n_frames <= 16) k_kd_simt<16><<<grid, 256, 0, st>>>(k);
     else k_kd_simt<32><<<grid, 256, 0, st>>>(k);
+    ++n;
   }
-  return (int)P.kd.size();
+  return n;
 }
 
 size_t ke_smem_bytes(const Plan& P) {

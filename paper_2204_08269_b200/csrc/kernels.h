@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "jtfs_internal.h"
 
@@ -15,6 +16,15 @@ struct KDParams {
   float* part;       // micro-batch partials base
   int K, Kpad, Mpad, L, D, frame0, nframes, chunk, nchunks;
   int64_t y2_off, part_off, y2_stride, part_stride;
+  const int32_t* chunk_sel;  // selected time chunks (path sharding) or nullptr = all
+  int nsel;                  // number of selected chunks (= nchunks when chunk_sel is null)
+};
+
+// KD work-unit selection of jtfs_forward_units: per alpha, cnt[a] chunk ids at
+// d_sel + off[a] (device); cnt[a] == 0 skips the alpha.
+struct UnitSel {
+  const int32_t* d_sel = nullptr;
+  std::vector<int> off, cnt;
 };
 
 struct DevPath {
@@ -52,11 +62,12 @@ int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int
                       int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
                       const Band* d_band_L1, cudaStream_t st);
 int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st);
-int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st);
+int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, const UnitSel* sel = nullptr);
 size_t ke_smem_bytes(const Plan& P);
 int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
 cudaError_t ke_set_smem(const Plan& P);
-int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st, int* err);
+int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st, int* err,
+                 const UnitSel* sel = nullptr);
 cudaError_t tc_setup_device(Plan& P);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 

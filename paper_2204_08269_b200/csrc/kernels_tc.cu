@@ -322,6 +322,8 @@ struct TcParams {
   int S;           // A ring stages
   int tpu;         // tiles per work unit
   int nchunks;     // time chunks per signal (L / (Nt * tpu))
+  const int32_t* chunk_sel;  // selected chunks (path sharding) or nullptr = all
+  int nsel;        // number of selected chunks
   int n_mpart, n_mblk;  // M-parts and 128-row M-blocks per part
   int L, nframes, Mpad;
   int nsig;
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int units = p.nsig * p.nchunks * p.n_mpart;
+  const int units = p.nsig * p.nsel * p.n_mpart;
   const int nst = (p.nkc + 1) / 2;  // A'' stages (<= 2 records of 16 K-columns) per M-block
   // the CTA's tile sequence: unit u = blockIdx.x + i * gridDim.x, tile 0..tpu-1
   const int my_units = (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
@@ -431,7 +433,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t wbytes = (uint32_t)(p.Nt * NF * 4);
       for (int gt = 0; gt < my_tiles; ++gt) {
         const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
-        const int chunk = (u / p.n_mpart) % p.nchunks, b = u / (p.n_mpart * p.nchunks);
+        int chunk = (u / p.n_mpart) % p.nsel;
+        if (p.chunk_sel) chunk = p.chunk_sel[chunk];
+        const int b = u / (p.n_mpart * p.nsel);
         const int t0 = (chunk * p.tpu + gt % p.tpu) * p.Nt;
         const int wi = gt & 1, bi = gt % p.NBB;
         mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
@@ -549,7 +553,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int gt = 0; gt < my_tiles; ++gt) {
       const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
       const int mpart = u % p.n_mpart;
-      const int chunk = (u / p.n_mpart) % p.nchunks, b = u / (p.n_mpart * p.nchunks);
+      int chunk = (u / p.n_mpart) % p.nsel;
+      if (p.chunk_sel) chunk = p.chunk_sel[chunk];
+      const int b = u / (p.n_mpart * p.nsel);
       const int tile = gt % p.tpu;
       if (tile == 0) {
 #pragma unroll
@@ -702,9 +708,10 @@ void plan_tc(Plan& P) {
     // time chunk per work unit: the largest power of two <= 4096 that still gives
     // about 4 units per SM for a full micro-batch (partials are per chunk)
     if (ok) {
-      int64_t target = (int64_t)P.mb * P.tc_n_mpart * d.L / (4 * 148);
+      const int64_t sig = (P.prm.flags & JTFS_LATENCY) ? 1 : P.mb;  // signals per KD launch
+      int64_t target = sig * P.tc_n_mpart * d.L / (4 * 148);
       int ch = 4096;
-      while (ch > d.tc_Nt && ch > target) ch /= 2;
+      while (ch > d.tc_Nt && ch > target) ch /= 2;  // (JTFS_LATENCY: one signal per launch)
       d.chunk = std::min(ch, d.L);
       if (d.chunk < d.tc_Nt) d.chunk = d.tc_Nt;
       d.nchunks = d.L / d.chunk;
@@ -727,7 +734,7 @@ cudaError_t tc_setup_device(Plan& P) {
 }
 
 int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st,
-                 int* err) {
+                 int* err, const UnitSel* sel) {
   const int NF = nf_of(P.n_frames);
   int sms = 148;
   {
@@ -738,6 +745,8 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
   int launches = 0;
   for (size_t i = 0; i < P.kd.size(); ++i) {
     const auto& d = P.kd[i];
+    const int nsel = sel ? sel->cnt[i] : d.nchunks;
+    if (nsel == 0) continue;
     // ---- KY: fp16 split of the Y'' tiles ----
     {
       tc::KYParams q{};
@@ -775,6 +784,8 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.S = d.tc_S;
     p.tpu = d.tc_tpu;
     p.nchunks = d.nchunks;
+    p.chunk_sel = sel ? sel->d_sel + sel->off[i] : nullptr;
+    p.nsel = nsel;
     p.n_mpart = P.tc_n_mpart;
     p.n_mblk = P.tc_n_mblk;
     p.L = d.L;
@@ -794,7 +805,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.part = part;
     p.part_off = d.part_off;
     p.part_stride = P.part_total;
-    const int units = nsig * d.nchunks * P.tc_n_mpart;
+    const int units = nsig * nsel * P.tc_n_mpart;
     const int grid = std::min(units, sms);
     const size_t sm = tc_smem(d, NF);
     cudaEvent_t e0 = nullptr, e1 = nullptr;

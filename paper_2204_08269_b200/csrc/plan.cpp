@@ -618,8 +618,13 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   w.y16 = al((size_t)mb * p.y16_total * 2);
   w.ys = al((size_t)mb * p.ys_total * 4);
   w.part = al((size_t)mb * p.part_total * 4);
+  {
+    size_t nsel = 0;  // jtfs_forward_units' chunk lists (at most one id per 64-column chunk)
+    for (const auto& d : p.kd) nsel += (size_t)std::max(1, d.L / 64);
+    w.sel = al(nsel * 4);
+  }
   w.flag = 256;
-  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.flag;
+  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.sel + w.flag;
   return w;
 }
 

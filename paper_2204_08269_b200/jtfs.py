@@ -24,6 +24,7 @@ _lib = C.CDLL(LIB_PATH)
 JTFS_OK, JTFS_ERR_INVALID_ARG, JTFS_ERR_UNSUPPORTED, JTFS_ERR_OOM = 0, 1, 2, 3
 JTFS_ERR_CUDA, JTFS_ERR_WORKSPACE, JTFS_ERR_NONFINITE = 4, 5, 6
 JTFS_CHECK_FINITE = 1
+JTFS_LATENCY = 2
 JTFS_PAD_REFLECT, JTFS_PAD_PERIODIC = 0, 1
 PATH_SPIN, PATH_PSI_T_PHI_F, PATH_PHI_T_PSI_F, PATH_PHI_T_PHI_F = 0, 1, 2, 3
 
@@ -32,6 +33,7 @@ EXPORTS = [
     "jtfs_lambda_xi", "jtfs_workspace_size", "jtfs_forward", "jtfs_forward_host",
     "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_cost", "jtfs_profile_enable",
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
+    "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -54,6 +56,11 @@ class jtfs_path_t(C.Structure):
                 ("xi_alpha", C.c_double), ("xi_beta", C.c_double)]
 
 
+class jtfs_unit_t(C.Structure):
+    _fields_ = [("alpha", C.c_int32), ("chunk", C.c_int32), ("col0", C.c_int32), ("ncols", C.c_int32),
+                ("cost", C.c_double)]
+
+
 _P = C.c_void_p
 _lib.jtfs_plan.argtypes = [C.c_int] * 8 + [C.POINTER(_P)]
 _lib.jtfs_plan_create.argtypes = [C.POINTER(jtfs_params), C.POINTER(_P)]
@@ -71,6 +78,10 @@ _lib.jtfs_cost.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c
 _lib.jtfs_profile_enable.argtypes = [_P, C.c_int32]
 _lib.jtfs_profile_read.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32, C.c_int32]
 _lib.jtfs_profile_read_kd.argtypes = [_P, C.POINTER(C.c_double), C.c_int32, C.c_int32]
+_lib.jtfs_units.argtypes = [_P, C.POINTER(jtfs_unit_t), C.c_int32, C.POINTER(C.c_int32)]
+_lib.jtfs_partials_size.argtypes = [_P, C.POINTER(C.c_int64)]
+_lib.jtfs_forward_units.argtypes = [_P, _P, C.c_int64, C.POINTER(C.c_int32), C.c_int32, _P, _P, _P, C.c_size_t, _P]
+_lib.jtfs_reduce_pack.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -224,6 +235,39 @@ class Plan:
         _check(_lib.jtfs_forward_host(self._h, _ptr(x_host), B, _ptr(out_host), _ptr(x_dev), _ptr(out_dev),
                                       _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_forward_host")
         return out_host
+
+    # ---- path sharding (jtfs_units / jtfs_forward_units / jtfs_reduce_pack) ----
+    def units(self):
+        """KD work units of one signal: list of dicts (alpha, chunk, col0, ncols, cost); id = index."""
+        n = C.c_int32()
+        _check(_lib.jtfs_units(self._h, None, 0, C.byref(n)), "jtfs_units")
+        arr = (jtfs_unit_t * max(n.value, 1))()
+        _check(_lib.jtfs_units(self._h, arr, n.value, C.byref(n)), "jtfs_units")
+        return [dict(alpha=u.alpha, chunk=u.chunk, col0=u.col0, ncols=u.ncols, cost=u.cost)
+                for u in arr[:n.value]]
+
+    @property
+    def partials_size(self) -> int:
+        v = C.c_int64()
+        _check(_lib.jtfs_partials_size(self._h, C.byref(v)), "jtfs_partials_size")
+        return int(v.value)
+
+    def forward_units(self, x, unit_ids, partials, out, stream=None):
+        """KA..KC + S0/S1 into out + KD partials of the listed units (others zeroed)."""
+        B = x.shape[0]
+        ids = (C.c_int32 * max(len(unit_ids), 1))(*[int(i) for i in unit_ids])
+        ws = self.workspace(B)
+        _check(_lib.jtfs_forward_units(self._h, _ptr(x), B, ids, len(unit_ids), _ptr(partials), _ptr(out),
+                                       _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_forward_units")
+        return partials, out
+
+    def reduce_pack(self, partials, out, stream=None):
+        """phi_F pooling + phi paths + packing of S2 from summed partials (same workspace)."""
+        B = partials.shape[0]
+        ws = self.workspace(B)
+        _check(_lib.jtfs_reduce_pack(self._h, _ptr(partials), B, _ptr(out), _ptr(ws), ws.numel(),
+                                     _stream_handle(stream)), "jtfs_reduce_pack")
+        return out
 
     def debug_tap(self, tap: int, x):
         import torch

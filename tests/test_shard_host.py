@@ -1,0 +1,106 @@
+"""Host logic of the path-sharded forward (paper_2204_08269_b200/shard.py), on CPU.
+
+The CUDA work of `forward_units` / `reduce_pack` is covered by
+tests/test_gpu_shard.py; here: the unit table of a host-only plan (c4 config),
+the deterministic LPT assignment, and the exchange of disjoint partial slices
+over a world_size-2 gloo group (exact: every slice is nonzero on one rank only).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2204_08269_b200 import shard
+
+C4 = dict(N=2 ** 17, J=13, Q=16, J_fr=5, T=2 ** 13, F=4)
+
+
+@pytest.fixture(scope="module")
+def jt():
+    from paper_2204_08269_b200 import build
+    build.build()
+    from paper_2204_08269_b200 import jtfs
+    return jtfs
+
+
+def test_unit_table_tiles_every_alpha(jt):
+    plan = jt.Plan(**C4, device=-1, flags=jt.JTFS_LATENCY)
+    units = plan.units()
+    assert len(units) > 148                      # enough units for one signal to fill the GPU
+    by_alpha = {}
+    for u in units:
+        by_alpha.setdefault(u["alpha"], []).append(u)
+        assert u["cost"] > 0 and u["ncols"] > 0
+    assert sorted(by_alpha) == list(range(plan.layout.n_alpha))
+    for a, us in by_alpha.items():
+        cols = sorted((u["col0"], u["ncols"]) for u in us)
+        assert cols[0][0] == 0
+        for (c0, n0), (c1, _) in zip(cols, cols[1:]):
+            assert c1 == c0 + n0                 # contiguous, non-overlapping chunks
+    # the batch plan of the same config uses coarser chunks
+    assert len(jt.Plan(**C4, device=-1).units()) <= len(units)
+    # a host-only plan refuses to compute (no CPU fallback)
+    import ctypes as C
+    ids = (C.c_int32 * 1)(0)
+    st = jt.library().jtfs_forward_units(plan.handle, None, 1, ids, 1, None, None, None, 0, None)
+    assert st == jt.JTFS_ERR_UNSUPPORTED
+
+
+def test_lpt_assignment():
+    rng = np.random.default_rng(3)
+    costs = rng.uniform(1, 100, 257).tolist()
+    for world in (1, 2, 3, 8):
+        parts = shard.lpt_assign(costs, world)
+        assert parts == shard.lpt_assign(costs, world)           # deterministic
+        flat = sorted(i for p in parts for i in p)
+        assert flat == list(range(len(costs)))                   # a partition
+        loads = [sum(costs[i] for i in p) for p in parts]
+        assert max(loads) - min(loads) <= max(costs)             # LPT bound
+    with pytest.raises(ValueError):
+        shard.lpt_assign(costs, 0)
+
+
+def _fill(n_units, seg, ids):
+    buf = np.zeros(n_units * seg, dtype=np.float32)
+    for u in ids:
+        k = np.arange(seg)
+        buf[u * seg:(u + 1) * seg] = (np.sin(u * 7.0 + k) * 10 ** ((u % 7) - 3)).astype(np.float32)
+    return buf
+
+
+def _worker(rank, world, port, n_units, seg, costs, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = shard.lpt_assign(costs, world)[rank]
+        t = torch.from_numpy(_fill(n_units, seg, mine))
+        shard.exchange_partials(t, dst=0)
+        if rank == 0:
+            q.put(t.numpy().tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_exchange_partials_gloo_world2(jt):
+    import torch.multiprocessing as mp
+    plan = jt.Plan(**C4, device=-1, flags=jt.JTFS_LATENCY)
+    costs = [u["cost"] for u in plan.units()]
+    n_units, seg = len(costs), 8
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_units, seg, costs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = _fill(n_units, seg, range(n_units)).tobytes()
+    assert got == want                                          # byte-identical to one rank
