@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Throughput benchmark of the B200 forward JTFS (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c4]
 
 Workload (BASELINE configs[2], "instrument-note batch"): N = 2^16, J = 12, Q = 16,
 J_fr = 5, Q_fr = 1, T = 2^13, F = 4, 256 synthetic notes per GPU.
@@ -11,6 +11,11 @@ no data-path collective); timing = max over ranks of the summed per-step CUDA
 event times; the L2 is flushed (256 MiB write) before every timed step.
 Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle
 (the reference arm of this tier) on the same workload, one signal per step.
+
+`--workload c4` (not the headline metric): latency of ONE long
+signal (bird texture, N = 2^17, J = 13) path-sharded over the ranks
+(paper_2204_08269_b200/shard.py: KD units split by LPT, partials summed onto
+rank 0, KE there); strong scaling, ms per forward, max over ranks.
 """
 from __future__ import annotations
 
@@ -27,6 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = dict(N=2 ** 16, J=12, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
+CFG4 = dict(N=2 ** 17, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
 METRIC = "JTFS signals/s (N=2^16,J=12,Q=16) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "signals/s"
 WORKLOAD = "instrument-note batch (BASELINE configs[2]): N=2^16, J=12, Q=16, J_fr=5, Q_fr=1, T=2^13, F=4"
@@ -135,6 +141,48 @@ def run_reference(args, rank, world):
     return 0
 
 
+def run_c4(args, rank, world, local, dev):
+    """Path-sharded single-signal latency (config c4)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2204_08269_b200 import jtfs, shard, signals
+    plan = jtfs.Plan(N=CFG4["N"], J=CFG4["J"], Q=CFG4["Q"], J_fr=CFG4["J_fr"], Q_fr=CFG4["Q_fr"], T=CFG4["T"],
+                     F=CFG4["F"], device=local, flags=jtfs.JTFS_LATENCY)
+    x = torch.from_numpy(signals.bird_texture(seed=7)[None, :].copy()).to(dev)
+    for _ in range(args.warmup):
+        shard.forward_sharded(plan, x)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    times = []
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        shard.forward_sharded(plan, x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": "JTFS c4 path-sharded forward latency (N=2^17, J=13, Q=16, one signal)", "value": ms,
+            "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "c4 bird texture (seed 7), one signal, KD units split by LPT over ranks",
+                       "units": len(plan.units()), **CFG4}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -143,6 +191,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="signals per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4"])
     args = ap.parse_args()
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -161,6 +210,8 @@ def main():
         _build.build()
     if world > 1:
         dist.barrier()
+    if args.workload == "c4":
+        return run_c4(args, rank, world, local, dev)
     from paper_2204_08269_b200 import jtfs, signals
 
     B = args.batch
