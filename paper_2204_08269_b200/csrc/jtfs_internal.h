@@ -71,7 +71,8 @@ struct AlphaKD {
   int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
   int64_t y16_off = 0;  // fp16 offset of Y16_alpha [hi|lo][K16][L] in one signal's Y16 buffer (KY output)
   int64_t ys_off = 0;   // float offset of the per-tile inverse Y scales (L / 64 slots) in one signal's ys
-  int64_t wtab_off = 0; // float offset of the phi_T taps table [L][NF] in wtab
+  int64_t wtab_off = 0; // float offset of the phi_T pooling table in wtab
+  int pool_mode = 0;    // 0: taps [L][NF]; 1: cubic-moment coefficients [L/32][4][NF] (kernels_tc.cu)
   int nslices = 0;      // KD partial slices per signal and alpha (time chunks x epilogue sets)
 };
 
@@ -120,7 +121,7 @@ struct Plan {
   std::vector<float> A;                  // complex interleaved A_alpha^T tables (SIMT KD)
   std::vector<uint16_t> A16;             // A''_alpha re/im, row-scaled fp16 hi/lo, pre-tiled/swizzled (tcgen05 KD)
   std::vector<float> Ainv;               // per alpha and row: 1 / (power-of-two row scale of A16)
-  std::vector<float> wtab;               // per alpha: phi_T taps per time column and frame [L][NF]
+  std::vector<float> wtab;               // per alpha: phi_T pooling table (taps or moment coefficients)
   int64_t y16_total = 0, ys_total = 0;   // per signal: fp16 elements of Y16, per-tile scale slots
   std::vector<float> g;                  // time pooling taps per alpha
   std::vector<float> W;                  // lambda pooling matrices per filter

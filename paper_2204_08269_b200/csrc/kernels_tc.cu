@@ -259,6 +259,27 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&vr)[16], const uint32
   }
 }
 
+// moment form of the phi_T pooling over 16 columns J0..J0+15 of a 32-column
+// block: S_k += |Z_j| u_j^k, u_j = (j - 15.5) / 16 (exact in fp32), k = 0..3
+template <int J0>
+__device__ __forceinline__ void mom_chunk(const uint32_t (&vr)[16], const uint32_t (&vi)[16], float (&S)[4]) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 re = make_float2(__uint_as_float(vr[j]), __uint_as_float(vr[j + 1]));
+    const float2 im = make_float2(__uint_as_float(vi[j]), __uint_as_float(vi[j + 1]));
+    const float2 sq = ffma2v(im, im, fmul2(re, re));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float mag = sqrt_fast(h ? sq.y : sq.x);
+      const float u = ((float)(J0 + j + h) - 15.5f) * 0.0625f;
+      S[0] += mag;
+      S[1] = fmaf(mag, u, S[1]);
+      S[2] = fmaf(mag, u * u, S[2]);
+      S[3] = fmaf(mag, u * u * u, S[3]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // KY: one CTA per (signal, tile): max |Y''| over the K' x Nt tile -> s_Y (power of
 // two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y - hi) into the
@@ -330,7 +351,8 @@ struct TcParams {
   unsigned long long* prof;  // measurement only (JTFS_TC_PROF): per-role wait-cycle counters or nullptr
   const uint16_t* A;   // A''_alpha records [Mpad / 128][nkc] x 16 KiB
   const float* ainv;   // 1 / s_m per row [Mpad]
-  const float* wtab;   // phi_T taps [L][NF]
+  const float* wtab;   // phi_T pooling table: taps [L][NF] (pool_mode 0) or cubic moments [L/32][4][NF] (1)
+  int pool_mode;
   const float* ys;     // 1 / s_Y per (signal, tile): ys[b * ys_stride + tile]
   int64_t ys_stride;
   float* part;
@@ -430,7 +452,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== B producer: fp16 hi / lo tile + taps =====================
     if (lane == 0) {
       const uint32_t btx = (uint32_t)(2 * p.K16 * p.Nt * 2);
-      const uint32_t wbytes = (uint32_t)(p.Nt * NF * 4);
+      const int wcol = p.pool_mode ? NF / 8 : NF;  // table floats per time column
+      const uint32_t wbytes = (uint32_t)(p.Nt * wcol * 4);
       for (int gt = 0; gt < my_tiles; ++gt) {
         const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
         int chunk = (u / p.n_mpart) % p.nsel;
@@ -440,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int wi = gt & 1, bi = gt % p.NBB;
         mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
         mbar_expect_tx(w_full + wi, wbytes);
-        bulk_load(Wt + wi * p.Nt * NF, p.wtab + (size_t)t0 * NF, wbytes, w_full + wi);
+        bulk_load(Wt + wi * p.Nt * NF, p.wtab + (size_t)t0 * wcol, wbytes, w_full + wi);
         mbar_wait(b_empty + bi, (uint32_t)((gt / p.NBB) + 1) & 1u);
         mbar_expect_tx(b_full + bi, btx);
         for (int h = 0; h < 2; ++h) {
@@ -578,19 +601,60 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
         const int half = p.Nt / 2;
-        for (int c0 = 0; c0 < half; c0 += 16) {
-          uint32_t vr[16], vi[16];
-          tmem_ld16(tb + c0, vr);
-          tmem_ld16(tb + p.Nt + c0, vi);
-          tmem_wait_ld();
-          reg_fence16(vr);
-          reg_fence16(vi);
-          if (c0 + 16 >= half) {  // last read of this buffer: hand it back to the MMA
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty + ab);
+        if (p.pool_mode == 1) {
+          // moment form: per 32-column block S_k = sum_j |Z_j| u_j^k (k <= 3, u_j
+          // compile-time), then part += G_k S_k with the block's 4 x NF coefficients
+          const float* gco = Wt + wi * p.Nt * NF + (cbeg / 32) * 4 * NF;
+          for (int c0 = 0; c0 < half; c0 += 32) {
+            float S[4] = {0.f, 0.f, 0.f, 0.f};
+            {
+              uint32_t vr[16], vi[16];
+              tmem_ld16(tb + c0, vr);
+              tmem_ld16(tb + p.Nt + c0, vi);
+              tmem_wait_ld();
+              reg_fence16(vr);
+              reg_fence16(vi);
+              mom_chunk<0>(vr, vi, S);
+            }
+            {
+              uint32_t vr[16], vi[16];
+              tmem_ld16(tb + c0 + 16, vr);
+              tmem_ld16(tb + p.Nt + c0 + 16, vi);
+              tmem_wait_ld();
+              reg_fence16(vr);
+              reg_fence16(vi);
+              if (c0 + 32 >= half) {  // last read of this buffer: hand it back to the MMA
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty + ab);
+              }
+              mom_chunk<16>(vr, vi, S);
+            }
+            const float4* g4 = reinterpret_cast<const float4*>(gco + (c0 / 32) * 4 * NF);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int m4 = 0; m4 < NF / 4; ++m4) {
+                const float4 w = g4[k * (NF / 4) + m4];
+                part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), S[k], part[2 * m4 + 0]);
+                part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), S[k], part[2 * m4 + 1]);
+              }
           }
-          epi_chunk<NF>(vr, vi, wt + c0 * NF, part);
+        } else {
+          for (int c0 = 0; c0 < half; c0 += 16) {
+            uint32_t vr[16], vi[16];
+            tmem_ld16(tb + c0, vr);
+            tmem_ld16(tb + p.Nt + c0, vi);
+            tmem_wait_ld();
+            reg_fence16(vr);
+            reg_fence16(vi);
+            if (c0 + 16 >= half) {  // last read of this buffer: hand it back to the MMA
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acc_empty + ab);
+            }
+            epi_chunk<NF>(vr, vi, wt + c0 * NF, part);
+          }
         }
         e_math += clock64() - tm0;
 #pragma unroll
@@ -795,6 +859,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.A = P.d_A16 + d.tc_a16_off;
     p.ainv = P.d_Ainv + d.tc_ainv_off;
     p.wtab = P.d_wtab + d.wtab_off;
+    p.pool_mode = d.pool_mode;
     p.ys = ys + d.ys_off;
     p.ys_stride = P.ys_total;
     static unsigned long long* prof = nullptr;

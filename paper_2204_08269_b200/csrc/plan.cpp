@@ -509,16 +509,87 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       P.ys_total += std::max(1, d.L / 64);
       d.wtab_off = (int64_t)P.wtab.size();
       const float* g = P.g.data() + d.g_off;
-      for (int t = 0; t < d.L; ++t)
-        for (int m = 0; m < NF; ++m) {
-          float w = 0.f;
-          if (m < P.n_frames) {
-            int64_t i = ((int64_t)(P.frame0 + m) * d.D - t) % d.L;
-            if (i < 0) i += d.L;
-            w = g[i];
-          }
-          P.wtab.push_back(w);
+      auto tap = [&](int m, int64_t t) -> double {
+        if (m >= P.n_frames) return 0.0;
+        int64_t i = ((int64_t)(P.frame0 + m) * d.D - t) % d.L;
+        if (i < 0) i += d.L;
+        return (double)g[i];
+      };
+      // phi_T pooling in moment form where it is exact to fp32 (kernels_tc.cu,
+      // DESIGN.md §6): over each 32-column block, every frame's tap sequence is
+      // replaced by its least-squares cubic in u_j = (j - 15.5) / 16 (coefficients
+      // rounded to fp32).  The mode is used only if, on every block and frame,
+      // the evaluated cubic deviates from the fp32 taps by <= 2^-22 of that block's
+      // largest tap (the taps' own fp32 rounding is 2^-24), plus 2^-40 max |g|.
+      d.pool_mode = 0;
+      if (d.L % 32 == 0 && !std::getenv("JTFS_POOL_EXACT")) {  // env: measurement / validation only
+        double gmax = 0;
+        for (int t = 0; t < d.L; ++t) gmax = std::max(gmax, std::abs((double)g[t]));
+        // normal equations of the cubic fit (same for every block)
+        double Mn[4][4] = {}, U[32][4];
+        for (int j = 0; j < 32; ++j) {
+          const double u = (j - 15.5) / 16.0;
+          U[j][0] = 1;
+          U[j][1] = u;
+          U[j][2] = u * u;
+          U[j][3] = u * u * u;
+          for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) Mn[r][c] += U[j][r] * U[j][c];
         }
+        // invert the 4x4 (Gauss-Jordan, fp64)
+        double Inv[4][8];
+        for (int r = 0; r < 4; ++r)
+          for (int c = 0; c < 8; ++c) Inv[r][c] = c < 4 ? Mn[r][c] : (c - 4 == r ? 1.0 : 0.0);
+        for (int c = 0; c < 4; ++c) {
+          int piv = c;
+          for (int r = c + 1; r < 4; ++r)
+            if (std::abs(Inv[r][c]) > std::abs(Inv[piv][c])) piv = r;
+          for (int k = 0; k < 8; ++k) std::swap(Inv[c][k], Inv[piv][k]);
+          const double dv = Inv[c][c];
+          for (int k = 0; k < 8; ++k) Inv[c][k] /= dv;
+          for (int r = 0; r < 4; ++r)
+            if (r != c) {
+              const double f = Inv[r][c];
+              for (int k = 0; k < 8; ++k) Inv[r][k] -= f * Inv[c][k];
+            }
+        }
+        std::vector<float> tab;
+        tab.reserve((size_t)d.L / 32 * 4 * NF);
+        bool ok = true;
+        for (int blk = 0; blk < d.L / 32 && ok; ++blk) {
+          double G[4][32] = {};  // [k][m]
+          for (int m = 0; m < NF; ++m) {
+            double rhs[4] = {0, 0, 0, 0}, w[32], wmax = 0;
+            for (int j = 0; j < 32; ++j) {
+              w[j] = tap(m, (int64_t)blk * 32 + j);
+              wmax = std::max(wmax, std::abs(w[j]));
+              for (int r = 0; r < 4; ++r) rhs[r] += U[j][r] * w[j];
+            }
+            double c[4];
+            for (int r = 0; r < 4; ++r) {
+              c[r] = 0;
+              for (int k = 0; k < 4; ++k) c[r] += Inv[r][4 + k] * rhs[k];
+            }
+            double worst = 0;
+            for (int j = 0; j < 32; ++j) {
+              double f = 0;
+              for (int k = 0; k < 4; ++k) f += (double)(float)c[k] * U[j][k];
+              worst = std::max(worst, std::abs(f - w[j]));
+            }
+            if (worst > std::ldexp(wmax, -22) + std::ldexp(gmax, -40)) ok = false;
+            for (int k = 0; k < 4; ++k) G[k][m] = c[k];
+          }
+          for (int k = 0; k < 4; ++k)
+            for (int m = 0; m < NF; ++m) tab.push_back((float)G[k][m]);
+        }
+        if (ok) {
+          d.pool_mode = 1;
+          P.wtab.insert(P.wtab.end(), tab.begin(), tab.end());
+        }
+      }
+      if (d.pool_mode == 0)
+        for (int t = 0; t < d.L; ++t)
+          for (int m = 0; m < NF; ++m) P.wtab.push_back((float)tap(m, t));
     }
   }
   // micro-batch: one micro-batch's workspace <= 16 GiB (HBM is 180 GB; larger
