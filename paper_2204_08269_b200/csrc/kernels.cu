@@ -217,7 +217,16 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
   CT* smem = reinterpret_cast<CT*>(smem_raw);
   CT* Ws = smem + G * LS;
   stage_twiddles<LOG2A, NT>(Ws, Wtab + tw_offset(LOG2A));
-  const CT* WL = Wtab + tw_offset(LOG2A + LOG2B);  // exp(-2 pi i t / L) for the inter-pass twiddle
+  // inter-pass twiddle W_L^x, x = ka * nb < L, as W_L^{x_lo} * W_L^{x_hi 2^LOG2A}
+  // (x_lo < La: the first La entries of the length-L table; x_hi < Lb: the
+  // length-Lb table), both staged in shared memory
+  CT* Wlo = Ws + La;
+  CT* Whi = Wlo + La;
+  {
+    const CT* WL = Wtab + tw_offset(LOG2A + LOG2B);
+    for (int t = threadIdx.x; t < La; t += NT) Wlo[t] = __ldg(WL + t);
+    for (int t = threadIdx.x; t < Lb; t += NT) Whi[t] = __ldg(Wtab + tw_offset(LOG2B) + t);
+  }
   constexpr int CPB = Lb / G;  // column groups per big row
   const int rho = blockIdx.x / CPB;
   const int nb0 = (blockIdx.x % CPB) * G;
@@ -242,7 +251,9 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int idx = threadIdx.x + i * NT, g = idx % G, ka = idx / G;
-      w[i] = twiddle<DIR>(WL, ka * (nb0 + g));
+      const int x = ka * (nb0 + g);
+      const CT t = cmul(Wlo[x & (La - 1)], Whi[x >> LOG2A]);
+      w[i] = DIR < 0 ? t : CxT<CT>::make(t.x, -t.y);
     }
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -625,13 +636,25 @@ void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, con
   constexpr int ELEMS = sizeof(CT) == 8 ? 4096 : 2048;  // 32 KiB of smem per CTA
   constexpr int LOG2A = (LOG2L + 1) / 2, LOG2B = LOG2L / 2;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B;
-  constexpr int GA = ELEMS / La, GB = ELEMS / Lb;
+  // pass A gathers columns (stride Lb): 16 columns per CTA when the column is
+  // long enough (128 B contiguous per row of the gather), else ELEMS / La
+  constexpr int GA0 = ELEMS / La;
+  constexpr int GA = (GA0 < 16 && 16 <= Lb && sizeof(CT) == 8 && La >= 256) ? 16 : GA0;
+  constexpr int GB = ELEMS / Lb;
   constexpr int NT = ELEMS / 8;
   static_assert(GA >= 1 && GB >= 1 && GA <= Lb && GB <= La, "four-step tile");
-  k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA>
-      <<<nbig * (Lb / GA), NT, ((size_t)GA * pad_row(La) + La) * sizeof(CT), st>>>(pa, tmp, W);
-  k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB>
-      <<<nbig * (La / GB), NT, ((size_t)GB * pad_row(Lb) + Lb) * sizeof(CT), st>>>(pb, tmp, W);
+  const size_t sma = ((size_t)GA * pad_row(La) + 2 * La + Lb) * sizeof(CT);
+  const size_t smb = ((size_t)GB * pad_row(Lb) + Lb) * sizeof(CT);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr = true;
+  }
+  k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA><<<nbig * (Lb / GA), NT, sma, st>>>(pa, tmp, W);
+  k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB><<<nbig * (La / GB), NT, smb, st>>>(pb, tmp, W);
 }
 
 template <class F>
