@@ -12,7 +12,8 @@ What it computes (PAPER.md = "P:<line>"):
   * Eq. (3) (P:88-92): S2 = | X *_{t,lambda} Psi | *_{t,lambda} Phi_{T,F};
   * Eq. (4) (P:96-100): the same without frequential averaging;
   * first-order S1 = U1 * phi_T, no Phi_F (P:251-252), out_3D layout (P:251-255);
-  * the phi-only lowpass paths (north_star; readings R11 of DESIGN.md).
+  * the phi-only lowpass paths (north_star; readings R11 of DESIGN.md);
+  * second-order time scattering (Scattering1D; `time_scattering`).
 Everything the paper leaves unstated (filter constants, ladder, subsampling
 rule, padding, admissibility, lambda-axis boundary, spin orientation, path
 order) follows the readings R1-R20 of DESIGN.md §3 (= SURVEY.md §8(c)).
@@ -398,6 +399,29 @@ def jtfs_forward(x: np.ndarray, p: Params, paths=None, s: Schedule | None = None
     S2 = np.full((len(s.paths), s.lam_out, s.n_frames), np.nan)
     for pi, m in maps.items():
         S2[pi] = m
+    return dict(S0=S0, S1=S1, S2=S2)
+
+
+def time_scattering(x: np.ndarray, p: Params, s: Schedule | None = None):
+    """Second-order time scattering (Scattering1D): "applying only a
+    1-D temporal wavelet filterbank to the first-order scalogram",
+    i.e. S2_t[lambda, alpha] = (|U1_lambda * psi_alpha| * phi_T) at the retained
+    frames, without any convolution along lambda (compare Eq. (3)).
+
+    Readings: the same banks, critical subsampling (R5), padding
+    (R6) and admissible pairs j1(lambda) < j2(alpha) (R7) as the JTFS of Eq. (3),
+    so |U1 * psi_alpha| is |Y2_alpha| of first_order(); rows ordered alpha-major
+    then lambda (schedule order).  Returns dict(S0=(frames,), S1=(n1, frames),
+    S2=(n2, frames)) with n2 = sum_alpha |adm(alpha)|."""
+    s = s or schedule(p)
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (p.N,):
+        raise ValueError(f"x must have shape ({p.N},)")
+    if not np.all(np.isfinite(x)):
+        raise ValueError("non-finite input")
+    S0, S1, _, _, Y2 = first_order(x, s)
+    rows = [phi_T_pool(np.abs(Y2[a]), s.k_alpha[a], s) for a in s.alphas]
+    S2 = np.concatenate(rows, axis=0) if rows else np.zeros((0, s.n_frames))
     return dict(S0=S0, S1=S1, S2=S2)
 
 

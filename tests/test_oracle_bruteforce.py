@@ -144,7 +144,8 @@ def brute_jtfs(x, prm):
                 V = (circ_matrix(fr_taps("phi", 0, 0)) @ G).real
                 V = V[[r * 2 ** k for r in range(s.lam_out)]]
                 S2.append(V[:, frames])
-    return dict(S0=S0, S1=S1, S2=np.array(S2))
+    S2t = [time_pool(np.abs(Y2[a]), s.k_alpha[a]) for a in s.alphas]
+    return dict(S0=S0, S1=S1, S2=np.array(S2), S2t=np.concatenate(S2t, axis=0))
 
 
 CASES = [
@@ -165,6 +166,20 @@ def test_oracle_equals_bruteforce(prm):
     b = brute_jtfs(x, prm)
     for key in ("S0", "S1", "S2"):
         ref = b[key]
+        err = np.max(np.abs(a[key] - ref)) / np.max(np.abs(ref))
+        assert err < 1e-11, (key, err)
+
+
+@pytest.mark.parametrize("prm", CASES[:2] + CASES[3:], ids=lambda p: f"N{p.N}J{p.J}Q{p.Q}{p.pad[0]}Q2{p.Q2}")
+def test_time_scattering_equals_bruteforce(prm):
+    # Scattering1D second order (NEXT-2): |U1 * psi_alpha| * phi_T, no lambda convolution
+    rng = np.random.default_rng(prm.N + 7)
+    x = rng.standard_normal(prm.N)
+    a = O.time_scattering(x, prm)
+    b = brute_jtfs(x, prm)
+    s = O.schedule(prm)
+    assert a["S2"].shape == (sum(len(s.adm[al]) for al in s.alphas), s.n_frames)
+    for key, ref in (("S0", b["S0"]), ("S1", b["S1"]), ("S2", b["S2t"])):
         err = np.max(np.abs(a[key] - ref)) / np.max(np.abs(ref))
         assert err < 1e-11, (key, err)
 

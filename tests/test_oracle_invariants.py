@@ -141,3 +141,22 @@ def test_output_nonnegative_except_phi_phi():
     for i, p in enumerate(s.paths):
         if p[0] != O.PHI_T_PHI_F:
             assert np.all(r["S2"][i] >= -1e-12 * np.abs(r["S2"]).max())
+
+
+def test_time_scattering_invariants():
+    # Scattering1D (NEXT-2): zero -> zero, positive homogeneity, non-negativity,
+    # periodic shift by T -> frame shift, and first order identical to the JTFS's
+    prm = O.Params(N=2 ** 10, J=6, Q=8, J_fr=3, T=2 ** 6, F=8, pad="periodic")
+    s = O.schedule(prm)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(prm.N)
+    r = O.time_scattering(x, prm, s=s)
+    z = O.time_scattering(np.zeros(prm.N), prm, s=s)
+    assert all(np.all(v == 0) for v in z.values())
+    r3 = O.time_scattering(-3.0 * x, prm, s=s)
+    np.testing.assert_allclose(r3["S2"], 3.0 * r["S2"], rtol=1e-12, atol=1e-12 * np.abs(r["S2"]).max())
+    assert r["S2"].min() >= -1e-12 * r["S2"].max()
+    sh = O.time_scattering(np.roll(x, prm.T), prm, s=s)
+    np.testing.assert_allclose(sh["S2"][:, 1:], r["S2"][:, :-1], rtol=1e-9, atol=1e-12 * np.abs(r["S2"]).max())
+    j = O.jtfs_forward(x, prm, s=s, paths=[])
+    np.testing.assert_array_equal(j["S1"], r["S1"])
