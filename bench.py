@@ -12,6 +12,10 @@ event times; the L2 is flushed (256 MiB write) before every timed step.
 Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle
 (the reference arm of this tier) on the same workload, one signal per step.
 
+`--workload scat1d`: second-order time scattering at the
+paper's Scattering1D setting (J = 13, Q = 16, T = 2^11, 32 frames),
+256 notes per GPU, signals/s.
+
 `--workload c4` (not the headline metric): latency of ONE long
 signal (bird texture, N = 2^17, J = 13) path-sharded over the ranks
 (paper_2204_08269_b200/shard.py: KD units split by LPT, partials summed onto
@@ -33,6 +37,7 @@ sys.path.insert(0, ROOT)
 
 CFG = dict(N=2 ** 16, J=12, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
 CFG4 = dict(N=2 ** 17, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
+CFGS1D = dict(N=2 ** 16, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 11, F=4)
 METRIC = "JTFS signals/s (N=2^16,J=12,Q=16) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "signals/s"
 WORKLOAD = "instrument-note batch (BASELINE configs[2]): N=2^16, J=12, Q=16, J_fr=5, Q_fr=1, T=2^13, F=4"
@@ -183,6 +188,48 @@ def run_c4(args, rank, world, local, dev):
     return 0
 
 
+def run_scat1d(args, rank, world, local, dev):
+    """Time scattering throughput (NEXT-2), batch-sharded like c3."""
+    import torch
+    import torch.distributed as dist
+    from paper_2204_08269_b200 import jtfs, signals
+    B = args.batch
+    plan = jtfs.Plan(**{k: CFGS1D[k] for k in ("N", "J", "Q", "J_fr", "Q_fr", "T", "F")}, device=local)
+    x = torch.from_numpy(signals.notes(B, seed0=1000 + rank * B)).to(dev)
+    out = torch.empty(B, plan.scat1d_layout.floats_per_signal, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        plan.scattering1d(x, out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        plan.scattering1d(x, out)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    if rank == 0:
+        lay = plan.scat1d_layout
+        print(json.dumps({
+            "metric": "time scattering (Scattering1D) signals/s (N=2^16, J=13, Q=16, T=2^11)",
+            "value": B * world * args.steps / (total_ms / 1e3), "unit": "signals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "notes, Scattering1D setting of P:309-310", "batch_per_gpu": B,
+                       "n1": lay.n1, "n2": lay.n2, "frames": lay.n_frames,
+                       "l2": "flushed before every timed step (256 MiB write)", **CFGS1D}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,7 +238,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="signals per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "scat1d"])
     args = ap.parse_args()
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -212,6 +259,8 @@ def main():
         dist.barrier()
     if args.workload == "c4":
         return run_c4(args, rank, world, local, dev)
+    if args.workload == "scat1d":
+        return run_scat1d(args, rank, world, local, dev)
     from paper_2204_08269_b200 import jtfs, signals
 
     B = args.batch

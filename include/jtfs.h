@@ -202,6 +202,32 @@ JTFS_API jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_
 JTFS_API jtfs_status jtfs_reduce_pack(jtfs_plan_t plan, const float* partials, int64_t B, float* out,
                                       void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Second-order time scattering (Scattering1D):
+ * "applying only a 1-D temporal wavelet filterbank to the first-order
+ * scalogram": S2_t[lambda, alpha] = (|U1_lambda * psi_alpha| * phi_T) at the
+ * retained frames, over the plan's admissible pairs j1(lambda) < j2(alpha)
+ * (DESIGN.md §3 R7) -- the JTFS's Y2 without the lambda convolution.  Shares
+ * every first stage of jtfs_forward (KA..KC); the frequential filters of the
+ * plan are unused.  Record of one signal, fp32:
+ *   [ S0 : n_frames ][ S1 : n1 x n_frames ][ S2_t : n2 x n_frames ],
+ * S2_t rows alpha-major (active alphas in jtfs_paths order), then lambda. */
+typedef struct {
+  int32_t n1, n2, n_frames, frame0;
+  int64_t off_s0, off_s1, off_s2, floats_per_signal;
+} jtfs_scat1d_layout_t;
+
+JTFS_API jtfs_status jtfs_scat1d_layout(jtfs_plan_t plan, jtfs_scat1d_layout_t* layout);
+
+/* (lambda, alpha) of every S2_t row: pairs[2 r] = lambda (first-order filter
+ * index), pairs[2 r + 1] = alpha (second-order bank index); writes min(cap, n2) rows. */
+JTFS_API jtfs_status jtfs_scat1d_paths(jtfs_plan_t plan, int32_t* pairs, int32_t cap);
+
+/* Time scattering of x (device fp32 [B][N]) into out (device fp32
+ * [B][floats_per_signal of jtfs_scat1d_layout]); same workspace, stream and
+ * error rules as jtfs_forward. */
+JTFS_API jtfs_status jtfs_scattering1d(jtfs_plan_t plan, const float* x, int64_t B, float* out,
+                                       void* ws, size_t ws_bytes, void* stream);
+
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)

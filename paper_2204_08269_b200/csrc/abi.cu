@@ -439,6 +439,70 @@ jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B, 
   return JTFS_OK;
 }
 
+// ---- second-order time scattering (jtfs.h: jtfs_scat1d_layout / _paths / jtfs_scattering1d) ----
+namespace {
+void scat1d_layout_of(const jtfs::Plan& P, jtfs_scat1d_layout_t* o) {
+  int n2 = 0;
+  for (const auto& d : P.kd) n2 += d.K;
+  o->n1 = P.n1;
+  o->n2 = n2;
+  o->n_frames = P.n_frames;
+  o->frame0 = P.frame0;
+  o->off_s0 = 0;
+  o->off_s1 = P.n_frames;
+  o->off_s2 = o->off_s1 + (int64_t)P.n1 * P.n_frames;
+  o->floats_per_signal = o->off_s2 + (int64_t)n2 * P.n_frames;
+}
+}  // namespace
+
+jtfs_status jtfs_scat1d_layout(jtfs_plan_t plan, jtfs_scat1d_layout_t* layout) {
+  if (!plan || !layout) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  scat1d_layout_of(plan->P, layout);
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_scat1d_paths(jtfs_plan_t plan, int32_t* pairs, int32_t cap) {
+  if (!plan || (cap > 0 && !pairs) || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  int32_t r = 0;
+  for (const auto& d : plan->P.kd)
+    for (int l = 0; l < d.K; ++l, ++r)
+      if (r < cap) {
+        pairs[2 * r] = l;
+        pairs[2 * r + 1] = d.alpha;
+      }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_scattering1d(jtfs_plan_t plan, const float* x, int64_t B, float* out, void* ws, size_t ws_bytes,
+                              void* stream) {
+  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK || B == 0) return s;
+  jtfs::Plan& P = plan->P;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mb = std::min<int64_t>(B, P.mb);
+  WsPtrs w = carve(P, ws, mb);
+  jtfs_scat1d_layout_t lay;
+  scat1d_layout_of(P, &lay);
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    const int nb = (int)std::min<int64_t>(mb, B - b0);
+    const float* xb = x + b0 * P.N;
+    float* ob = out + b0 * lay.floats_per_signal;
+    { StageScope sc(P, 0, st); sc.done(jtfs::launch_pad_fft(P, xb, nb, w.xhat, w.tmp, st)); }
+    { StageScope sc(P, 1, st); sc.done(jtfs::launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st)); }
+    {
+      StageScope sc(P, 2, st);
+      sc.done(jtfs::launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, ob, lay.floats_per_signal, lay.off_s0,
+                                     lay.off_s1, P.d_u1_off, P.d_k1, P.d_band_L1, st));
+    }
+    { StageScope sc(P, 3, st); sc.done(jtfs::launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
+    { StageScope sc(P, 4, st); sc.done(jtfs::launch_time_scat(P, w.y2, nb, ob, lay.floats_per_signal, lay.off_s2, st)); }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return JTFS_OK;
+}
+
 // ---- path sharding (jtfs.h: jtfs_units / jtfs_forward_units / jtfs_reduce_pack) ----
 namespace {
 // unit table of one signal: alpha-major, chunk-minor

@@ -762,6 +762,84 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2,
   return n;
 }
 
+// ---------------------------------------------------------------------------------
+// KT: second-order time scattering (Scattering1D):
+// S2_t[alpha][lambda][m] = sum_t g_alpha[(frame0 + m) D - t mod L] |Y2_alpha[lambda](t)|
+// -- the phi_T pooling of |Y2| at the retained frames, no lambda convolution.
+// One CTA per (signal, lambda row); fixed-order reduction (bit-stable).
+// ---------------------------------------------------------------------------------
+struct KTParams {
+  const float* y2;   // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
+  const float* g;    // phi_T taps g_alpha[L]
+  float* out;        // out record of signal 0 at row0's first frame; signal stride fps
+  int64_t y2_stride, fps;
+  int L, D, frame0, nframes, K;
+};
+
+template <int NF>
+__global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
+  __shared__ float red[8][NF];
+  const int b = blockIdx.x / p.K, l = blockIdx.x % p.K;
+  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * l) * p.L;
+  const float* im = re + p.L;
+  float acc[NF];
+#pragma unroll
+  for (int m = 0; m < NF; ++m) acc[m] = 0.f;
+  for (int t = threadIdx.x; t < p.L; t += 256) {
+    const float a = __ldg(re + t), c = __ldg(im + t);
+    const float mag = sqrtf(fmaf(a, a, c * c));
+#pragma unroll
+    for (int m = 0; m < NF; ++m) {
+      if (m < p.nframes) {
+        int i = ((p.frame0 + m) * p.D - t) % p.L;
+        if (i < 0) i += p.L;
+        acc[m] = fmaf(__ldg(p.g + i), mag, acc[m]);
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < NF; ++m) {
+    float v = acc[m];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][m] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NF && threadIdx.x < p.nframes) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    p.out[(int64_t)b * p.fps + (int64_t)l * p.nframes + threadIdx.x] = v;
+  }
+}
+
+int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64_t fps, int64_t off_s2,
+                     cudaStream_t st) {
+  int row0 = 0, n = 0;
+  for (const auto& d : P.kd) {
+    KTParams k{};
+    k.y2 = y2 + 2 * d.y2_off;
+    k.g = P.d_g + d.g_off;
+    k.out = out + off_s2 + (int64_t)row0 * P.n_frames;
+    k.y2_stride = 2 * P.y2_total;
+    k.fps = fps;
+    k.L = d.L;
+    k.D = d.D;
+    k.frame0 = P.frame0;
+    k.nframes = P.n_frames;
+    k.K = d.K;
+    const int grid = nsig * d.K;
+    if (P.n_frames <= 8) k_time_scat<8><<<grid, 256, 0, st>>>(k);
+    else if (P.n_frames <= 16) k_time_scat<16><<<grid, 256, 0, st>>>(k);
+    else if (P.n_frames <= 32) k_time_scat<32><<<grid, 256, 0, st>>>(k);
+    else k_time_scat<64><<<grid, 256, 0, st>>>(k);
+    row0 += d.K;
+    ++n;
+  }
+  return n;
+}
+
 int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, const UnitSel* sel) {
   int n = 0;
   for (size_t i = 0; i < P.kd.size(); ++i) {

@@ -65,6 +65,8 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2,
 int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, const UnitSel* sel = nullptr);
 size_t ke_smem_bytes(const Plan& P);
 int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
+int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64_t fps, int64_t off_s2,
+                     cudaStream_t st);
 cudaError_t ke_set_smem(const Plan& P);
 int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st, int* err,
                  const UnitSel* sel = nullptr);

@@ -34,6 +34,7 @@ EXPORTS = [
     "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_cost", "jtfs_profile_enable",
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
+    "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -54,6 +55,11 @@ class jtfs_layout_t(C.Structure):
 class jtfs_path_t(C.Structure):
     _fields_ = [("kind", C.c_int32), ("theta", C.c_int32), ("alpha", C.c_int32), ("beta", C.c_int32),
                 ("xi_alpha", C.c_double), ("xi_beta", C.c_double)]
+
+
+class jtfs_scat1d_layout_t(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("n1", "n2", "n_frames", "frame0")] + \
+               [(n, C.c_int64) for n in ("off_s0", "off_s1", "off_s2", "floats_per_signal")]
 
 
 class jtfs_unit_t(C.Structure):
@@ -82,6 +88,9 @@ _lib.jtfs_units.argtypes = [_P, C.POINTER(jtfs_unit_t), C.c_int32, C.POINTER(C.c
 _lib.jtfs_partials_size.argtypes = [_P, C.POINTER(C.c_int64)]
 _lib.jtfs_forward_units.argtypes = [_P, _P, C.c_int64, C.POINTER(C.c_int32), C.c_int32, _P, _P, _P, C.c_size_t, _P]
 _lib.jtfs_reduce_pack.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
+_lib.jtfs_scat1d_layout.argtypes = [_P, C.POINTER(jtfs_scat1d_layout_t)]
+_lib.jtfs_scat1d_paths.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32]
+_lib.jtfs_scattering1d.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -268,6 +277,40 @@ class Plan:
         _check(_lib.jtfs_reduce_pack(self._h, _ptr(partials), B, _ptr(out), _ptr(ws), ws.numel(),
                                      _stream_handle(stream)), "jtfs_reduce_pack")
         return out
+
+    # ---- second-order time scattering (jtfs_scat1d_layout / _paths / jtfs_scattering1d) ----
+    @property
+    def scat1d_layout(self):
+        lay = jtfs_scat1d_layout_t()
+        _check(_lib.jtfs_scat1d_layout(self._h, C.byref(lay)), "jtfs_scat1d_layout")
+        return lay
+
+    def scat1d_paths(self):
+        """[(lambda, alpha)] of every S2_t row."""
+        n = self.scat1d_layout.n2
+        arr = (C.c_int32 * max(2 * n, 1))()
+        _check(_lib.jtfs_scat1d_paths(self._h, arr, n), "jtfs_scat1d_paths")
+        return [(arr[2 * r], arr[2 * r + 1]) for r in range(n)]
+
+    def scattering1d(self, x, out=None, stream=None):
+        """Time scattering: x float32 CUDA [B, N] -> [B, n_frames (1 + n1 + n2)]."""
+        import torch
+        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+        B = x.shape[0]
+        lay = self.scat1d_layout
+        if out is None:
+            out = torch.empty(B, lay.floats_per_signal, dtype=torch.float32, device=x.device)
+        ws = self.workspace(B)
+        _check(_lib.jtfs_scattering1d(self._h, _ptr(x), B, _ptr(out), _ptr(ws), ws.numel(),
+                                      _stream_handle(stream)), "jtfs_scattering1d")
+        return out
+
+    def unpack_scat1d(self, out):
+        lay = self.scat1d_layout
+        fr = lay.n_frames
+        return (out[..., lay.off_s0:lay.off_s0 + fr],
+                out[..., lay.off_s1:lay.off_s2].reshape(*out.shape[:-1], lay.n1, fr),
+                out[..., lay.off_s2:].reshape(*out.shape[:-1], lay.n2, fr))
 
     def debug_tap(self, tap: int, x):
         import torch

@@ -114,3 +114,27 @@ def test_host_plan_refuses_forward_and_destroy_null(jt):
     assert st == jt.JTFS_ERR_UNSUPPORTED
     assert p.workspace_size(8) > 0
     p.close()
+
+
+# ---- second-order time scattering (Scattering1D) ----
+SCAT1D = dict(N=2 ** 16, J=13, Q=16, J_fr=5, T=2 ** 11, F=4)   # the paper's setting
+
+
+@pytest.mark.parametrize("kw", [dict(N=2 ** 10, J=6, Q=8, J_fr=3, T=2 ** 6, F=8), SCAT1D],
+                         ids=["c1", "paper_s1d"])
+def test_scat1d_layout_and_paths_match_oracle(jt, kw):
+    plan = jt.Plan(**kw, device=-1)
+    lay = plan.scat1d_layout
+    s = O.schedule(O.Params(**kw))
+    pairs = [(lam, a) for a in s.alphas for lam in s.adm[a]]
+    assert lay.n1 == s.n1 and lay.n_frames == s.n_frames and lay.n2 == len(pairs)
+    assert plan.scat1d_paths() == pairs
+    assert lay.floats_per_signal == s.n_frames * (1 + s.n1 + len(pairs))
+
+
+def test_scat1d_paper_shape(jt):
+    # Q = 16, J = 13, T = 2^11 on the 2^16-sample excerpts -> 32 time frames,
+    # first order n1 = 175 (the 1423-dim vector = n1 + n2; n2 depends on the
+    # admissibility reading, so only n1 and the frames are pinned)
+    lay = jt.Plan(**SCAT1D, device=-1).scat1d_layout
+    assert (lay.n_frames, lay.n1) == (32, 175)
