@@ -105,16 +105,15 @@ __device__ __forceinline__ void dft_reg(CT (&v)[R]) {
 }
 
 // One Stockham pass of radix R over G rows of length L held in smem s[g*LS + padx(e)].
-// W: the length-L twiddle table exp(-2 pi i t / L), t < L, staged in shared memory.
+// Wp: this pass's twiddles in shared memory, Wp[(r - 1) * Ns + k] = exp(-2 pi i r k / (R Ns))
+// (k = j mod Ns is contiguous across a warp: conflict-free or broadcast reads).
 template <int LOG2L, int R, int G, int NT, int DIR, int LS, class CT>
-__device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* W) {
+__device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* Wp) {
   constexpr int L = 1 << LOG2L;
   constexpr int LR = L / R;
   constexpr int NBF = G * LR;
   constexpr int BPT = (NBF + NT - 1) / NT;
-  constexpr int LOG2R = ilog2c(R);
   const int Ns = 1 << log2Ns;
-  const int twshift = LOG2L - (log2Ns + LOG2R);
   CT v[BPT][R];
   int base[BPT];
 #pragma unroll
@@ -130,7 +129,7 @@ __device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* W) {
       if (Ns > 1) {
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-          const CT w = W[(r * k) << twshift];
+          const CT w = Wp[(r - 1) * Ns + k];
           v[i][r] = cmul(v[i][r], DIR < 0 ? w : CxT<CT>::make(w.x, -w.y));
         }
       }
@@ -151,19 +150,35 @@ __device__ __forceinline__ void stockham_pass(CT* s, int log2Ns, const CT* W) {
   __syncthreads();
 }
 
-// Stage the length-L twiddle table (contiguous in global memory) into shared memory.
+// Stage the per-pass twiddle tables of a length-L FFT into shared memory (at
+// most L entries): for every pass with Ns > 1 (same pass sequence as fft_smem),
+// Ws[off + (r - 1) * Ns + k] = W_L[(r k) << (LOG2L - log2Ns - log2R)], read from
+// the contiguous length-L table Wg (exp(-2 pi i t / L)).
 template <int LOG2L, int NT, class CT>
 __device__ __forceinline__ void stage_twiddles(CT* Ws, const CT* __restrict__ Wg) {
-#pragma unroll 4
-  for (int t = threadIdx.x; t < (1 << LOG2L); t += NT) Ws[t] = __ldg(Wg + t);
+  constexpr int REM = LOG2L % 3;
+  int off = 0, log2Ns = REM;  // the radix-2^REM pass runs at Ns = 1 (no twiddles)
+  if constexpr (LOG2L >= 3) {
+    for (int p = 0; p < LOG2L / 3; ++p, log2Ns += 3) {
+      const int Ns = 1 << log2Ns;
+      if (Ns > 1) {
+        const int sh = LOG2L - log2Ns - 3;
+        for (int idx = threadIdx.x; idx < 7 * Ns; idx += NT) {
+          const int r = idx / Ns + 1, k = idx % Ns;
+          Ws[off + idx] = __ldg(Wg + ((r * k) << sh));
+        }
+        off += 7 * Ns;
+      }
+    }
+  }
 }
 
 // Full FFT of G rows in smem (caller has __syncthreads()'d after filling s and the
-// shared twiddle table Ws of length L).
+// shared per-pass twiddle tables Ws built by stage_twiddles<LOG2L>).
 template <int LOG2L, int G, int NT, int DIR, int LS = pad_row(1 << LOG2L), class CT>
 __device__ __forceinline__ void fft_smem(CT* s, const CT* Ws) {
   constexpr int REM = LOG2L % 3;
-  int log2Ns = 0;
+  int log2Ns = 0, off = 0;
   if constexpr (REM != 0) {
     stockham_pass<LOG2L, (1 << REM), G, NT, DIR, LS>(s, 0, Ws);
     log2Ns = REM;
@@ -171,7 +186,8 @@ __device__ __forceinline__ void fft_smem(CT* s, const CT* Ws) {
   if constexpr (LOG2L >= 3) {
 #pragma unroll 1
     for (int p = 0; p < LOG2L / 3; ++p) {
-      stockham_pass<LOG2L, 8, G, NT, DIR, LS>(s, log2Ns, Ws);
+      stockham_pass<LOG2L, 8, G, NT, DIR, LS>(s, log2Ns, Ws + off);
+      if (log2Ns > 0) off += 7 << log2Ns;
       log2Ns += 3;
     }
   }
