@@ -657,13 +657,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         e_math += clock64() - tm0;
-#pragma unroll
-        for (int k = 0; k < MAXSLOT; ++k)
-          if (k == mb) {
-#pragma unroll
-            for (int m = 0; m < NF / 2; ++m)
-              accr[k][m] = make_float2(fmaf(part[m].x, inv, accr[k][m].x), fmaf(part[m].y, inv, accr[k][m].y));
-          }
+        // warp-uniform branch to the M-block's slot (a predicated loop over all
+        // MAXSLOT slots would issue MAXSLOT x NF FMAs)
+        switch (mb) {
+#define JTFS_ACC_SLOT(K)                                                                         \
+  case K:                                                                                        \
+    if constexpr (K < MAXSLOT) {                                                                 \
+      _Pragma("unroll") for (int m = 0; m < NF / 2; ++m) accr[K][m] = ffma2(part[m], inv, accr[K][m]); \
+    }                                                                                            \
+    break;
+          JTFS_ACC_SLOT(0) JTFS_ACC_SLOT(1) JTFS_ACC_SLOT(2) JTFS_ACC_SLOT(3) JTFS_ACC_SLOT(4)
+          JTFS_ACC_SLOT(5) JTFS_ACC_SLOT(6) JTFS_ACC_SLOT(7) JTFS_ACC_SLOT(8)
+#undef JTFS_ACC_SLOT
+          default: break;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(w_empty + wi);  // this warp is done with the tile's taps
