@@ -71,6 +71,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   UP(P.d_wtab, P.wtab.data(), P.wtab.size() * 4);
   UP(P.d_g, P.g.data(), P.g.size() * 4);
   UP(P.d_W, P.W.data(), P.W.size() * 4);
+  UP(P.d_Wrange, P.Wrange.data(), P.Wrange.size() * 4);
   UP(P.d_hphi, P.hphi.data(), P.hphi.size() * 4);
   UP(P.d_twiddle, P.twiddle.data(), P.twiddle.size() * 4);
   UP(P.d_twiddle64, P.twiddle64.data(), P.twiddle64.size() * 8);
@@ -91,7 +92,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
     std::vector<DevFilter> df;
     std::vector<int32_t> rp;
     for (const auto& f : P.fr) {
-      df.push_back(DevFilter{f.k, f.nrows, f.row0, (int32_t)rp.size(), f.w_off});
+      df.push_back(DevFilter{f.k, f.nrows, f.row0, (int32_t)rp.size(), f.w_off, f.wr_off});
       rp.insert(rp.end(), f.rprime.begin(), f.rprime.end());
     }
     UP(P.d_fr, df.data(), df.size() * sizeof(DevFilter));
@@ -235,6 +236,7 @@ void fill_ke_params(jtfs::Plan& P, jtfs::KEParams& kp, const float* part, const 
   kp.alphas = (const DevAlpha*)P.d_alphas;
   kp.rprime = P.d_rprime;
   kp.W = P.d_W;
+  kp.Wrange = (const int2*)P.d_Wrange;
   const int nbeta = (int)P.bf.xi.size();
   kp.hpsi = (const float2*)P.d_hphi;
   kp.hphiF = P.d_hphi + (size_t)2 * nbeta * P.N_fr;

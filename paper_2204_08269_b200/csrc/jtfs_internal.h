@@ -90,6 +90,7 @@ struct FrFilter {
   int row0, nrows;  // row block inside the M rows of every alpha
   std::vector<int> rprime;  // the retained rows r' (decimated grid indices)
   int64_t w_off;    // float offset of the lambda-pooling matrix W [lambda_out][nrows]
+  int64_t wr_off;   // offset (int pairs) of the per-output band [first, last] of W's row q in Wrange
 };
 
 struct Plan {
@@ -125,6 +126,7 @@ struct Plan {
   int64_t y16_total = 0, ys_total = 0;   // per signal: fp16 elements of Y16, per-tile scale slots
   std::vector<float> g;                  // time pooling taps per alpha
   std::vector<float> W;                  // lambda pooling matrices per filter
+  std::vector<int32_t> Wrange;           // per filter and output row q: first, last + 1 row of |W| >= 1e-9 max
   std::vector<float> hphi;               // phi_t paths: [n_beta][N_fr] complex psi_{beta,+1} taps,
                                          // then [N_fr] real phi_F taps, then [NPT] real phi_T taps
   std::vector<float> twiddle;            // per-length tables exp(-2 pi i t / L), L = 2..N_tw, at offset L - 2
@@ -140,6 +142,7 @@ struct Plan {
   float* d_wtab = nullptr;
   float* d_g = nullptr;
   float* d_W = nullptr;
+  int32_t* d_Wrange = nullptr;
   float* d_hphi = nullptr;
   float* d_twiddle = nullptr;
   double* d_twiddle64 = nullptr;

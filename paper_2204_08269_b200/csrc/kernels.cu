@@ -563,11 +563,19 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
     // spinned or psi_t x phi_f: sum the KD partials over chunks in fixed order
     const DevAlpha a = p.alphas[P.alpha_slot];
     const float* part = p.part + (int64_t)b * p.part_stride + a.part_off;
+    const int64_t cstride = (int64_t)p.Mpad * nf;
     for (int idx = threadIdx.x; idx < f.nrows * nf; idx += blockDim.x) {
-      const int r = idx / nf, m = idx % nf;
+      const float* src = part + (int64_t)f.row0 * nf + idx;  // (row0 + r) * nf + m
       float acc = 0.f;
-      for (int c = 0; c < a.nchunks; ++c)
-        acc += part[((int64_t)c * p.Mpad + f.row0 + r) * nf + m];
+      int c = 0;
+      for (; c + 8 <= a.nchunks; c += 8) {  // 8 loads in flight, sums in fixed order
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (c + j) * cstride);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += v[j];
+      }
+      for (; c < a.nchunks; ++c) acc += __ldg(src + c * cstride);
       Pm[idx] = acc;
     }
     __syncthreads();
@@ -575,8 +583,10 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
   const float* Wf = p.W + f.w_off;
   for (int idx = threadIdx.x; idx < p.lam_out * nf; idx += blockDim.x) {
     const int q = idx / nf, m = idx % nf;
+    const int2 band = __ldg(p.Wrange + f.wr_off + q);  // rows with |W| >= 1e-9 max (plan.cpp)
+    const float* wq = Wf + (int64_t)q * f.nrows;
     float acc = 0.f;
-    for (int r = 0; r < f.nrows; ++r) acc = fmaf(__ldg(Wf + (int64_t)q * f.nrows + r), Pm[r * nf + m], acc);
+    for (int r = band.x; r < band.y; ++r) acc = fmaf(__ldg(wq + r), Pm[r * nf + m], acc);
     outp[idx] = acc;
   }
 }

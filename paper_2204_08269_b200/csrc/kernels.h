@@ -33,6 +33,7 @@ struct DevPath {
 struct DevFilter {
   int32_t k, nrows, row0, rp_off;
   int64_t w_off;
+  int64_t wr_off;  // [lam_out] int2 {first, last + 1} row of each output's phi_F band
 };
 struct DevAlpha {
   int32_t nchunks, pad;
@@ -45,6 +46,7 @@ struct KEParams {
   const DevAlpha* alphas;
   const int32_t* rprime;
   const float* W;
+  const int2* Wrange;
   const float2* hpsi;  // [n_beta][N_fr] psi_{beta,+1} taps
   const float* hphiF;  // [N_fr]
   const float* gT;     // [NPT]

@@ -365,6 +365,23 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       for (int q = 0; q < P.lam_out; ++q)
         for (int i = 0; i < f.nrows; ++i) P.W.push_back(q == f.rprime[i] ? 1.f : 0.f);
     }
+    // per output row q: the band [first, last] of rows with |W| >= kEpsPool of the
+    // filter's largest weight (the same cut that selects the retained rows)
+    {
+      double wmax = 0;
+      for (int64_t i = f.w_off; i < (int64_t)P.W.size(); ++i) wmax = std::max(wmax, (double)std::fabs(P.W[i]));
+      f.wr_off = (int64_t)P.Wrange.size() / 2;
+      for (int q = 0; q < P.lam_out; ++q) {
+        int lo = f.nrows, hi = -1;
+        for (int i = 0; i < f.nrows; ++i)
+          if (std::fabs((double)P.W[f.w_off + (int64_t)q * f.nrows + i]) >= kEpsPool * wmax) {
+            lo = std::min(lo, i);
+            hi = std::max(hi, i);
+          }
+        P.Wrange.push_back(lo);
+        P.Wrange.push_back(hi + 1);
+      }
+    }
     f.row0 = P.M;
     P.M += f.nrows;
   }
