@@ -16,6 +16,11 @@ Prints ONE JSON line on rank 0.  `--impl reference` times the fp64 CPU oracle
 paper's Scattering1D setting (J = 13, Q = 16, T = 2^11, 32 frames),
 256 notes per GPU, signals/s.
 
+`--workload resynth`: texture resynthesis (the paper's only timing:
+720 ms per iteration): one bird-texture signal N = 2^16, J = 12, Q = 12,
+T = 2^13; an iteration is forward + normalised-error loss + jtfs_backward + bold-driver
+step; ms per iteration (lower is better), E after 20 and 100 iterations.
+
 `--workload c4` (not the headline metric): latency of ONE long
 signal (bird texture, N = 2^17, J = 13) path-sharded over the ranks
 (paper_2204_08269_b200/shard.py: KD units split by LPT, partials summed onto
@@ -38,6 +43,7 @@ sys.path.insert(0, ROOT)
 CFG = dict(N=2 ** 16, J=12, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
 CFG4 = dict(N=2 ** 17, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
 CFGS1D = dict(N=2 ** 16, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 11, F=4)
+CFGRS = dict(N=2 ** 16, J=12, Q=12, J_fr=5, Q_fr=1, T=2 ** 13, F=32)  # P:359, P:366, P:370 (F = 2^J_fr, R12)
 METRIC = "JTFS signals/s (N=2^16,J=12,Q=16) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "signals/s"
 WORKLOAD = "instrument-note batch (BASELINE configs[2]): N=2^16, J=12, Q=16, J_fr=5, Q_fr=1, T=2^13, F=4"
@@ -230,6 +236,43 @@ def run_scat1d(args, rank, world, local, dev):
     return 0
 
 
+def run_resynth(args, rank, world, local, dev):
+    """Texture resynthesis iteration time (NEXT-1), one signal per GPU."""
+    import torch
+    import torch.distributed as dist
+    from paper_2204_08269_b200 import jtfs, resynth, signals
+    plan = jtfs.Plan(**{k: CFGRS[k] for k in ("N", "J", "Q", "J_fr", "Q_fr", "T", "F")}, device=local)
+    x = torch.from_numpy(signals.bird_texture(2 ** 16, seed=7 + rank)[None, :].copy()).to(dev)
+    y0 = torch.from_numpy(signals.white(1, 2 ** 16, seed=100 + rank)).to(dev) * float(x.std())
+    resynth.resynthesize(plan, x, y0, iters=args.warmup)          # warm-up (plans, workspaces)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    iters = max(args.steps, 100)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    y, hist = resynth.resynthesize(plan, x, y0, iters=iters)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / (iters + 1)   # iters candidate evaluations + the initial gradient
+    if rank == 0:
+        print(json.dumps({
+            "metric": "texture resynthesis ms per iteration (forward + backward + step), N=2^16, J=12, Q=12, T=2^13",
+            "value": ms, "unit": "ms", "n_gpus": world, "steps": iters, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": ms / 720.0, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "resynthesis of one bird texture from white noise, bold driver",
+                       "E_after_20": hist[min(20, len(hist) - 1)], "E_after_100": hist[min(100, len(hist) - 1)],
+                       "E_0": hist[0], **CFGRS}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -238,7 +281,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="signals per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "scat1d"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "scat1d", "resynth"])
     args = ap.parse_args()
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -261,6 +304,8 @@ def main():
         return run_c4(args, rank, world, local, dev)
     if args.workload == "scat1d":
         return run_scat1d(args, rank, world, local, dev)
+    if args.workload == "resynth":
+        return run_resynth(args, rank, world, local, dev)
     from paper_2204_08269_b200 import jtfs, signals
 
     B = args.batch

@@ -228,6 +228,27 @@ JTFS_API jtfs_status jtfs_scat1d_paths(jtfs_plan_t plan, int32_t* pairs, int32_t
 JTFS_API jtfs_status jtfs_scattering1d(jtfs_plan_t plan, const float* x, int64_t B, float* out,
                                        void* ws, size_t ws_bytes, void* stream);
 
+/* ---- Backward: vector-Jacobian product of jtfs_forward for
+ * texture resynthesis by gradient descent (the gradient "is
+ * computed via reverse-ordered Hermitian adjoints of the forward scattering
+ * operations").  dx = d<dout, jtfs_forward(x)>/dx, every stage the exact
+ * adjoint of the forward kernels; the subgradient of |z| at z = 0 is 0.
+ *   x     device fp32 [B][N] (the point of linearisation; the forward intermediates
+ *         are recomputed)
+ *   dout  device fp32 [B][floats_per_signal] (gradient of the loss w.r.t. the record)
+ *   dx    device fp32 [B][N] (output)
+ * Workspace: jtfs_backward_workspace_size (separate from the forward's); same
+ * stream / error rules as jtfs_forward. */
+JTFS_API jtfs_status jtfs_backward_workspace_size(jtfs_plan_t plan, int64_t B, size_t* bytes);
+JTFS_API jtfs_status jtfs_backward(jtfs_plan_t plan, const float* x, int64_t B, const float* dout, float* dx,
+                                   void* ws, size_t ws_bytes, void* stream);
+
+/* Debug/test query: byte offsets inside the backward workspace (for B signals)
+ * of its regions, in this order: 0 X_hat, 1 tmp, 2 U1, 3 U1hat, 4 Y_phi, 5 Y2,
+ * 6 scratch out, 7 dP, 8 dY_phi, 9 dY2, 10 DFT(dY2), 11 dU1hat, 12 dU1, 13 W,
+ * 14 DFT(dU1 W/|W|), 15 dX_hat, 16 dx_pad; offsets[17] = total.  Host query. */
+JTFS_API jtfs_status jtfs_backward_regions(jtfs_plan_t plan, int64_t B, int64_t* offsets, int32_t cap);
+
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)

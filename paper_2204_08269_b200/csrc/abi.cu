@@ -77,6 +77,33 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   UP(P.d_twiddle64, P.twiddle64.data(), P.twiddle64.size() * 8);
   for (auto& g : P.u1_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
   for (auto& g : P.y2_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
+  {
+    // backward tables (kernels.cu launch_backward)
+    std::vector<FoldRow> u1flat;
+    for (auto& g : P.u1_groups) u1flat.insert(u1flat.end(), g.rows.begin(), g.rows.end());
+    UP(P.u1_rows_flat, u1flat.data(), u1flat.size() * sizeof(FoldRow));
+    // y2 rows of (alpha, lambda): in each L group, alphas in kd order, K rows each
+    std::vector<std::vector<FoldRow>> per(P.n1);
+    for (auto& g : P.y2_groups) {
+      size_t r = 0;
+      for (const auto& d : P.kd) {
+        if (ilog2_exact(d.L) != g.log2L) continue;
+        for (int l = 0; l < d.K; ++l, ++r) {
+          FoldRow fr = g.rows[r];
+          fr.pad = g.log2L;
+          per[l].push_back(fr);
+        }
+      }
+    }
+    std::vector<FoldRow> flat;
+    std::vector<int32_t> off(1, 0);
+    for (int l = 0; l < P.n1; ++l) {
+      flat.insert(flat.end(), per[l].begin(), per[l].end());
+      off.push_back((int32_t)flat.size());
+    }
+    UP(P.d_bw_rows, flat.data(), std::max<size_t>(flat.size(), 1) * sizeof(FoldRow));
+    UP(P.d_bw_rowoff, off.data(), off.size() * 4);
+  }
   UP(P.d_u1_off, P.u1_off.data(), P.u1_off.size() * 8);
   {
     std::vector<int32_t> k1(P.k1.begin(), P.k1.end());
@@ -438,6 +465,112 @@ jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B, 
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "stream sync");
+  return JTFS_OK;
+}
+
+// ---- backward / VJP (jtfs.h: jtfs_backward_workspace_size / jtfs_backward) ----
+namespace {
+struct BwdLayoutBytes {
+  size_t xhat, tmp, u1, u1hat, yphi, y2, out, dP, dyphi, gy2, G, gu1hat, gu1, wb, gw, gxhat, gxpad, total;
+};
+BwdLayoutBytes bwd_layout(const jtfs::Plan& P, int64_t nb) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const jtfs::WsLayout f = jtfs::ws_layout(P, nb);
+  BwdLayoutBytes w{};
+  w.xhat = f.xhat;
+  w.tmp = f.tmp;
+  w.u1 = f.u1;
+  w.u1hat = f.u1hat;
+  w.yphi = f.yphi;
+  w.y2 = f.y2;
+  const int64_t fps = (int64_t)P.n_frames * (1 + P.n1) + (int64_t)P.paths.size() * P.lam_out * P.n_frames;
+  w.out = al((size_t)nb * fps * 4);
+  w.dP = al((size_t)nb * P.kd.size() * P.Mpad * P.n_frames * 4);
+  w.dyphi = al((size_t)nb * P.n1 * P.NPT * 4);
+  w.gy2 = al((size_t)nb * P.y2_total * 8);
+  w.G = al((size_t)nb * P.y2_total * 8);
+  w.gu1hat = al((size_t)nb * P.u1_total * 8);
+  w.gu1 = al((size_t)nb * P.u1_total * 4);
+  w.wb = al((size_t)nb * P.u1_total * 8);
+  w.gw = al((size_t)nb * P.u1_total * 8);
+  w.gxhat = al((size_t)nb * P.N_pad * 8);
+  w.gxpad = al((size_t)nb * P.N_pad * 4);
+  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.out + w.dP + w.dyphi + w.gy2 + w.G + w.gu1hat +
+            w.gu1 + w.wb + w.gw + w.gxhat + w.gxpad;
+  return w;
+}
+int64_t bwd_mb(const jtfs::Plan& P, int64_t B) {
+  const size_t per = bwd_layout(P, 1).total;
+  const int64_t cap = std::max<int64_t>(1, (int64_t)(((size_t)8 << 30) / std::max<size_t>(per, 1)));
+  return std::max<int64_t>(1, std::min<int64_t>(B, cap));
+}
+jtfs::BwdWs bwd_carve(const jtfs::Plan& P, void* ws, int64_t nb) {
+  const BwdLayoutBytes L = bwd_layout(P, nb);
+  char* c = (char*)ws;
+  jtfs::BwdWs w{};
+  w.xhat = (float2*)c; c += L.xhat;
+  w.tmp = (float2*)c; c += L.tmp;
+  w.u1 = (float*)c; c += L.u1;
+  w.u1hat = (float2*)c; c += L.u1hat;
+  w.yphi = (float*)c; c += L.yphi;
+  w.y2 = (float*)c; c += L.y2;
+  w.scratch_out = (float*)c; c += L.out;
+  w.dP = (float*)c; c += L.dP;
+  w.dyphi = (float*)c; c += L.dyphi;
+  w.gy2 = (float*)c; c += L.gy2;
+  w.G = (float2*)c; c += L.G;
+  w.gu1hat = (float2*)c; c += L.gu1hat;
+  w.gu1 = (float*)c; c += L.gu1;
+  w.wb = (float2*)c; c += L.wb;
+  w.gw = (float2*)c; c += L.gw;
+  w.gxhat = (float2*)c; c += L.gxhat;
+  w.gxpad = (float*)c; c += L.gxpad;
+  return w;
+}
+}  // namespace
+
+jtfs_status jtfs_backward_workspace_size(jtfs_plan_t plan, int64_t B, size_t* bytes) {
+  if (!plan || !bytes || B < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  *bytes = B == 0 ? 0 : bwd_layout(plan->P, bwd_mb(plan->P, B)).total;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_backward_regions(jtfs_plan_t plan, int64_t B, int64_t* offsets, int32_t cap) {
+  if (!plan || !offsets || B < 1 || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const BwdLayoutBytes L = bwd_layout(plan->P, bwd_mb(plan->P, B));
+  const size_t sz[17] = {L.xhat, L.tmp, L.u1, L.u1hat, L.yphi, L.y2, L.out, L.dP, L.dyphi,
+                         L.gy2, L.G, L.gu1hat, L.gu1, L.wb, L.gw, L.gxhat, L.gxpad};
+  int64_t o = 0;
+  for (int i = 0; i < 18 && i < cap; ++i) {
+    offsets[i] = o;
+    if (i < 17) o += (int64_t)sz[i];
+  }
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_backward(jtfs_plan_t plan, const float* x, int64_t B, const float* dout, float* dx, void* ws,
+                          size_t ws_bytes, void* stream) {
+  if (!plan) return fail(JTFS_ERR_INVALID_ARG, "plan is NULL");
+  jtfs::Plan& P = plan->P;
+  if (P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan (device = -1) cannot run backward");
+  if (B < 0) return fail(JTFS_ERR_INVALID_ARG, "B < 0");
+  if (B == 0) return JTFS_OK;
+  if (!x || !dout || !dx || !ws) return fail(JTFS_ERR_INVALID_ARG, "NULL buffer");
+  if (!aligned(x, 16) || !aligned(dout, 16) || !aligned(dx, 16) || !aligned(ws, 256))
+    return fail(JTFS_ERR_INVALID_ARG, "misaligned buffer");
+  const int64_t mb = bwd_mb(P, B);
+  if (ws_bytes < bwd_layout(P, mb).total) return fail(JTFS_ERR_WORKSPACE, "backward workspace too small");
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const jtfs::BwdWs w = bwd_carve(P, ws, mb);
+  jtfs_layout_t lay;
+  layout_of(P, &lay);
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    const int nb = (int)std::min<int64_t>(mb, B - b0);
+    jtfs::launch_backward(P, x + b0 * P.N, nb, dout + b0 * lay.floats_per_signal, dx + b0 * P.N, w, st);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return JTFS_OK;
 }
 

@@ -153,6 +153,11 @@ struct Plan {
   int64_t* d_u1_off = nullptr; // per lambda
   int32_t* d_k1 = nullptr;     // per lambda
   Band* d_band_L1 = nullptr;   // phi_T bands per k
+  // backward (VJP) tables: per lambda its (alpha, lambda) Y2 rows (pad = log2 L_alpha),
+  // offsets [n1 + 1]; the first-order rows in lambda order
+  FoldRow* d_bw_rows = nullptr;
+  int32_t* d_bw_rowoff = nullptr;
+  FoldRow* u1_rows_flat = nullptr;
   std::vector<void*> allocations;
 
   int mb = 16;                 // signals per micro-batch

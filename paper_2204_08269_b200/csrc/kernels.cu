@@ -597,6 +597,9 @@ __global__ void k_check_finite(const float* x, int64_t n, int* flag) {
     if (!isfinite(x[i])) atomicOr(flag, 1);
 }
 
+// backward (VJP) kernels -- see backward.inc
+#include "backward.inc"
+
 }  // namespace dev
 
 // =================================================================================
@@ -903,6 +906,207 @@ cudaError_t ke_set_smem(const Plan& P) {
 
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st) {
   k_check_finite<<<296, 256, 0, st>>>(x, n, flag);
+}
+
+
+// =================================================================================
+// backward (VJP) orchestration, see backward.inc
+// =================================================================================
+int launch_backward(Plan& P, const float* x, int nb, const float* dout, float* dx, const BwdWs& w,
+                    cudaStream_t st) {
+  int n = 0;
+  const float2* W32 = (const float2*)P.d_twiddle;
+  const int ltw = ilog2_exact(P.N_tw);
+  // ---- forward recompute of the intermediates (X_hat, U1hat, Y_phi, Y2) ----
+  n += launch_pad_fft(P, x, nb, w.xhat, w.tmp, st);
+  n += launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st);
+  jtfs_layout_t lay{};
+  {
+    int64_t off_s1 = P.n_frames, off_s2 = off_s1 + (int64_t)P.n1 * P.n_frames;
+    lay.off_s0 = 0;
+    lay.off_s1 = off_s1;
+    lay.off_s2 = off_s2;
+    lay.floats_per_signal = off_s2 + (int64_t)P.paths.size() * P.lam_out * P.n_frames;
+  }
+  n += launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, w.scratch_out, lay.floats_per_signal, lay.off_s0,
+                        lay.off_s1, P.d_u1_off, P.d_k1, (const Band*)P.d_band_L1, st);
+  n += launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st);
+  // ---- KE^T ----
+  const int NF = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : P.n_frames <= 32 ? 32 : 64;
+  const int64_t dP_stride = (int64_t)P.kd.size() * P.Mpad * P.n_frames;
+  cudaMemsetAsync(w.dP, 0, (size_t)nb * dP_stride * 4, st);
+  {
+    BwdKEParams k{};
+    k.paths = (const DevPath*)P.d_paths;
+    k.filters = (const DevFilter*)P.d_fr;
+    k.W = P.d_W;
+    k.Wrange = (const int2*)P.d_Wrange;
+    k.dout = dout;
+    k.dP = w.dP;
+    k.fps = lay.floats_per_signal;
+    k.off_s2 = lay.off_s2;
+    k.dP_stride = dP_stride;
+    k.lam_out = P.lam_out;
+    k.n_frames = P.n_frames;
+    k.Mpad = P.Mpad;
+    k_bwd_ke<<<dim3(nb, (unsigned)P.paths.size()), 256, 0, st>>>(k);
+    ++n;
+  }
+  {
+    BwdPhiParams k{};
+    k.paths = (const DevPath*)P.d_paths;
+    k.filters = (const DevFilter*)P.d_fr;
+    k.rprime = P.d_rprime;
+    k.W = P.d_W;
+    k.Wrange = (const int2*)P.d_Wrange;
+    const int nbeta = (int)P.bf.xi.size();
+    k.hpsi = (const float2*)P.d_hphi;
+    k.hphiF = P.d_hphi + (size_t)2 * nbeta * P.N_fr;
+    k.gT = k.hphiF + P.N_fr;
+    k.yphi = w.yphi;
+    k.dout = dout;
+    k.dyphi = w.dyphi;
+    k.fps = lay.floats_per_signal;
+    k.off_s2 = lay.off_s2;
+    k.n_paths = (int)P.paths.size();
+    k.n1 = P.n1;
+    k.NPT = P.NPT;
+    k.N_fr = P.N_fr;
+    k.lam_out = P.lam_out;
+    k.n_frames = P.n_frames;
+    k.frame0 = P.frame0;
+    k.k_phiphi = P.prm.average_fr ? P.log2F : 0;
+    int maxrows = 0;
+    for (const auto& f : P.fr) maxrows = std::max(maxrows, f.nrows);
+    const size_t sm = (size_t)2 * P.n1 * P.NPT * 4 + (size_t)maxrows * P.NPT * 8;
+    cudaFuncSetAttribute(k_bwd_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    k_bwd_phi<<<nb, 256, sm, st>>>(k);
+    ++n;
+  }
+  // ---- KD^T per alpha ----
+  for (size_t a = 0; a < P.kd.size(); ++a) {
+    const auto& d = P.kd[a];
+    BwdKDParams k{};
+    k.A = (const float2*)P.d_A + d.a_off;
+    k.y2 = w.y2 + 2 * d.y2_off;
+    k.dP = w.dP + (int64_t)a * P.Mpad * P.n_frames;
+    k.g = P.d_g + d.g_off;
+    k.gy2 = w.gy2 + 2 * d.y2_off;
+    k.y2_stride = 2 * P.y2_total;
+    k.dP_stride = dP_stride;
+    k.K = d.K;
+    k.Kpad = d.Kpad;
+    k.Mpad = P.Mpad;
+    k.L = d.L;
+    k.D = d.D;
+    k.frame0 = P.frame0;
+    k.nframes = P.n_frames;
+    const size_t sm = (size_t)d.Kpad * 32 * 8 + (size_t)d.Kpad * 64 * 8 + 64 * 32 * 8 + 32 * NF * 4 + 64 * NF * 4;
+    const int grid = nb * (d.L / 32);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      kern<<<grid, 256, sm, st>>>(k);
+    };
+    if (d.Kpad <= 64) {
+      if (NF == 8) go(k_bwd_kd<8, 64>); else if (NF == 16) go(k_bwd_kd<16, 64>); else go(k_bwd_kd<32, 64>);
+    } else if (d.Kpad <= 128) {
+      if (NF == 8) go(k_bwd_kd<8, 128>); else if (NF == 16) go(k_bwd_kd<16, 128>); else go(k_bwd_kd<32, 128>);
+    } else {
+      if (NF == 8) go(k_bwd_kd<8, 192>); else if (NF == 16) go(k_bwd_kd<16, 192>); else go(k_bwd_kd<32, 192>);
+    }
+    ++n;
+  }
+  // ---- KC^T: G = DFT(dY2) per y2 row ----
+  for (const auto& g : P.y2_groups) {
+    const int nr = (int)g.rows.size();
+    ProbPlanarC2C pc{w.gy2, w.G, 2 * P.y2_total, P.y2_total, g.d_rows, nr, 1 << g.log2L};
+    dispatch_log2(g.log2L, [&](auto c) {
+      constexpr int LG = decltype(c)::value;
+      if constexpr (LG <= 12) launch_rows<LG, -1>(pc, nb * nr, W32, ltw, st);
+      else launch_fft4<LG, -1>(pc, pc, nb * nr, w.tmp, W32, ltw, st);
+    });
+    n += g.log2L <= 12 ? 1 : 2;
+  }
+  {
+    BwdU1Params k{};
+    k.rows = P.d_bw_rows;
+    k.rowoff = P.d_bw_rowoff;
+    k.G = w.G;
+    k.G_stride = P.y2_total;
+    k.bandvals = P.d_bandvals;
+    k.u1_off = P.d_u1_off;
+    k.k1 = P.d_k1;
+    k.band_L1 = (const Band*)P.d_band_L1;
+    k.dout = dout;
+    k.dyphi = w.dyphi;
+    k.gu1hat = w.gu1hat;
+    k.u1_total = P.u1_total;
+    k.fps = lay.floats_per_signal;
+    k.off_s1 = lay.off_s1;
+    k.n1 = P.n1;
+    k.N_pad = P.N_pad;
+    k.NPT = P.NPT;
+    k.frame0 = P.frame0;
+    k.n_frames = P.n_frames;
+    k.total = (int64_t)nb * P.u1_total;
+    k_bwd_gather_u1hat<<<(unsigned)((k.total + 255) / 256), 256, 0, st>>>(k);
+    ++n;
+  }
+  // ---- KB^T ----
+  for (const auto& g : P.u1_groups) {
+    const int nr = (int)g.rows.size();
+    ProbC2RealRow pr{w.gu1hat, w.gu1, P.u1_total, g.d_rows, nr, 1.f};
+    ProbFoldComplex pw{w.xhat, P.N_pad, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, w.wb, P.u1_total};
+    ProbGradMod pg{w.gu1, w.wb, w.gw, P.u1_total, g.d_rows, nr};
+    dispatch_log2(g.log2L, [&](auto c) {
+      constexpr int LG = decltype(c)::value;
+      if constexpr (LG <= 12) {
+        launch_rows<LG, +1>(pr, nb * nr, W32, ltw, st);
+        launch_rows<LG, +1>(pw, nb * nr, W32, ltw, st);
+        launch_rows<LG, -1>(pg, nb * nr, W32, ltw, st);
+      } else {
+        launch_fft4<LG, +1>(pr, pr, nb * nr, w.tmp, W32, ltw, st);
+        launch_fft4<LG, +1>(pw, pw, nb * nr, w.tmp, W32, ltw, st);
+        launch_fft4<LG, -1>(pg, pg, nb * nr, w.tmp, W32, ltw, st);
+      }
+    });
+    n += g.log2L <= 12 ? 3 : 6;
+  }
+  {
+    BwdXParams k{};
+    k.rows = P.u1_rows_flat;
+    k.k1 = P.d_k1;
+    k.GW = w.gw;
+    k.u1_total = P.u1_total;
+    k.fps = lay.floats_per_signal;
+    k.off_s0 = lay.off_s0;
+    k.bandvals = P.d_bandvals;
+    k.band_pad = P.band_phiT_pad;
+    k.dout = dout;
+    k.gxhat = w.gxhat;
+    k.n1 = P.n1;
+    k.N_pad = P.N_pad;
+    k.NPT = P.NPT;
+    k.frame0 = P.frame0;
+    k.n_frames = P.n_frames;
+    k_bwd_gather_xhat<<<dim3((P.N_pad + 255) / 256, nb), 256, 0, st>>>(k);
+    ++n;
+  }
+  // ---- KA^T ----
+  {
+    ProbPadAdj pa{w.gxhat, w.gxpad, P.N_pad};
+    dispatch_log2(ilog2_exact(P.N_pad), [&](auto c) {
+      constexpr int LG = decltype(c)::value;
+      if constexpr (LG <= 12) launch_rows<LG, +1>(pa, nb, W32, ltw, st);
+      else launch_fft4<LG, +1>(pa, pa, nb, w.tmp, W32, ltw, st);
+    });
+    n += ilog2_exact(P.N_pad) <= 12 ? 1 : 2;
+    const int64_t total = (int64_t)nb * P.N;
+    k_bwd_unpad<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(w.gxpad, dx, P.N, P.N_pad, P.pad_left,
+                                                                 P.prm.pad_mode == JTFS_PAD_PERIODIC, total);
+    ++n;
+  }
+  return n;
 }
 
 }  // namespace jtfs

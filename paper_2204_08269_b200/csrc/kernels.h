@@ -73,6 +73,14 @@ cudaError_t ke_set_smem(const Plan& P);
 int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st, int* err,
                  const UnitSel* sel = nullptr);
 cudaError_t tc_setup_device(Plan& P);
+
+// backward (VJP) workspace pointers for one micro-batch (abi.cu carves them)
+struct BwdWs {
+  float2 *xhat, *tmp, *u1hat, *G, *gu1hat, *wb, *gw, *gxhat;
+  float *u1, *yphi, *y2, *scratch_out, *dP, *dyphi, *gy2, *gu1, *gxpad;
+};
+int launch_backward(Plan& P, const float* x, int nb, const float* dout, float* dx, const BwdWs& w,
+                    cudaStream_t st);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 
 }  // namespace jtfs

@@ -35,6 +35,7 @@ EXPORTS = [
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
+    "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -91,6 +92,9 @@ _lib.jtfs_reduce_pack.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_scat1d_layout.argtypes = [_P, C.POINTER(jtfs_scat1d_layout_t)]
 _lib.jtfs_scat1d_paths.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32]
 _lib.jtfs_scattering1d.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
+_lib.jtfs_backward_workspace_size.argtypes = [_P, C.c_int64, C.POINTER(C.c_size_t)]
+_lib.jtfs_backward.argtypes = [_P, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]
+_lib.jtfs_backward_regions.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), C.c_int32]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -277,6 +281,28 @@ class Plan:
         _check(_lib.jtfs_reduce_pack(self._h, _ptr(partials), B, _ptr(out), _ptr(ws), ws.numel(),
                                      _stream_handle(stream)), "jtfs_reduce_pack")
         return out
+
+    # ---- backward (vector-Jacobian product; jtfs_backward) ----
+    def backward(self, x, dout, dx=None, stream=None):
+        """dx = d<dout, forward(x)>/dx (x float32 CUDA [B, N], dout [B, floats_per_signal])."""
+        import torch
+        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and dout.is_contiguous()
+        B = x.shape[0]
+        if dx is None:
+            dx = torch.empty_like(x)
+        n = C.c_size_t()
+        _check(_lib.jtfs_backward_workspace_size(self._h, B, C.byref(n)), "jtfs_backward_workspace_size")
+        if getattr(self, "_bws", None) is None or self._bws.numel() < n.value:
+            self._bws = torch.empty(max(n.value, 1), dtype=torch.uint8, device=x.device)
+        _check(_lib.jtfs_backward(self._h, _ptr(x), B, _ptr(dout), _ptr(dx), _ptr(self._bws), self._bws.numel(),
+                                  _stream_handle(stream)), "jtfs_backward")
+        return dx
+
+    def backward_regions(self, B: int):
+        """Byte offsets of the backward workspace regions (jtfs_backward_regions)."""
+        arr = (C.c_int64 * 18)()
+        _check(_lib.jtfs_backward_regions(self._h, B, arr, 18), "jtfs_backward_regions")
+        return list(arr)
 
     # ---- second-order time scattering (jtfs_scat1d_layout / _paths / jtfs_scattering1d) ----
     @property
