@@ -170,9 +170,9 @@ __device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
 //  elements), lbo = stride between 64-element MN groups, sbo = 1024 between 8-row
 //  K groups.  (Both verified bit-exact with tools/tc_unit16.cu.)
 constexpr uint32_t kLayoutSW128 = 2, kLayoutSW32 = 6;
-constexpr int kRec = 16384;    // one A'' K-record: 128 rows x 16 fp16 x {re_hi, re_lo, im_hi, im_lo}
+constexpr int kRec = 8192;     // one A'' K-record: 128 rows x 16 fp16 x {hi, lo}
 constexpr int kImg = 4096;     // one 128 x 16 fp16 image inside a record
-constexpr int kStage = 32768;  // one pipeline stage: up to two consecutive K-records
+constexpr int kStage = 32768;  // one pipeline stage: up to four consecutive K-records
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -280,6 +280,36 @@ __device__ __forceinline__ void mom_chunk(const uint32_t (&vr)[16], const uint32
   }
 }
 
+// interleaved (re, im) accumulator columns: 16 time columns per 32 TMEM columns
+template <int NF>
+__device__ __forceinline__ void epi_chunk_i(const uint32_t (&v)[32], const float* wt, float2 (&part)[NF / 2]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float re = __uint_as_float(v[2 * j]), im = __uint_as_float(v[2 * j + 1]);
+    const float mag = sqrt_fast(fmaf(re, re, im * im));
+    const float4* w4 = reinterpret_cast<const float4*>(wt + j * NF);
+#pragma unroll
+    for (int m4 = 0; m4 < NF / 4; ++m4) {
+      const float4 w = w4[m4];
+      part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mag, part[2 * m4 + 0]);
+      part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mag, part[2 * m4 + 1]);
+    }
+  }
+}
+template <int J0>
+__device__ __forceinline__ void mom_chunk_i(const uint32_t (&v)[32], float (&S)[4]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float re = __uint_as_float(v[2 * j]), im = __uint_as_float(v[2 * j + 1]);
+    const float mag = sqrt_fast(fmaf(re, re, im * im));
+    const float u = ((float)(J0 + j) - 15.5f) * 0.0625f;
+    S[0] += mag;
+    S[1] = fmaf(mag, u, S[1]);
+    S[2] = fmaf(mag, u * u, S[2]);
+    S[3] = fmaf(mag, u * u * u, S[3]);
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // KY: one CTA per (signal, tile): max |Y''| over the K' x Nt tile -> s_Y (power of
 // two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y - hi) into the
@@ -317,19 +347,28 @@ __global__ void __launch_bounds__(256) k_ky(KYParams p) {
   E = max(E, -100);
   const float s = __uint_as_float((uint32_t)(13 - E + 127) << 23);
   if (threadIdx.x == 0) p.ys[(int64_t)b * p.ys_stride + tile] = __uint_as_float((uint32_t)(E - 13 + 127) << 23);
-  __half* hi = p.y16 + (int64_t)b * p.y16_stride + t0;
-  __half* lo = hi + (int64_t)p.K16 * p.L;
-  const int nh = p.Nt / 2;
-  for (int i = threadIdx.x; i < p.K16 * nh; i += 256) {
-    const int k = i / nh, c = 2 * (i % nh);
-    float2 v = make_float2(0.f, 0.f);
-    if (k < p.K2) v = __ldg(reinterpret_cast<const float2*>(Y + (int64_t)k * p.L + c));
-    v.x *= s;
-    v.y *= s;
-    const __half2 h = __floats2half2_rn(v.x, v.y);
-    const float2 hf = __half22float2(h);
-    *reinterpret_cast<__half2*>(hi + (int64_t)k * p.L + c) = h;
-    *reinterpret_cast<__half2*>(lo + (int64_t)k * p.L + c) = __floats2half2_rn(v.x - hf.x, v.y - hf.y);
+  // planes [hi | lo][K16][2L]: row 2l = (Yr, Yi) per time column, row 2l+1 = (-Yi, Yr)
+  // (the 2x2 real block of Y2[l] along N: D[m][2t] = Re Z, D[m][2t+1] = Im Z)
+  __half* hi = p.y16 + (int64_t)b * p.y16_stride + 2 * t0;
+  __half* lo = hi + (int64_t)p.K16 * 2 * p.L;
+  const int64_t rs = 2 * (int64_t)p.L;  // plane row stride
+  for (int i = threadIdx.x; i < (p.K16 / 2) * p.Nt; i += 256) {
+    const int l = i / p.Nt, c = i % p.Nt;
+    float yr = 0.f, yi = 0.f;
+    if (2 * l < p.K2) {
+      yr = __ldg(Y + (int64_t)(2 * l) * p.L + c) * s;
+      yi = __ldg(Y + (int64_t)(2 * l + 1) * p.L + c) * s;
+    }
+    const __half2 h0 = __floats2half2_rn(yr, yi);   // row 2l
+    const float2 f0 = __half22float2(h0);
+    const __half2 l0 = __floats2half2_rn(yr - f0.x, yi - f0.y);
+    const __half2 h1 = __floats2half2_rn(-yi, yr);  // row 2l+1 (negation is exact)
+    const float2 f1 = __half22float2(h1);
+    const __half2 l1 = __floats2half2_rn(-yi - f1.x, yr - f1.y);
+    *reinterpret_cast<__half2*>(hi + (2 * l) * rs + 2 * c) = h0;
+    *reinterpret_cast<__half2*>(lo + (2 * l) * rs + 2 * c) = l0;
+    *reinterpret_cast<__half2*>(hi + (2 * l + 1) * rs + 2 * c) = h1;
+    *reinterpret_cast<__half2*>(lo + (2 * l + 1) * rs + 2 * c) = l1;
   }
 }
 
@@ -367,11 +406,11 @@ constexpr int kProdWarp = 8, kMmaWarp = 9, kBWarp = 10;
 struct SmemLayout {
   uint32_t bhi[2], blo[2], ast, wt, bars, total;
 };
-__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int NF) {
+__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int NF, int pool_mode) {
   SmemLayout l{};
   auto up = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
   uint32_t o = 0;
-  const uint32_t bsz = (uint32_t)(K16 * Nt * 2);  // one fp16 K16 x Nt image
+  const uint32_t bsz = (uint32_t)(K16 * 2 * Nt * 2);  // one fp16 K16 x 2Nt image (complex along N)
   for (int i = 0; i < 2; ++i) {
     if (i < NBB) {
       l.bhi[i] = o;
@@ -385,8 +424,8 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int 
   }
   l.ast = o;
   o += (uint32_t)S * kStage;
-  l.wt = o;  // [2][Nt][NF]
-  o += (uint32_t)(2 * Nt * NF * 4);
+  l.wt = o;  // [2][Nt][NF] taps, or [2][Nt / 32][4][NF] moment coefficients
+  o += (uint32_t)(2 * Nt * (pool_mode ? NF / 8 : NF) * 4);
   l.bars = up(o, 8);
   o = l.bars + 8 * (4 + 4 + 8 + 2 * S) + 16;
   l.total = o + 1024;  // + alignment slack of the dynamic smem base
@@ -400,7 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  const SmemLayout lay = smem_layout(p.K16, p.Nt, p.NBB, p.S, NF);
+  const SmemLayout lay = smem_layout(p.K16, p.Nt, p.NBB, p.S, NF, p.pool_mode);
+  const int wfl = p.Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
   uint8_t* Ast = base + lay.ast;
   float* Wt = reinterpret_cast<float*>(base + lay.wt);  // [2][Nt][NF]
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + lay.bars);
@@ -443,36 +483,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int units = p.nsig * p.nsel * p.n_mpart;
-  const int nst = (p.nkc + 1) / 2;  // A'' stages (<= 2 records of 16 K-columns) per M-block
+  const int nst = (p.nkc + 3) / 4;  // A'' stages (<= 4 records of 16 K-columns) per M-block
   // the CTA's tile sequence: unit u = blockIdx.x + i * gridDim.x, tile 0..tpu-1
   const int my_units = (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const int my_tiles = my_units * p.tpu;
 
   if (warp == kBWarp) {
     // ===================== B producer: fp16 hi / lo tile + taps =====================
-    if (lane == 0) {
-      const uint32_t btx = (uint32_t)(2 * p.K16 * p.Nt * 2);
-      const int wcol = p.pool_mode ? NF / 8 : NF;  // table floats per time column
-      const uint32_t wbytes = (uint32_t)(p.Nt * wcol * 4);
-      for (int gt = 0; gt < my_tiles; ++gt) {
-        const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
-        int chunk = (u / p.n_mpart) % p.nsel;
-        if (p.chunk_sel) chunk = p.chunk_sel[chunk];
-        const int b = u / (p.n_mpart * p.nsel);
-        const int t0 = (chunk * p.tpu + gt % p.tpu) * p.Nt;
-        const int wi = gt & 1, bi = gt % p.NBB;
+    // one copy per lane (copies issued by one thread complete one after another):
+    // lane 0 the taps, lanes 1.. the TMA boxes (planes x 64-column groups x row boxes)
+    const int ncg = 2 * p.Nt / 64, nboxes = 2 * ncg * p.nbr;  // 2Nt columns: complex block along N
+    const uint32_t btx = (uint32_t)(2 * p.K16 * 2 * p.Nt * 2);
+    const int wcol = p.pool_mode ? NF / 8 : NF;  // table floats per time column
+    const uint32_t wbytes = (uint32_t)(p.Nt * wcol * 4);
+    for (int gt = 0; gt < my_tiles; ++gt) {
+      const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
+      int chunk = (u / p.n_mpart) % p.nsel;
+      if (p.chunk_sel) chunk = p.chunk_sel[chunk];
+      const int b = u / (p.n_mpart * p.nsel);
+      const int t0 = (chunk * p.tpu + gt % p.tpu) * p.Nt;
+      const int wi = gt & 1, bi = gt % p.NBB;
+      if (lane == 0) {
         mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
         mbar_expect_tx(w_full + wi, wbytes);
-        bulk_load(Wt + wi * p.Nt * NF, p.wtab + (size_t)t0 * wcol, wbytes, w_full + wi);
+        bulk_load(Wt + wi * wfl, p.wtab + (size_t)t0 * wcol, wbytes, w_full + wi);
         mbar_wait(b_empty + bi, (uint32_t)((gt / p.NBB) + 1) & 1u);
         mbar_expect_tx(b_full + bi, btx);
-        for (int h = 0; h < 2; ++h) {
-          uint8_t* dst = base + (h ? lay.blo[bi] : lay.bhi[bi]);
-          for (int cg = 0; cg < p.Nt / 64; ++cg)
-            for (int rb = 0; rb < p.nbr; ++rb)
-              tma_load_4d(dst + cg * (p.K16 * 128) + rb * (p.BRk * 128), &tmB, b_full + bi, t0 + cg * 64,
-                          rb * p.BRk, h, b);
-        }
+      }
+      __syncwarp();
+      for (int i = lane - 1; i >= 0 && i < nboxes; i += 31) {
+        const int h = i / (ncg * p.nbr), cg = (i / p.nbr) % ncg, rb = i % p.nbr;
+        uint8_t* dst = base + (h ? lay.blo[bi] : lay.bhi[bi]);
+        tma_load_4d(dst + cg * (p.K16 * 128) + rb * (p.BRk * 128), &tmB, b_full + bi, 2 * t0 + cg * 64, rb * p.BRk,
+                    h, b);
       }
     }
   } else if (warp == kProdWarp) {
@@ -491,9 +534,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int st = 0; st < nst; ++st) {
             if ((int)s == lane) {
               mbar_wait(a_empty + s, ph ^ 1);
-              const uint32_t bytes = (uint32_t)(min(2, p.nkc - 2 * st) * kRec);
+              const uint32_t bytes = (uint32_t)(min(4, p.nkc - 4 * st) * kRec);
               mbar_expect_tx(a_full + s, bytes);
-              bulk_load(Ast + s * kStage, arec + (size_t)(2 * st) * (kRec / 2), bytes, a_full + s);
+              bulk_load(Ast + s * kStage, arec + (size_t)(4 * st) * (kRec / 2), bytes, a_full + s);
             }
             ++j;
             if (++s == (uint32_t)p.S) {
@@ -509,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t s = 0, ph = 0, cnt = 0;
     long long w_b = 0, w_acc = 0, w_a = 0;
     const long long t_start = clock64();
-    const uint32_t idesc = idesc_f16(p.Nt);
+    const uint32_t idesc = idesc_f16(2 * p.Nt);  // N = 2 Nt: (re, im) interleaved per time column
     const uint32_t colstride = (uint32_t)(p.K16 * 128);
     const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 256, kLayoutSW32);
     for (int gt = 0; gt < my_tiles; ++gt) {
@@ -522,26 +565,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ab = cnt % (uint32_t)p.nbuf, use = cnt / (uint32_t)p.nbuf;
         mbar_wait_t(acc_empty + ab, (use + 1) & 1, w_acc);
         tc_fence_after();
-        const uint32_t d_re = tmem_base + ab * 2u * (uint32_t)p.Nt;
-        const uint32_t d_im = d_re + (uint32_t)p.Nt;
+        const uint32_t dd = tmem_base + ab * 2u * (uint32_t)p.Nt;
         for (int st = 0; st < nst; ++st) {
           mbar_wait_t(a_full + s, ph, w_a);
           tc_fence_after();
           if (elect_one()) {
             const uint64_t dst = dA0 + (uint64_t)((s * kStage) >> 4);
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int kc = 2 * st + r;
+            for (int r = 0; r < 4; ++r) {
+              const int kc = 4 * st + r;
               if (kc < p.nkc) {
                 const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
                 const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
                 const uint32_t acc0 = kc > 0 ? 1u : 0u;
-                mma_f16(d_re, a + (0 * kImg >> 4), dBh + yo, idesc, acc0);
-                mma_f16(d_re, a + (0 * kImg >> 4), dBl + yo, idesc, 1u);
-                mma_f16(d_re, a + (1 * kImg >> 4), dBh + yo, idesc, 1u);
-                mma_f16(d_im, a + (2 * kImg >> 4), dBh + yo, idesc, acc0);
-                mma_f16(d_im, a + (2 * kImg >> 4), dBl + yo, idesc, 1u);
-                mma_f16(d_im, a + (3 * kImg >> 4), dBh + yo, idesc, 1u);
+                mma_f16(dd, a, dBh + yo, idesc, acc0);                        // A_hi B_hi
+                mma_f16(dd, a, dBl + yo, idesc, 1u);                          // A_hi B_lo
+                mma_f16(dd, a + (uint64_t)(kImg >> 4), dBh + yo, idesc, 1u);  // A_lo B_hi
               }
             }
             mma_commit(a_empty + s);
@@ -589,14 +628,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int wi = gt & 1;
       mbar_wait_t(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
       const float inv = __ldg(p.ys + (int64_t)b * p.ys_stride + chunk * p.tpu + tile);
-      const float* wt = Wt + wi * p.Nt * NF + cbeg * NF;
+      const float* wt = Wt + wi * wfl + cbeg * NF;
 #pragma unroll 1
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
         const uint32_t ab = cnt % (uint32_t)p.nbuf;
         mbar_wait_t(acc_full + ab, (cnt / (uint32_t)p.nbuf) & 1u, e_acc);
         const long long tm0 = clock64();
         tc_fence_after();
-        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ab * 2u * (uint32_t)p.Nt + (uint32_t)cbeg;
+        // accumulator columns 2t / 2t+1 = Re / Im of time column t; this set's time
+        // columns [cbeg, cbeg + Nt/2) start at TMEM column 2 cbeg
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ab * 2u * (uint32_t)p.Nt + 2u * (uint32_t)cbeg;
         float2 part[NF / 2];
 #pragma unroll
         for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
@@ -604,31 +645,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.pool_mode == 1) {
           // moment form: per 32-column block S_k = sum_j |Z_j| u_j^k (k <= 3, u_j
           // compile-time), then part += G_k S_k with the block's 4 x NF coefficients
-          const float* gco = Wt + wi * p.Nt * NF + (cbeg / 32) * 4 * NF;
+          const float* gco = Wt + wi * wfl + (cbeg / 32) * 4 * NF;
           for (int c0 = 0; c0 < half; c0 += 32) {
             float S[4] = {0.f, 0.f, 0.f, 0.f};
             {
-              uint32_t vr[16], vi[16];
-              tmem_ld16(tb + c0, vr);
-              tmem_ld16(tb + p.Nt + c0, vi);
+              uint32_t v[32];
+              tmem_ld32(tb + 2 * c0, v);
               tmem_wait_ld();
-              reg_fence16(vr);
-              reg_fence16(vi);
-              mom_chunk<0>(vr, vi, S);
+              reg_fence(v);
+              mom_chunk_i<0>(v, S);
             }
             {
-              uint32_t vr[16], vi[16];
-              tmem_ld16(tb + c0 + 16, vr);
-              tmem_ld16(tb + p.Nt + c0 + 16, vi);
+              uint32_t v[32];
+              tmem_ld32(tb + 2 * c0 + 32, v);
               tmem_wait_ld();
-              reg_fence16(vr);
-              reg_fence16(vi);
+              reg_fence(v);
               if (c0 + 32 >= half) {  // last read of this buffer: hand it back to the MMA
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acc_empty + ab);
               }
-              mom_chunk<16>(vr, vi, S);
+              mom_chunk_i<16>(v, S);
             }
             const float4* g4 = reinterpret_cast<const float4*>(gco + (c0 / 32) * 4 * NF);
 #pragma unroll
@@ -642,18 +679,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           for (int c0 = 0; c0 < half; c0 += 16) {
-            uint32_t vr[16], vi[16];
-            tmem_ld16(tb + c0, vr);
-            tmem_ld16(tb + p.Nt + c0, vi);
+            uint32_t v[32];
+            tmem_ld32(tb + 2 * c0, v);
             tmem_wait_ld();
-            reg_fence16(vr);
-            reg_fence16(vi);
+            reg_fence(v);
             if (c0 + 16 >= half) {  // last read of this buffer: hand it back to the MMA
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(acc_empty + ab);
             }
-            epi_chunk<NF>(vr, vi, wt + c0 * NF, part);
+            epi_chunk_i<NF>(v, wt + c0 * NF, part);
           }
         }
         e_math += clock64() - tm0;
@@ -742,13 +777,13 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, void* base, int rank, const 
 
 int nf_of(int nframes) { return nframes <= 8 ? 8 : nframes <= 16 ? 16 : 32; }
 size_t tc_smem(const AlphaKD& d, int nf) {
-  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, d.tc_S, nf).total;
+  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, d.tc_S, nf, d.pool_mode).total;
 }
 }  // namespace
 
 // choose the per-alpha tensor-core tiling (called by build_plan): the first of
-// (Nt, B buffers, min stages) = (128, 2, 3), (128, 1, 3), (128, 2, 2), (128, 1, 2),
-// (64, 2, 3), (64, 1, 2) that fits, then as many A'' stages as fit (<= 6)
+// (Nt, B buffers, min stages) = (128, 2, 3), (128, 2, 2), (128, 1, 3), (128, 1, 2),
+// (64, 2, 2), (64, 1, 2), (32, 1, 2) that fits, then as many A'' stages as fit (<= 6)
 void plan_tc(Plan& P) {
   const int NF = nf_of(P.n_frames);
   const size_t budget = 227 * 1024;
@@ -765,7 +800,11 @@ void plan_tc(Plan& P) {
     d.tc_nbr = (d.tc_K16 + 255) / 256;
     d.tc_BRk = (d.tc_K16 / d.tc_nbr + 7) / 8 * 8;
     bool ok = false;
-    const int cand[6][3] = {{128, 2, 3}, {128, 1, 3}, {128, 2, 2}, {128, 1, 2}, {64, 2, 3}, {64, 1, 2}};
+    // Nt = 128 (MMA N = 256, the efficient shape) first; two B buffers when they fit
+    // with >= min_s2 A stages (JTFS_TC_MINS2: measurement-only override, default 2)
+    const char* e_m2 = std::getenv("JTFS_TC_MINS2");
+    const int min_s2 = e_m2 ? std::max(2, std::atoi(e_m2)) : 2;
+    const int cand[7][3] = {{128, 2, 3}, {128, 2, min_s2}, {128, 1, 3}, {128, 1, 2}, {64, 2, 2}, {64, 1, 2}, {32, 1, 2}};
     for (const auto& c : cand) {
       if (c[0] > nt_max || c[0] > d.L) continue;
       d.tc_Nt = c[0];
@@ -788,11 +827,14 @@ void plan_tc(Plan& P) {
       d.nchunks = d.L / d.chunk;
       d.tc_tpu = d.chunk / d.tc_Nt;
     }
-    if (!ok || d.L < 64 || d.chunk % d.tc_Nt || d.tc_nbr * d.tc_BRk < d.tc_K16) P.kd_impl = 0;
+    // the moment-form epilogue works on 32-column blocks of each set's Nt / 2 columns
+    if (!ok || d.L < 64 || d.chunk % d.tc_Nt || d.tc_nbr * d.tc_BRk < d.tc_K16 || (d.pool_mode && d.tc_Nt < 64))
+      P.kd_impl = 0;
   }
 }
 
 cudaError_t tc_setup_device(Plan& P) {
+  if (P.kd_impl != 1) return cudaSuccess;
   const int NF = nf_of(P.n_frames);
   size_t mx = 0;
   for (auto& d : P.kd) mx = std::max(mx, tc_smem(d, NF));
@@ -836,8 +878,8 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
       ++launches;
     }
     CUtensorMap tmB;
-    cuuint64_t dims[4] = {(cuuint64_t)d.L, (cuuint64_t)d.tc_K16, 2, (cuuint64_t)nsig};
-    cuuint64_t strides[3] = {(cuuint64_t)d.L * 2, (cuuint64_t)d.tc_K16 * d.L * 2, (cuuint64_t)P.y16_total * 2};
+    cuuint64_t dims[4] = {(cuuint64_t)(2 * d.L), (cuuint64_t)d.tc_K16, 2, (cuuint64_t)nsig};
+    cuuint64_t strides[3] = {(cuuint64_t)d.L * 4, (cuuint64_t)d.tc_K16 * d.L * 4, (cuuint64_t)P.y16_total * 2};
     cuuint32_t box[4] = {64, (cuuint32_t)d.tc_BRk, 1, 1};
     if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 4, dims, strides, box,
                 CU_TENSOR_MAP_SWIZZLE_128B)) {
@@ -851,7 +893,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.BRk = d.tc_BRk;
     p.nbr = d.tc_nbr;
     p.NBB = d.tc_NBB;
-    p.nbuf = 512 / (2 * d.tc_Nt);
+    p.nbuf = std::min(4, 512 / (2 * d.tc_Nt));  // accumulator buffers of 2 Nt columns (4 barrier pairs)
     p.S = d.tc_S;
     p.tpu = d.tc_tpu;
     p.nchunks = d.nchunks;

@@ -433,15 +433,14 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       }
     }
   }
-  // A''_alpha for the tensor cores (kernels_tc.cu): for complex row m and Y'' row
-  // k' = 2l + c (c = 0: Re Y2[l], c = 1: Im Y2[l]),
-  //   A_re''[m][2l] =  Re A[m][l],  A_re''[m][2l+1] = -Im A[m][l]   (Re Z = Ar Yr - Ai Yi)
-  //   A_im''[m][2l] =  Im A[m][l],  A_im''[m][2l+1] =  Re A[m][l]   (Im Z = Ai Yr + Ar Yi)
+  // A''_alpha for the tensor cores (kernels_tc.cu, complex along N): for complex row m
+  // and K' index k' = 2l + c,  A''[m][2l] = Re A[m][l],  A''[m][2l+1] = Im A[m][l];
+  // with B'' the 2x2 real block of Y2[l] along N (KY), D[m][2t] = Re Z, D[m][2t+1] = Im Z.
   // Each row is scaled by a power of two s_m (max |entry| * s_m in [2^13, 2^14)) and
   // split into fp16 hi = rn(a s_m), lo = rn(a s_m - hi); Ainv holds 1 / s_m.
   // Stored pre-tiled for cp.async.bulk: per (128-row M-block, 16-wide K chunk) one
-  // 16 KiB record [re_hi | re_lo | im_hi | im_lo], each a 4 KiB UMMA K-major
-  // SWIZZLE_32B image (8-row x 32 B atoms, 16 B chunk index ^= row bit 2).
+  // 8 KiB record [hi | lo], each a 4 KiB UMMA K-major SWIZZLE_32B image (8-row x 32 B
+  // atoms, 16 B chunk index ^= row bit 2).
   P.A16.clear();
   P.Ainv.clear();
   for (auto& d : P.kd) {
@@ -451,7 +450,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     d.tc_a16_off = (int64_t)P.A16.size();
     d.tc_ainv_off = (int64_t)P.Ainv.size();
     const size_t base = P.A16.size();
-    P.A16.resize(base + (size_t)nblk * nkc * 8192, 0);
+    P.A16.resize(base + (size_t)nblk * nkc * 4096, 0);
     P.Ainv.resize(P.Ainv.size() + P.Mpad, 1.f);
     std::vector<int> row_f(P.Mpad, -1), row_i(P.Mpad, 0);
     for (size_t fi = 0; fi < P.fr.size(); ++fi)
@@ -463,7 +462,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       const int mb = m / 128, r = m % 128, kc = col / 16, kk = col % 16;
       const uint32_t o = (uint32_t)((r / 8) * 256 + (r % 8) * 32 + kk * 2);
       const uint32_t sw = o ^ (((o >> 7) & 1u) << 4);
-      P.A16[base + ((size_t)mb * nkc + kc) * 8192 + (size_t)img * 2048 + sw / 2] = h;
+      P.A16[base + ((size_t)mb * nkc + kc) * 4096 + (size_t)img * 2048 + sw / 2] = h;
     };
     std::vector<std::complex<double>> arow(d.K);
     for (int m = 0; m < P.Mpad; ++m) {
@@ -481,15 +480,12 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       const double s = std::ldexp(1.0, 13 - E);  // amax * s in [2^13, 2^14)
       P.Ainv[d.tc_ainv_off + m] = (float)std::ldexp(1.0, E - 13);
       for (int lam = 0; lam < d.K; ++lam) {
-        const double ar = arow[lam].real() * s, ai = arow[lam].imag() * s;
-        const double v[4] = {ar, -ai, ai, ar};  // re: (2l, 2l+1), im: (2l, 2l+1)
-        for (int t = 0; t < 4; ++t) {
-          const int img = (t / 2) * 2;            // 0: re, 2: im  (+1 for lo)
-          const int col = 2 * lam + (t % 2);
-          const uint16_t h = half_rn(v[t]);
-          const uint16_t l = half_rn(v[t] - half_to_double(h));
-          put(m, img, col, h);
-          put(m, img + 1, col, l);
+        const double v[2] = {arow[lam].real() * s, arow[lam].imag() * s};
+        for (int c = 0; c < 2; ++c) {
+          const uint16_t h = half_rn(v[c]);
+          const uint16_t l = half_rn(v[c] - half_to_double(h));
+          put(m, 0, 2 * lam + c, h);
+          put(m, 1, 2 * lam + c, l);
         }
       }
     }
@@ -521,7 +517,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     for (auto& d : P.kd) {
       const int K16 = (2 * d.K + 15) / 16 * 16;
       d.y16_off = P.y16_total;
-      P.y16_total += (int64_t)2 * K16 * d.L;
+      P.y16_total += (int64_t)2 * K16 * 2 * d.L;  // [hi | lo][K16][2L]: complex block along N
       d.ys_off = P.ys_total;
       P.ys_total += std::max(1, d.L / 64);
       d.wtab_off = (int64_t)P.wtab.size();
