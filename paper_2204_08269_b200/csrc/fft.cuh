@@ -193,6 +193,105 @@ __device__ __forceinline__ void fft_smem(CT* s, const CT* Ws) {
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Fused variant: the first pass takes its inputs straight from global memory
+// (load(g, e)) and the last pass writes straight to global memory (store(g, e, v)),
+// which saves one shared-memory round trip (and one barrier) at each end.  COLMAJOR
+// maps consecutive threads to consecutive rows g (coalesced column gathers of the
+// four-step pass A); otherwise to consecutive elements of a row.
+// Preconditions: LOG2L >= 3; the shared per-pass twiddles are staged and visible
+// (the caller's barrier after stage_twiddles -- the first pass uses none).
+// ---------------------------------------------------------------------------------
+template <int LOG2L, int R, int G, int NT, int DIR, int LS, bool COLMAJOR, bool FROM_G, bool TO_G, class CT,
+          class LF, class SF>
+__device__ __forceinline__ void stockham_pass_x(CT* s, int log2Ns, const CT* Wp, const LF& load, const SF& store) {
+  constexpr int L = 1 << LOG2L;
+  constexpr int LR = L / R;
+  constexpr int NBF = G * LR;
+  constexpr int BPT = (NBF + NT - 1) / NT;
+  const int Ns = 1 << log2Ns;
+  CT v[BPT][R];
+  int gg[BPT], e0s[BPT];
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    const int bf = threadIdx.x + i * NT;
+    gg[i] = -1;
+    if ((NBF % NT == 0) || bf < NBF) {
+      const int g = COLMAJOR ? bf % G : bf / LR, j = COLMAJOR ? bf / G : bf % LR;
+      if constexpr (FROM_G) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i][r] = load(g, j + r * LR);
+      } else {
+        const CT* row = s + g * LS;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i][r] = row[padx(j + r * LR)];
+      }
+      gg[i] = g;
+      e0s[i] = j;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    if (gg[i] >= 0) {
+      const int j = e0s[i];
+      const int k = j & (Ns - 1);
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const CT w = Wp[(r - 1) * Ns + k];
+          v[i][r] = cmul(v[i][r], DIR < 0 ? w : CxT<CT>::make(w.x, -w.y));
+        }
+      }
+      dft_reg<R, DIR>(v[i]);
+      e0s[i] = (j - k) * R + k;
+    }
+  }
+  if constexpr (!FROM_G && !TO_G) __syncthreads();  // in place: all reads before any write
+#pragma unroll
+  for (int i = 0; i < BPT; ++i) {
+    if (gg[i] >= 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (TO_G) store(gg[i], e0s[i] + r * Ns, v[i][r]);
+        else s[gg[i] * LS + padx(e0s[i] + r * Ns)] = v[i][r];
+      }
+    }
+  }
+  if constexpr (!TO_G) __syncthreads();
+}
+
+// Full fused FFT of G rows: inputs from load (FUSE_IN) or from smem (the caller has
+// filled it and synchronised), outputs to store (FUSE_OUT) or left in smem in
+// natural order.  Pass order: radix-2^REM at Ns = 1 (if LOG2L % 3), then radix-8.
+template <int LOG2L, int G, int NT, int DIR, int LS, bool COLMAJOR, bool FUSE_IN, bool FUSE_OUT, class CT,
+          class LF, class SF>
+__device__ __forceinline__ void fft_fused(CT* s, const CT* Ws, const LF& load, const SF& store) {
+  static_assert(LOG2L >= 3, "fused FFT needs at least one radix-8 pass");
+  constexpr int REM = LOG2L % 3;
+  constexpr int NP8 = LOG2L / 3;
+  int log2Ns = 0, off = 0;
+  if constexpr (REM != 0) {
+    stockham_pass_x<LOG2L, (1 << REM), G, NT, DIR, LS, COLMAJOR, FUSE_IN, false>(s, 0, Ws, load, store);
+    log2Ns = REM;
+  }
+#pragma unroll
+  for (int p = 0; p < NP8; ++p) {
+    const bool first = (REM == 0 && p == 0), last = (p == NP8 - 1);
+    const CT* Wp = Ws + off;
+    if (first && last) {
+      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, FUSE_IN, FUSE_OUT>(s, log2Ns, Wp, load, store);
+    } else if (first) {
+      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, FUSE_IN, false>(s, log2Ns, Wp, load, store);
+    } else if (last) {
+      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, false, FUSE_OUT>(s, log2Ns, Wp, load, store);
+    } else {
+      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, false, false>(s, log2Ns, Wp, load, store);
+    }
+    if (log2Ns > 0) off += 7 << log2Ns;
+    log2Ns += 3;
+  }
+}
+
 // offset of the length-L table inside the concatenated per-length twiddle tables
 // (lengths 2, 4, ..., 2^k stored back to back: offset(L) = L - 2)
 __host__ __device__ constexpr int tw_offset(int log2L) { return (1 << log2L) - 2; }

@@ -129,7 +129,16 @@ __global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typena
   CT* Ws = smem + G * LS;
   stage_twiddles<LOG2L, NT>(Ws, Wtab + tw_offset(LOG2L));
   const int rho0 = blockIdx.x * G;
-  {
+  if constexpr (LOG2L >= 3) {
+    // first pass straight from global memory, last pass straight to global memory
+    auto ld = [&](int g, int e) -> CT {
+      return (rho0 + g < nrows) ? prob.load(rho0 + g, e) : CxT<CT>::make(0, 0);
+    };
+    auto st = [&](int g, int e, CT v) {
+      if (rho0 + g < nrows) prob.store(rho0 + g, e, v);
+    };
+    fft_fused<LOG2L, G, NT, DIR, LS, false, true, true>(smem, Ws, ld, st);
+  } else {
     CT v[EPT];  // all global loads of this thread in flight together
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -141,13 +150,13 @@ __global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typena
       const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
       smem[g * LS + padx(e)] = v[i];
     }
-  }
-  __syncthreads();
-  fft_smem<LOG2L, G, NT, DIR, LS>(smem, Ws);
+    __syncthreads();
+    fft_smem<LOG2L, G, NT, DIR, LS>(smem, Ws);
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
-    if (rho0 + g < nrows) prob.store(rho0 + g, e, smem[g * LS + padx(e)]);
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      if (rho0 + g < nrows) prob.store(rho0 + g, e, smem[g * LS + padx(e)]);
+    }
   }
 }
 
@@ -162,7 +171,41 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
   float2* Ws = smem + G * LS;
   stage_twiddles<LOG2L, NT>(Ws, Wtab + tw_offset(LOG2L));
   const int rho0 = blockIdx.x * G;
-  {
+  auto modulus = [&]() {
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      const int rho = min(rho0 + g, nrows - 1);
+      const float sc = prob.rows[rho % prob.nrows].scale;
+      const float2 v = smem[g * LS + padx(e)];
+      const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc;
+      smem[g * LS + padx(e)] = make_float2(u, 0.f);
+      if (u1dbg && rho0 + g < nrows) {
+        const int b = (rho0 + g) / prob.nrows, r = (rho0 + g) % prob.nrows;
+        u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = u;
+      }
+    }
+    __syncthreads();
+  };
+  auto st = [&](int g, int e, float2 v) {
+    const int rho = rho0 + g;
+    if (rho < nrows) {
+      const int b = rho / prob.nrows, r = rho % prob.nrows;
+      u1hat[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = v;
+    }
+  };
+  if constexpr (LOG2L >= 3) {
+    // IDFT: first pass straight from the band fold (global), result left in smem;
+    // modulus in smem; DFT of U1: last pass straight to U1hat (global)
+    auto ld = [&](int g, int e) -> float2 {
+      return (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+    };
+    auto none = [&](int, int, float2) {};
+    fft_fused<LOG2L, G, NT, +1, LS, false, true, false>(smem, Ws, ld, none);
+    modulus();
+    auto nold = [&](int, int) -> float2 { return make_float2(0.f, 0.f); };
+    fft_fused<LOG2L, G, NT, -1, LS, false, false, true>(smem, Ws, nold, st);
+  } else {
     float2 v[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -174,31 +217,14 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
       const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
       smem[g * LS + padx(e)] = v[i];
     }
-  }
-  __syncthreads();
-  fft_smem<LOG2L, G, NT, +1, LS>(smem, Ws);
+    __syncthreads();
+    fft_smem<LOG2L, G, NT, +1, LS>(smem, Ws);
+    modulus();
+    fft_smem<LOG2L, G, NT, -1, LS>(smem, Ws);
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
-    const int rho = min(rho0 + g, nrows - 1);
-    const float sc = prob.rows[rho % prob.nrows].scale;
-    const float2 v = smem[g * LS + padx(e)];
-    const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc;
-    smem[g * LS + padx(e)] = make_float2(u, 0.f);
-    if (u1dbg && rho0 + g < nrows) {
-      const int b = (rho0 + g) / prob.nrows, r = (rho0 + g) % prob.nrows;
-      u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = u;
-    }
-  }
-  __syncthreads();
-  fft_smem<LOG2L, G, NT, -1, LS>(smem, Ws);
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
-    const int rho = rho0 + g;
-    if (rho < nrows) {
-      const int b = rho / prob.nrows, r = rho % prob.nrows;
-      u1hat[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = smem[g * LS + padx(e)];
+    for (int i = 0; i < EPT; ++i) {
+      const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
+      st(g, e, smem[g * LS + padx(e)]);
     }
   }
 }
@@ -230,37 +256,16 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
   constexpr int CPB = Lb / G;  // column groups per big row
   const int rho = blockIdx.x / CPB;
   const int nb0 = (blockIdx.x % CPB) * G;
-  {
-    CT v[EPT];
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int idx = threadIdx.x + i * NT, g = idx % G, na = idx / G;
-      v[i] = prob.load(rho, na * Lb + nb0 + g);
-    }
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int idx = threadIdx.x + i * NT, g = idx % G, na = idx / G;
-      smem[g * LS + padx(na)] = v[i];
-    }
-  }
-  __syncthreads();
-  fft_smem<LOG2A, G, NT, DIR, LS>(smem, Ws);
   CT* out = tmp + (int64_t)rho * L;
-  {
-    CT w[EPT];
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int idx = threadIdx.x + i * NT, g = idx % G, ka = idx / G;
-      const int x = ka * (nb0 + g);
-      const CT t = cmul(Wlo[x & (La - 1)], Whi[x >> LOG2A]);
-      w[i] = DIR < 0 ? t : CxT<CT>::make(t.x, -t.y);
-    }
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int idx = threadIdx.x + i * NT, g = idx % G, ka = idx / G;
-      out[ka * Lb + nb0 + g] = cmul(smem[g * LS + padx(ka)], w[i]);
-    }
-  }
+  // column g of this block = big-row column nb0 + g; consecutive threads take
+  // consecutive columns (coalesced gathers and scatters), first / last pass fused
+  auto ld = [&](int g, int na) -> CT { return prob.load(rho, na * Lb + nb0 + g); };
+  auto st = [&](int g, int ka, CT v) {
+    const int x = ka * (nb0 + g);
+    const CT t = cmul(Wlo[x & (La - 1)], Whi[x >> LOG2A]);
+    out[ka * Lb + nb0 + g] = cmul(v, DIR < 0 ? t : CxT<CT>::make(t.x, -t.y));
+  };
+  fft_fused<LOG2A, G, NT, DIR, LS, true, true, true>(smem, Ws, ld, st);
 }
 
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
@@ -277,21 +282,11 @@ __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __r
   const int rho = blockIdx.x / RPB;
   const int ka0 = (blockIdx.x % RPB) * G;
   const CT* in = tmp + (int64_t)rho * L;
-  {
-    CT v[EPT];
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int idx = threadIdx.x + i * NT, g = idx / Lb, e = idx % Lb;
-      v[i] = in[(ka0 + g) * Lb + e];
-    }
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int idx = threadIdx.x + i * NT, g = idx / Lb, e = idx % Lb;
-      smem[g * LS + padx(e)] = v[i];
-    }
-  }
-  __syncthreads();
-  fft_smem<LOG2B, G, NT, DIR, LS>(smem, Ws);
+  // rows (ka0 + g) of the intermediate are contiguous: first pass fused with the loads;
+  // results stay in smem for the transposed (coalesced) store below
+  auto ld = [&](int g, int e) -> CT { return in[(ka0 + g) * Lb + e]; };
+  auto none = [&](int, int, CT) {};
+  fft_fused<LOG2B, G, NT, DIR, LS, false, true, false>(smem, Ws, ld, none);
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int idx = threadIdx.x + i * NT, g = idx % G, kb = idx / G;
