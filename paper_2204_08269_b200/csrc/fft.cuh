@@ -264,14 +264,15 @@ __device__ __forceinline__ void stockham_pass_x(CT* s, int log2Ns, const CT* Wp,
 // filled it and synchronised), outputs to store (FUSE_OUT) or left in smem in
 // natural order.  Pass order: radix-2^REM at Ns = 1 (if LOG2L % 3), then radix-8.
 template <int LOG2L, int G, int NT, int DIR, int LS, bool COLMAJOR, bool FUSE_IN, bool FUSE_OUT, class CT,
-          class LF, class SF>
+          class LF, class SF, bool COL_FIRST = COLMAJOR>
 __device__ __forceinline__ void fft_fused(CT* s, const CT* Ws, const LF& load, const SF& store) {
+  // COL_FIRST: thread mapping of the first pass (the loads); COLMAJOR: of the others
   static_assert(LOG2L >= 3, "fused FFT needs at least one radix-8 pass");
   constexpr int REM = LOG2L % 3;
   constexpr int NP8 = LOG2L / 3;
   int log2Ns = 0, off = 0;
   if constexpr (REM != 0) {
-    stockham_pass_x<LOG2L, (1 << REM), G, NT, DIR, LS, COLMAJOR, FUSE_IN, false>(s, 0, Ws, load, store);
+    stockham_pass_x<LOG2L, (1 << REM), G, NT, DIR, LS, COL_FIRST, FUSE_IN, false>(s, 0, Ws, load, store);
     log2Ns = REM;
   }
 #pragma unroll
@@ -279,9 +280,9 @@ __device__ __forceinline__ void fft_fused(CT* s, const CT* Ws, const LF& load, c
     const bool first = (REM == 0 && p == 0), last = (p == NP8 - 1);
     const CT* Wp = Ws + off;
     if (first && last) {
-      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, FUSE_IN, FUSE_OUT>(s, log2Ns, Wp, load, store);
+      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COL_FIRST, FUSE_IN, FUSE_OUT>(s, log2Ns, Wp, load, store);
     } else if (first) {
-      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, FUSE_IN, false>(s, log2Ns, Wp, load, store);
+      stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COL_FIRST, FUSE_IN, false>(s, log2Ns, Wp, load, store);
     } else if (last) {
       stockham_pass_x<LOG2L, 8, G, NT, DIR, LS, COLMAJOR, false, FUSE_OUT>(s, log2Ns, Wp, load, store);
     } else {

@@ -282,16 +282,12 @@ __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __r
   const int rho = blockIdx.x / RPB;
   const int ka0 = (blockIdx.x % RPB) * G;
   const CT* in = tmp + (int64_t)rho * L;
-  // rows (ka0 + g) of the intermediate are contiguous: first pass fused with the loads;
-  // results stay in smem for the transposed (coalesced) store below
+  // rows (ka0 + g) of the intermediate are contiguous: the first pass (row-major
+  // threads) is fused with the loads; the last pass (column-major threads: consecutive
+  // ka, i.e. consecutive output bins ka + La kb) with the stores
   auto ld = [&](int g, int e) -> CT { return in[(ka0 + g) * Lb + e]; };
-  auto none = [&](int, int, CT) {};
-  fft_fused<LOG2B, G, NT, DIR, LS, false, true, false>(smem, Ws, ld, none);
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int idx = threadIdx.x + i * NT, g = idx % G, kb = idx / G;
-    prob.store(rho, ka0 + g + La * kb, smem[g * LS + padx(kb)]);
-  }
+  auto st = [&](int g, int kb, CT v) { prob.store(rho, ka0 + g + La * kb, v); };
+  fft_fused<LOG2B, G, NT, DIR, LS, true, true, true, CT, decltype(ld), decltype(st), false>(smem, Ws, ld, st);
 }
 
 // ---------------------------------------------------------------------------------
