@@ -437,3 +437,65 @@ def unpack_layout(s: Schedule):
 def pack(res: dict) -> np.ndarray:
     """O12: out_3D flattened row-major (reading R-O11/O12)."""
     return np.concatenate([res["S0"].ravel(), res["S1"].ravel(), res["S2"].ravel()])
+
+
+# ----------------------------------------------------------------------------
+# NEXT-4 (SURVEY §8(f)): scale-rate map export and mu-log compression
+# ----------------------------------------------------------------------------
+def u2_map_shape(s: Schedule, pi: int):
+    """(rows, cols) of u2_map for path pi (a SPIN or PSI_T_PHI_F path)."""
+    kind, _, a, b = s.paths[pi]
+    if kind == SPIN:
+        k = int(s.kf[b])
+    elif kind == PSI_T_PHI_F:
+        k = s.log2F if s.p.average_fr else 0
+    else:
+        raise ValueError("u2_map exists only for the psi_t paths (spinned, psi_t x phi_f)")
+    ka = s.k_alpha[a]
+    return -(-s.n1 // 2 ** k), -(-s.p.N // 2 ** ka)
+
+
+def u2_map(x: np.ndarray, p: Params, pi: int, s: Schedule | None = None) -> np.ndarray:
+    """Scale-rate visualisation of Fig. 1: |X * Psi_{alpha,beta,theta}|,
+    the joint wavelet modulus BEFORE the lowpass Phi (Eq. (3) without its last
+    convolution), on the whole time and log-frequency axes.
+
+    Readings (R21): the map is U2 of step O7 on its critical grid --
+    rows r' of the lambda axis decimated by 2^k (k = k_f(beta) in Eq. (3) mode,
+    log2 F for psi_t x phi_f, 0 in Eq. (4) mode), restricted to the rows over the
+    scalogram, r' 2^k < n1; columns n of the alpha grid (exponent k_alpha)
+    restricted to the unpadded signal, n in U(k_alpha) = [ceil(pad_left / 2^k_alpha),
+    + ceil(N / 2^k_alpha)).  Returns float64 (rows, cols)."""
+    s = s or schedule(p)
+    rows, cols = u2_map_shape(s, pi)
+    kind, theta, a, b = s.paths[pi]
+    x = np.asarray(x, dtype=np.float64)
+    _, _, _, _, Y2 = first_order(x, s)
+    G = _grid(dict(zip(s.adm[a], Y2[a])), Y2[a].shape[1], s, np.complex128)
+    if kind == SPIN:
+        fh, k = psi_fr_hat(b, theta, s), int(s.kf[b])
+    else:
+        fh, k = gauss_hat(s.sigma_F, s.N_fr, s.N_fr), (s.log2F if s.p.average_fr else 0)
+    U2 = np.abs(_ifft(_fft(G, axis=0) * fh[:, None], axis=0))[:: 2 ** k]   # O7, |X * Psi|
+    c0 = -(-s.pad_left // 2 ** s.k_alpha[a])
+    return U2[:rows, c0: c0 + cols]
+
+
+def mulog_mu(S2: np.ndarray) -> np.ndarray:
+    """Eq. (adalog:mu): mu(lambda_2) = (1/N) sum_n iint S x_n(lambda_2,
+    lambda, t) dt dlambda over a set of N examples; the integral over the sampled
+    (lambda, t) grid is the sum of the map.  S2: (B, P, lam_out, frames)."""
+    S2 = np.asarray(S2, dtype=np.float64)
+    return S2.sum(axis=(2, 3)).sum(axis=0) / S2.shape[0]
+
+
+def mulog(S2: np.ndarray, mu: np.ndarray, eps: float = 0.1) -> np.ndarray:
+    """Eq. (adalog): S~(lambda_2, lambda, t) = log(1 + S / (eps mu(lambda_2))),
+    eps = 0.1 per path.  Reading R22: applied to every second-order map
+    lambda_2 (the S2 paths); S0 / S1 are left as they are (the convnet
+    treats first order separately).  A path with mu = 0 (all-zero maps) maps to 0."""
+    S2 = np.asarray(S2, dtype=np.float64)
+    mu = np.asarray(mu, dtype=np.float64)
+    den = eps * mu[None, :, None, None]
+    safe = np.where(den > 0, den, 1.0)
+    return np.where(den > 0, np.log1p(S2 / safe), 0.0)

@@ -117,7 +117,8 @@ def brute_jtfs(x, prm):
 
     avg = prm.average_fr
     S2 = []
-    for kind, theta, a, b in s.paths:
+    U2maps = {}
+    for pi, (kind, theta, a, b) in enumerate(s.paths):
         if kind in (O.SPIN, O.PSI_T_PHI_F):
             G = np.zeros((Nfr, Y2[a].shape[1]), complex)
             for i, lam in enumerate(s.adm[a]):
@@ -128,6 +129,7 @@ def brute_jtfs(x, prm):
                 h, k = fr_taps("phi", 0, 0), (s.log2F if avg else 0)
             Z = circ_matrix(h) @ G                                     # conv along lambda
             U2 = np.abs(Z[[r * 2 ** k for r in range(Nfr >> k)]])
+            U2maps[pi] = (U2, k)
             P = time_pool(U2, s.k_alpha[a])
             S2.append(lam_pool(P, k) if avg else P[: s.n1])
         else:
@@ -145,7 +147,7 @@ def brute_jtfs(x, prm):
                 V = V[[r * 2 ** k for r in range(s.lam_out)]]
                 S2.append(V[:, frames])
     S2t = [time_pool(np.abs(Y2[a]), s.k_alpha[a]) for a in s.alphas]
-    return dict(S0=S0, S1=S1, S2=np.array(S2), S2t=np.concatenate(S2t, axis=0))
+    return dict(S0=S0, S1=S1, S2=np.array(S2), S2t=np.concatenate(S2t, axis=0), U2=U2maps)
 
 
 CASES = [
@@ -199,3 +201,23 @@ def test_reflect_pad_index_map():
     xp = O.pad_signal(x, s)
     ref = np.array([x[reflect_index(p, s.pad_left, prm.N)] for p in range(s.N_pad)])
     np.testing.assert_array_equal(xp, ref)
+
+
+@pytest.mark.parametrize("prm", CASES[:3], ids=lambda p: f"N{p.N}J{p.J}Q{p.Q}{p.pad[0]}{int(p.average_fr)}")
+def test_u2_map_equals_bruteforce(prm):
+    # NEXT-4 scale-rate map (Fig. 1): |X * Psi| before Phi, rows r' 2^k < n1,
+    # columns of the unpadded signal on the alpha grid (reading R21)
+    rng = np.random.default_rng(prm.N + 11)
+    x = rng.standard_normal(prm.N)
+    s = O.schedule(prm)
+    b = brute_jtfs(x, prm)
+    assert set(b["U2"]) == {pi for pi, pth in enumerate(s.paths) if pth[0] in (O.SPIN, O.PSI_T_PHI_F)}
+    for pi, (U2, k) in b["U2"].items():
+        a = s.paths[pi][2]
+        ka = s.k_alpha[a]
+        rows = len([r for r in range(s.N_fr >> k) if r * 2 ** k < s.n1])
+        c0 = -(-s.pad_left // 2 ** ka)
+        ref = U2[:rows, c0: c0 + -(-prm.N // 2 ** ka)]
+        got = O.u2_map(x, prm, pi, s)
+        assert got.shape == ref.shape == O.u2_map_shape(s, pi)
+        assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), pi
