@@ -249,6 +249,50 @@ JTFS_API jtfs_status jtfs_backward(jtfs_plan_t plan, const float* x, int64_t B, 
  * 14 DFT(dU1 W/|W|), 15 dX_hat, 16 dx_pad; offsets[17] = total.  Host query. */
 JTFS_API jtfs_status jtfs_backward_regions(jtfs_plan_t plan, int64_t B, int64_t* offsets, int32_t cap);
 
+/* ---- NEXT-4: mu-log compression and the scale-rate map ---- */
+
+/* mu(lambda_2) of Eq. (adalog:mu) over a batch of jtfs_forward records:
+ *   mu[p] = (1/B) sum_b sum_{lambda, t} S2_b[p][lambda][t]   for every S2 path p
+ * (jtfs_paths order; the double integral over the sampled grid is the map's sum),
+ * accumulated in fp64 in a fixed order (bit-stable), rounded to fp32.
+ *   S   device fp32 [B][floats_per_signal], B >= 1
+ *   mu  device fp32 [n_paths] (output)
+ * Asynchronous on `stream`.  For a set larger than one batch, average the per-batch
+ * mu weighted by the batch sizes. */
+JTFS_API jtfs_status jtfs_mulog_mu(jtfs_plan_t plan, const float* S, int64_t B, float* mu, void* stream);
+
+/* Eq. (adalog): out = S with every S2 value of path p replaced by
+ *   log(1 + S / (eps mu[p]))        (eps = 0.1 in the paper),
+ * S0 and S1 copied unchanged (reading R22: the transform is per second-order path
+ * lambda_2).  A path with eps * mu[p] <= 0 maps to 0.  out may alias S.
+ *   S, out  device fp32 [B][floats_per_signal];  mu device fp32 [n_paths];  eps > 0.
+ * Asynchronous on `stream`. */
+JTFS_API jtfs_status jtfs_mulog_apply(jtfs_plan_t plan, const float* S, int64_t B, const float* mu, float eps,
+                                      float* out, void* stream);
+
+/* jtfs_forward with the mu-log of Eq. (adalog) fused into the phi_F pooling /
+ * packing kernel (KE): out = [S0][S1][log(1 + S2 / (eps mu))] in one pass, bit-identical
+ * to jtfs_forward followed by jtfs_mulog_apply.  Arguments and rules as jtfs_forward,
+ * plus mu (device fp32 [n_paths], e.g. from jtfs_mulog_mu over a training set) and eps > 0. */
+JTFS_API jtfs_status jtfs_forward_mulog(jtfs_plan_t plan, const float* x, int64_t B, const float* mu, float eps,
+                                        float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Shape of the scale-rate map of S2 path `path` (reading R21): rows = ceil(n1 / 2^k),
+ * k = the path's lambda decimation (k_f(beta) for a spinned path in Eq. (3) mode,
+ * log2 F for psi_t x phi_f, 0 in Eq. (4) mode); cols = ceil(N / 2^k_alpha).  Only the
+ * psi_t paths (kinds SPIN, PSI_T_PHI_F) have one; other kinds or an out-of-range path
+ * return JTFS_ERR_INVALID_ARG.  Host query. */
+JTFS_API jtfs_status jtfs_u2_map_shape(jtfs_plan_t plan, int32_t path, int32_t* rows, int32_t* cols);
+
+/* Scale-rate visualisation of Fig. 1: |X * Psi_{alpha,beta,theta}|, the joint
+ * wavelet modulus BEFORE the lowpass Phi of Eq. (3), on the whole log-frequency and time
+ * axes: out[b][r][c] = |sum_lambda h_f[(r 2^k - lambda) mod N_fr] Y2_alpha[lambda][c0 + c]|,
+ * r' = r over the scalogram rows, c0 = ceil(pad_left / 2^k_alpha) (the unpadded signal).
+ *   x    device fp32 [B][N];  out device fp32 [B][rows][cols] (jtfs_u2_map_shape)
+ *   ws   the forward workspace (jtfs_workspace_size(plan, B)); asynchronous on `stream`. */
+JTFS_API jtfs_status jtfs_u2_map(jtfs_plan_t plan, const float* x, int64_t B, int32_t path, float* out,
+                                 void* ws, size_t ws_bytes, void* stream);
+
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)

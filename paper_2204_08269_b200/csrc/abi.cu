@@ -215,6 +215,8 @@ struct RunOpts {
   const jtfs::UnitSel* sel = nullptr;
   float* part = nullptr;  // KD partials target (default: the workspace's)
   bool skip_ke = false;
+  const float* mu = nullptr;  // fused mu-log in KE (jtfs_forward_mulog)
+  float mu_eps = 0.f;
 };
 
 void fill_ke_params(jtfs::Plan& P, jtfs::KEParams& kp, const float* part, const float* yphi, float* out);
@@ -250,6 +252,8 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   if (o.skip_ke) return "";
   KEParams kp{};
   fill_ke_params(P, kp, w.part, w.yphi, out);
+  kp.mu = o.mu;
+  kp.mu_eps = o.mu_eps;
   { StageScope s(P, 5, st); s.done(launch_ke(P, kp, nb, st)); }
   return "";
 }
@@ -417,8 +421,8 @@ static jtfs_status check_forward_args(jtfs_plan_t plan, const void* x, int64_t B
   return JTFS_OK;
 }
 
-jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* out, void* ws, size_t ws_bytes,
-                         void* stream) {
+static jtfs_status forward_impl(jtfs_plan_t plan, const float* x, int64_t B, float* out, void* ws,
+                                size_t ws_bytes, void* stream, const RunOpts& opts) {
   jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
   if (s != JTFS_OK || B == 0) return s;
   jtfs::Plan& P = plan->P;
@@ -439,12 +443,93 @@ jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* out
   layout_of(P, &lay);
   for (int64_t b0 = 0; b0 < B; b0 += mb) {
     const int nb = (int)std::min<int64_t>(mb, B - b0);
-    const std::string err = run_microbatch(P, x + b0 * P.N, nb, out + b0 * lay.floats_per_signal, w, false, 99, st);
+    const std::string err = run_microbatch(P, x + b0 * P.N, nb, out + b0 * lay.floats_per_signal, w, false, 99, st, opts);
     if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return JTFS_OK;
+}
+
+jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, float* out, void* ws, size_t ws_bytes,
+                         void* stream) {
+  return forward_impl(plan, x, B, out, ws, ws_bytes, stream, RunOpts());
+}
+
+jtfs_status jtfs_forward_mulog(jtfs_plan_t plan, const float* x, int64_t B, const float* mu, float eps, float* out,
+                               void* ws, size_t ws_bytes, void* stream) {
+  if (!(eps > 0.f)) return fail(JTFS_ERR_INVALID_ARG, "eps must be > 0");
+  if (B > 0 && !mu) return fail(JTFS_ERR_INVALID_ARG, "mu is NULL");
+  RunOpts o;
+  o.mu = mu;
+  o.mu_eps = eps;
+  return forward_impl(plan, x, B, out, ws, ws_bytes, stream, o);
+}
+
+jtfs_status jtfs_mulog_mu(jtfs_plan_t plan, const float* S, int64_t B, float* mu, void* stream) {
+  if (!plan || !S || !mu || B < 1) return fail(JTFS_ERR_INVALID_ARG, "bad argument (B must be >= 1)");
+  if (plan->P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");
+  DeviceGuard guard(plan->P.device);
+  jtfs::launch_mulog_mu(plan->P, S, B, mu, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
+}
+
+jtfs_status jtfs_mulog_apply(jtfs_plan_t plan, const float* S, int64_t B, const float* mu, float eps, float* out,
+                             void* stream) {
+  if (!plan || B < 0 || !(eps > 0.f)) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  if (plan->P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");
+  if (B == 0) return JTFS_OK;
+  if (!S || !mu || !out) return fail(JTFS_ERR_INVALID_ARG, "NULL buffer");
+  DeviceGuard guard(plan->P.device);
+  jtfs::launch_mulog_apply(plan->P, S, B, mu, eps, out, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
+}
+
+static bool u2_shape(const jtfs::Plan& P, int32_t path, int32_t* rows, int32_t* cols) {
+  if (path < 0 || path >= (int32_t)P.paths.size()) return false;
+  const jtfs_path_t& ph = P.paths[path];
+  if (ph.kind != JTFS_PATH_SPIN && ph.kind != JTFS_PATH_PSI_T_PHI_F) return false;
+  const jtfs::FrFilter& f = P.fr[P.path_filter[path]];
+  int ka = -1;
+  for (const auto& d : P.kd)
+    if (d.alpha == ph.alpha) ka = d.k_alpha;
+  if (ka < 0) return false;
+  *rows = (P.n1 + (1 << f.k) - 1) >> f.k;
+  *cols = (P.N + (1 << ka) - 1) >> ka;
+  return true;
+}
+
+jtfs_status jtfs_u2_map_shape(jtfs_plan_t plan, int32_t path, int32_t* rows, int32_t* cols) {
+  if (!plan || !rows || !cols) return fail(JTFS_ERR_INVALID_ARG, "NULL argument");
+  if (!u2_shape(plan->P, path, rows, cols))
+    return fail(JTFS_ERR_INVALID_ARG, "path has no scale-rate map (psi_t paths only) or is out of range");
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_u2_map(jtfs_plan_t plan, const float* x, int64_t B, int32_t path, float* out, void* ws,
+                        size_t ws_bytes, void* stream) {
+  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK) return s;
+  int32_t rows = 0, cols = 0;
+  if (!u2_shape(plan->P, path, &rows, &cols))
+    return fail(JTFS_ERR_INVALID_ARG, "path has no scale-rate map (psi_t paths only) or is out of range");
+  if (B == 0) return JTFS_OK;
+  jtfs::Plan& P = plan->P;
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t mb = std::min<int64_t>(B, P.mb);
+  WsPtrs w = carve(P, ws, mb);
+  for (int64_t b0 = 0; b0 < B; b0 += mb) {
+    const int nb = (int)std::min<int64_t>(mb, B - b0);
+    jtfs::launch_pad_fft(P, x + b0 * P.N, nb, w.xhat, w.tmp, st);
+    jtfs::launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st);
+    jtfs::launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st);
+    jtfs::launch_u2_map(P, w.y2, nb, path, rows, cols, out + b0 * (int64_t)rows * cols, st);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
 }
 
 jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B, float* out_host, float* x_dev,

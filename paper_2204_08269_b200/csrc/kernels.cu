@@ -490,6 +490,9 @@ __global__ void __launch_bounds__(256) k_kd_simt(KDParams p) {
   }
 }
 
+// Eq. (adalog) of one S2 value: log(1 + S / (eps mu)); 0 where eps mu <= 0
+__device__ __forceinline__ float mulog_val(float s, float den) { return den > 0.f ? log1pf(s / den) : 0.f; }
+
 // ---------------------------------------------------------------------------------
 // KE: lambda pooling (phi_F) of the pooled rows, phi-only paths, packing of S2.
 // One block per (signal, path).
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
         if (d < 0) d += p.N_fr;
         acc = fmaf(__ldg(p.hphiF + d), yphi[l * p.NPT + p.frame0 + m], acc);
       }
-      outp[idx] = acc;
+      outp[idx] = p.mu ? mulog_val(acc, p.mu_eps * __ldg(p.mu + pi)) : acc;
     }
     return;
   }
@@ -578,8 +581,82 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
     const float* wq = Wf + (int64_t)q * f.nrows;
     float acc = 0.f;
     for (int r = band.x; r < band.y; ++r) acc = fmaf(__ldg(wq + r), Pm[r * nf + m], acc);
-    outp[idx] = acc;
+    outp[idx] = p.mu ? mulog_val(acc, p.mu_eps * __ldg(p.mu + pi)) : acc;
   }
+}
+
+// ---------------------------------------------------------------------------------
+// NEXT-4.  mu(lambda_2) = (1/B) sum_b sum_{lambda,t} S2_b[p] (Eq. (adalog:mu)):
+// one block per path, fp64 per-thread sums in a fixed index order, fixed shared tree.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mulog_mu(const float* __restrict__ S, int64_t B, int64_t fps,
+                                                  int64_t off_s2, int map, float* __restrict__ mu) {
+  __shared__ double red[256];
+  const int pi = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t b = 0; b < B; ++b) {
+    const float* src = S + b * fps + off_s2 + (int64_t)pi * map;
+    for (int i = threadIdx.x; i < map; i += 256) acc += (double)__ldg(src + i);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mu[pi] = (float)(red[0] / (double)B);
+}
+
+// Eq. (adalog) over whole records: S0/S1 copied, S2 compressed (reading R22)
+__global__ void __launch_bounds__(256) k_mulog_apply(const float* S, int64_t n, int64_t fps, int64_t off_s2,
+                                                     int map, const float* __restrict__ mu, float eps,
+                                                     float* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i % fps;
+    const float v = S[i];
+    out[i] = j < off_s2 ? v : mulog_val(v, eps * __ldg(mu + (j - off_s2) / map));
+  }
+}
+
+// Scale-rate map of one psi_t path (Fig. 1; reading R21): |Z| before Phi.
+// grid (column blocks, rows, signals); the row's taps are block-uniform (broadcast),
+// Y2 rows are read coalesced along time.
+struct U2MapParams {
+  const float* y2;      // micro-batch Y2 base, planar rows 2l (re), 2l+1 (im), per alpha [2K][L]
+  const float2* hc;     // complex taps [N_fr] (psi path), or nullptr
+  const float* hr;      // real taps [N_fr] (phi_F path), or nullptr
+  float* out;           // [nsig][rows][cols]
+  int64_t y2_off, y2_stride;
+  int K, L, N_fr, k, c0, rows, cols, conj;
+};
+
+__global__ void __launch_bounds__(256) k_u2_map(U2MapParams p) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  const int r = blockIdx.y;
+  const int b = blockIdx.z;
+  if (c >= p.cols) return;
+  const float* Y = p.y2 + (int64_t)b * p.y2_stride + p.y2_off + p.c0 + c;
+  const int rp = r << p.k;
+  float zr = 0.f, zi = 0.f;
+  for (int l = 0; l < p.K; ++l) {
+    int d = (rp - l) % p.N_fr;
+    if (d < 0) d += p.N_fr;
+    float hr, hi;
+    if (p.hc) {
+      const float2 h = __ldg(p.hc + d);
+      hr = h.x;
+      hi = p.conj ? -h.y : h.y;
+    } else {
+      hr = __ldg(p.hr + d);
+      hi = 0.f;
+    }
+    const float yr = __ldg(Y + (int64_t)(2 * l) * p.L), yi = __ldg(Y + (int64_t)(2 * l + 1) * p.L);
+    zr = fmaf(hr, yr, zr);
+    zr = fmaf(-hi, yi, zr);
+    zi = fmaf(hr, yi, zi);
+    zi = fmaf(hi, yr, zi);
+  }
+  p.out[((int64_t)b * p.rows + r) * p.cols + c] = sqrtf(fmaf(zr, zr, zi * zi));
 }
 
 // check for NaN / Inf in x
@@ -893,6 +970,57 @@ int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st) {
 
 cudaError_t ke_set_smem(const Plan& P) {
   return cudaFuncSetAttribute(k_ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke_smem_bytes(P));
+}
+
+int launch_mulog_mu(const Plan& P, const float* S, int64_t B, float* mu, cudaStream_t st) {
+  const int64_t off_s2 = P.n_frames + (int64_t)P.n1 * P.n_frames;
+  const int map = P.lam_out * P.n_frames;
+  const int64_t fps = off_s2 + (int64_t)P.paths.size() * map;
+  k_mulog_mu<<<(unsigned)P.paths.size(), 256, 0, st>>>(S, B, fps, off_s2, map, mu);
+  return 1;
+}
+
+int launch_mulog_apply(const Plan& P, const float* S, int64_t B, const float* mu, float eps, float* out,
+                       cudaStream_t st) {
+  const int64_t off_s2 = P.n_frames + (int64_t)P.n1 * P.n_frames;
+  const int map = P.lam_out * P.n_frames;
+  const int64_t fps = off_s2 + (int64_t)P.paths.size() * map;
+  const int64_t n = B * fps;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_mulog_apply<<<(unsigned)blocks, 256, 0, st>>>(S, n, fps, off_s2, map, mu, eps, out);
+  return 1;
+}
+
+int launch_u2_map(const Plan& P, const float* y2, int nsig, int path, int rows, int cols, float* out,
+                  cudaStream_t st) {
+  const jtfs_path_t& ph = P.paths[path];
+  const FrFilter& f = P.fr[P.path_filter[path]];
+  int slot = -1;
+  for (size_t i = 0; i < P.kd.size(); ++i)
+    if (P.kd[i].alpha == ph.alpha) slot = (int)i;
+  const AlphaKD& d = P.kd[slot];
+  const int nbeta = (int)P.bf.xi.size();
+  U2MapParams k{};
+  k.y2 = y2;
+  if (f.kind == 0) {
+    // stored taps are psi_{beta,+1}; psi_{beta,-1} = their conjugate (psi_hat real, reading R10)
+    k.hc = (const float2*)P.d_hphi + (size_t)f.beta * P.N_fr;
+    k.conj = f.theta == -1;
+  } else {
+    k.hr = P.d_hphi + (size_t)2 * nbeta * P.N_fr;
+  }
+  k.out = out;
+  k.y2_off = 2 * d.y2_off;
+  k.y2_stride = 2 * P.y2_total;
+  k.K = d.K;
+  k.L = d.L;
+  k.N_fr = P.N_fr;
+  k.k = f.k;
+  k.c0 = (P.pad_left + (1 << d.k_alpha) - 1) >> d.k_alpha;
+  k.rows = rows;
+  k.cols = cols;
+  k_u2_map<<<dim3((cols + 255) / 256, rows, nsig), 256, 0, st>>>(k);
+  return 1;
 }
 
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st) {

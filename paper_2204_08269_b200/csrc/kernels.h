@@ -55,6 +55,8 @@ struct KEParams {
   float* out;
   int64_t fps, off_s2, part_stride;
   int n1, NPT, N_fr, lam_out, n_frames, frame0, Mpad, k_phiphi;
+  const float* mu;  // NEXT-4 fused mu-log (jtfs_forward_mulog): per path mu, or nullptr
+  float mu_eps;
 };
 
 int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2* tmp, cudaStream_t st);
@@ -81,6 +83,12 @@ struct BwdWs {
 };
 int launch_backward(Plan& P, const float* x, int nb, const float* dout, float* dx, const BwdWs& w,
                     cudaStream_t st);
+// NEXT-4: mu-log (Eqs. (adalog:mu), (adalog)) and the scale-rate map (Fig. 1)
+int launch_mulog_mu(const Plan& P, const float* S, int64_t B, float* mu, cudaStream_t st);
+int launch_mulog_apply(const Plan& P, const float* S, int64_t B, const float* mu, float eps, float* out,
+                       cudaStream_t st);
+int launch_u2_map(const Plan& P, const float* y2, int nsig, int path, int rows, int cols, float* out,
+                  cudaStream_t st);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 
 }  // namespace jtfs

@@ -36,6 +36,7 @@ EXPORTS = [
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
     "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions",
+    "jtfs_mulog_mu", "jtfs_mulog_apply", "jtfs_forward_mulog", "jtfs_u2_map_shape", "jtfs_u2_map",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -95,6 +96,11 @@ _lib.jtfs_scattering1d.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_backward_workspace_size.argtypes = [_P, C.c_int64, C.POINTER(C.c_size_t)]
 _lib.jtfs_backward.argtypes = [_P, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]
 _lib.jtfs_backward_regions.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), C.c_int32]
+_lib.jtfs_mulog_mu.argtypes = [_P, _P, C.c_int64, _P, _P]
+_lib.jtfs_mulog_apply.argtypes = [_P, _P, C.c_int64, _P, C.c_float, _P, _P]
+_lib.jtfs_forward_mulog.argtypes = [_P, _P, C.c_int64, _P, C.c_float, _P, _P, C.c_size_t, _P]
+_lib.jtfs_u2_map_shape.argtypes = [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+_lib.jtfs_u2_map.argtypes = [_P, _P, C.c_int64, C.c_int32, _P, _P, C.c_size_t, _P]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -347,6 +353,56 @@ class Plan:
         ws = self.workspace(B)
         _check(_lib.jtfs_debug_tap(self._h, tap, _ptr(x), B, _ptr(out), out.numel(), _ptr(ws), ws.numel(),
                                    _stream_handle(None)), "jtfs_debug_tap")
+        return out
+
+    # ---- NEXT-4: mu-log (Eqs. (adalog:mu), (adalog)) and the Fig. 1 map ----
+    def mulog_mu(self, S, stream=None):
+        """mu(lambda_2) of a batch of records S [B, floats_per_signal] -> float32 CUDA [n_paths]."""
+        import torch
+        assert S.dtype == torch.float32 and S.is_cuda and S.is_contiguous() and S.dim() == 2
+        mu = torch.empty(self.layout.n_paths, dtype=torch.float32, device=S.device)
+        _check(_lib.jtfs_mulog_mu(self._h, _ptr(S), S.shape[0], _ptr(mu), _stream_handle(stream)),
+               "jtfs_mulog_mu")
+        return mu
+
+    def mulog_apply(self, S, mu, eps: float = 0.1, out=None, stream=None):
+        """Records with every S2 value replaced by log(1 + S / (eps mu)); S0/S1 unchanged."""
+        import torch
+        assert S.dtype == torch.float32 and S.is_cuda and S.is_contiguous() and S.dim() == 2
+        if out is None:
+            out = torch.empty_like(S)
+        _check(_lib.jtfs_mulog_apply(self._h, _ptr(S), S.shape[0], _ptr(mu), float(eps), _ptr(out),
+                                     _stream_handle(stream)), "jtfs_mulog_apply")
+        return out
+
+    def forward_mulog(self, x, mu, eps: float = 0.1, out=None, stream=None):
+        """jtfs_forward with the mu-log fused into KE."""
+        import torch
+        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+        B = x.shape[0]
+        if out is None:
+            out = torch.empty(B, self.floats_per_signal, dtype=torch.float32, device=x.device)
+        ws = self.workspace(B)
+        _check(_lib.jtfs_forward_mulog(self._h, _ptr(x), B, _ptr(mu), float(eps), _ptr(out), _ptr(ws),
+                                       ws.numel(), _stream_handle(stream)), "jtfs_forward_mulog")
+        return out
+
+    def u2_map_shape(self, path: int):
+        r, c = C.c_int32(), C.c_int32()
+        _check(_lib.jtfs_u2_map_shape(self._h, path, C.byref(r), C.byref(c)), "jtfs_u2_map_shape")
+        return r.value, c.value
+
+    def u2_map(self, x, path: int, out=None, stream=None):
+        """Scale-rate map |X * Psi| of S2 path `path` before Phi: x [B, N] -> [B, rows, cols]."""
+        import torch
+        assert x.dtype == torch.float32 and x.is_cuda and x.is_contiguous() and x.dim() == 2
+        rows, cols = self.u2_map_shape(path)
+        B = x.shape[0]
+        if out is None:
+            out = torch.empty(B, rows, cols, dtype=torch.float32, device=x.device)
+        ws = self.workspace(B)
+        _check(_lib.jtfs_u2_map(self._h, _ptr(x), B, path, _ptr(out), _ptr(ws), ws.numel(),
+                                _stream_handle(stream)), "jtfs_u2_map")
         return out
 
     # ---- unpack the out_3D record ----

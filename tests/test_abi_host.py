@@ -138,3 +138,19 @@ def test_scat1d_paper_shape(jt):
     # admissibility reading, so only n1 and the frames are pinned)
     lay = jt.Plan(**SCAT1D, device=-1).scat1d_layout
     assert (lay.n_frames, lay.n1) == (32, 175)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_u2_map_shape_matches_oracle(jt, name):
+    # NEXT-4 scale-rate map (Fig. 1): host query vs the oracle's shape rule (reading R21)
+    kw = CFGS[name]
+    plan = hostplan(jt, **kw)
+    s = O.schedule(O.Params(**kw))
+    for pi, (kind, _, _, _) in enumerate(s.paths):
+        if kind in (O.SPIN, O.PSI_T_PHI_F):
+            assert plan.u2_map_shape(pi) == O.u2_map_shape(s, pi)
+        else:
+            with pytest.raises(jt.JTFSError):
+                plan.u2_map_shape(pi)
+    with pytest.raises(jt.JTFSError):
+        plan.u2_map_shape(len(s.paths))
