@@ -1,0 +1,68 @@
+"""Plain fp64 oracle of the K-nearest-neighbour parameter regression.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Shares no code with the CUDA path.
+
+PAPER.md Sec. 3.5 "Regression from Nearest Neighbors":
+  * neighbour sets built greedily, Eq.:
+        N_0 = {},  N_{k+1}(theta_i) = N_k(theta_i) U { argmin_{theta_j not in N_k} ||S g(theta_j) - S g(theta_i)||_2 },
+    "pairwise Euclidean distance with all other examples" -- so j != i (reading R23);
+  * estimate theta~_i = (1/K) sum_{theta_j in N_K(theta_i)} theta_j;
+  * error ratio theta~_i / theta_i per parameter;
+  * K = 40, the Isomap neighbour count.
+Readings (R23): distances in fp64 on the fp32 features; ties in the
+argmin broken by the smaller example index (the paper is silent; the greedy argmin
+with this tie-break equals a stable sort by (distance, index)).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def pairwise_sq_dist(F: np.ndarray) -> np.ndarray:
+    """D[i, j] = ||F_i - F_j||_2^2 in fp64, written as the plain sum of squared differences."""
+    F = np.asarray(F, dtype=np.float64)
+    n = F.shape[0]
+    D = np.empty((n, n))
+    for i in range(n):
+        diff = F - F[i]
+        D[i] = np.einsum("jd,jd->j", diff, diff)
+    return D
+
+
+def knn_sets(D: np.ndarray, K: int) -> np.ndarray:
+    """N_K(theta_i) for every i, in the order the greedy recursion of P:201-209 adds
+    them: row i = the K indices j != i of smallest D[i, j], ties -> smaller j."""
+    n = D.shape[0]
+    if not 1 <= K < n:
+        raise ValueError("need 1 <= K < n")
+    out = np.empty((n, K), dtype=np.int64)
+    idx = np.arange(n)
+    for i in range(n):
+        order = np.lexsort((idx, D[i]))          # primary key distance, then index
+        order = order[order != i]
+        out[i] = order[:K]
+    return out
+
+
+def knn_greedy(D: np.ndarray, K: int, i: int) -> list:
+    """The paper's recursion for one example, literally: K argmin steps over the
+    examples not yet chosen (and not i itself).  Small cases only."""
+    chosen = []
+    for _ in range(K):
+        best = None
+        for j in range(D.shape[0]):
+            if j == i or j in chosen:
+                continue
+            if best is None or D[i, j] < D[i, best]:
+                best = j
+        chosen.append(best)
+    return chosen
+
+
+def knn_regress(F: np.ndarray, theta: np.ndarray, K: int = 40):
+    """Returns (neighbours [n, K], theta_hat [n, P], ratio [n, P])."""
+    theta = np.asarray(theta, dtype=np.float64)
+    D = pairwise_sq_dist(F)
+    nb = knn_sets(D, K)
+    theta_hat = theta[nb].mean(axis=1)
+    return nb, theta_hat, theta_hat / theta

@@ -1,0 +1,76 @@
+"""Pins of the K-NN regression oracle.
+
+* the sort-based neighbour sets equal the paper's greedy argmin recursion, literally
+  transcribed, on small random sets;
+* points on a line with known gaps: the neighbour sets are known by hand;
+* K = n - 1: theta~_i = (sum theta - theta_i) / (n - 1) (closed form);
+* invariances of Euclidean K-NN: a translation / orthogonal rotation of the features
+  changes nothing; a permutation of the examples permutes the result;
+* the distance routine against the Gram-matrix identity ||a-b||^2 = a.a + b.b - 2 a.b.
+"""
+import numpy as np
+import pytest
+
+from oracle import knn as Kn
+
+
+def test_sets_equal_paper_greedy_recursion():
+    rng = np.random.default_rng(0)
+    for n, d, K in ((12, 3, 5), (30, 7, 11), (9, 2, 8)):
+        F = rng.standard_normal((n, d))
+        D = Kn.pairwise_sq_dist(F)
+        nb = Kn.knn_sets(D, K)
+        for i in range(n):
+            assert list(nb[i]) == Kn.knn_greedy(D, K, i)
+
+
+def test_ties_break_by_index_like_the_greedy_argmin():
+    F = np.array([[0.0], [1.0], [-1.0], [2.0], [-2.0]])   # equal distances on both sides
+    D = Kn.pairwise_sq_dist(F)
+    nb = Kn.knn_sets(D, 4)
+    assert list(nb[0]) == [1, 2, 3, 4] == Kn.knn_greedy(D, 4, 0)
+
+
+def test_points_on_a_line():
+    x = np.array([0.0, 1.0, 3.0, 7.0, 15.0])               # gaps 1, 2, 4, 8
+    nb = Kn.knn_sets(Kn.pairwise_sq_dist(x[:, None]), 2)
+    assert [list(r) for r in nb] == [[1, 2], [0, 2], [1, 0], [2, 1], [3, 2]]
+
+
+def test_k_equals_n_minus_one_closed_form():
+    rng = np.random.default_rng(1)
+    F = rng.standard_normal((10, 4))
+    th = rng.uniform(1, 2, size=(10, 3))
+    _, hat, ratio = Kn.knn_regress(F, th, K=9)
+    np.testing.assert_allclose(hat, (th.sum(0) - th) / 9, rtol=1e-14)
+    np.testing.assert_allclose(ratio, hat / th, rtol=1e-15)
+
+
+def test_invariances():
+    rng = np.random.default_rng(2)
+    F = rng.standard_normal((40, 6))
+    th = rng.uniform(1, 2, size=(40, 2))
+    nb, hat, _ = Kn.knn_regress(F, th, K=7)
+    Qm, _ = np.linalg.qr(rng.standard_normal((6, 6)))
+    nb2, hat2, _ = Kn.knn_regress(F @ Qm + 3.0, th, K=7)
+    assert np.array_equal(nb, nb2)
+    np.testing.assert_allclose(hat, hat2, rtol=1e-14)
+    perm = rng.permutation(40)
+    nb3, hat3, _ = Kn.knn_regress(F[perm], th[perm], K=7)
+    inv = np.argsort(perm)
+    np.testing.assert_allclose(hat3, hat[perm], rtol=1e-14)
+    assert all(set(perm[nb3[k]]) == set(nb[perm[k]]) for k in range(40))
+    del inv
+
+
+def test_distance_against_gram_identity():
+    rng = np.random.default_rng(3)
+    F = rng.standard_normal((25, 11))
+    G = F @ F.T
+    ref = np.diag(G)[:, None] + np.diag(G)[None, :] - 2 * G
+    np.testing.assert_allclose(Kn.pairwise_sq_dist(F), ref, atol=1e-12)
+
+
+def test_rejects_bad_k():
+    with pytest.raises(ValueError):
+        Kn.knn_sets(np.zeros((4, 4)), 4)
