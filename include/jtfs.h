@@ -293,6 +293,30 @@ JTFS_API jtfs_status jtfs_u2_map_shape(jtfs_plan_t plan, int32_t path, int32_t* 
 JTFS_API jtfs_status jtfs_u2_map(jtfs_plan_t plan, const float* x, int64_t B, int32_t path, float* out,
                                  void* ws, size_t ws_bytes, void* stream);
 
+/* ---- NEXT-3: K-nearest-neighbour parameter regression ----
+ * For every example i of a feature set F (e.g. JTFS records of the 16^3 AM/FM chirp grid,
+ * P:139-140), the K examples j != i at the smallest Euclidean distance ||F_j - F_i||_2 --
+ * the greedy argmin recursion of P:201-209, ties to the smaller index (reading R23) --
+ * and theta~_i = (1/K) sum_{j in N_K(i)} theta_j, ratio theta~_i / theta_i
+ * (P:210).  Distances are sums of squared differences in fp64 over the fp32 features.
+ * Plan-independent. */
+
+/* Workspace bytes for n examples (the n x n fp64 distance matrix).  Host query. */
+JTFS_API jtfs_status jtfs_knn_workspace_size(int64_t n, size_t* bytes);
+
+/*   F          device fp32, example i's features at F[i * ldf + 0 .. d)   (ldf >= d)
+ *   n, d       2 <= n <= 16384 examples, d >= 1 features
+ *   theta      device fp64 [n][n_params] parameters (may be NULL when n_params = 0)
+ *   K          1 <= K < n  (the paper uses K = 40)
+ *   nbr        device int32 [n][K] neighbour indices in the recursion's order (output)
+ *   theta_hat  device fp64 [n][n_params] or NULL;  ratio device fp64 [n][n_params] or NULL
+ *   ws         device, >= jtfs_knn_workspace_size(n) bytes, 256-byte aligned
+ * Asynchronous on `stream`; deterministic (fixed-order sums, total order on keys).
+ * JTFS_ERR_INVALID_ARG for sizes out of range / NULL buffers, JTFS_ERR_WORKSPACE. */
+JTFS_API jtfs_status jtfs_knn_regress(const float* F, int64_t n, int64_t d, int64_t ldf, const double* theta,
+                                      int32_t n_params, int32_t K, int32_t* nbr, double* theta_hat,
+                                      double* ratio, void* ws, size_t ws_bytes, void* stream);
+
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)

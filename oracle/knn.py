@@ -29,6 +29,23 @@ def pairwise_sq_dist(F: np.ndarray) -> np.ndarray:
     return D
 
 
+def sq_dist_rows(F: np.ndarray, rows) -> np.ndarray:
+    """Rows `rows` of pairwise_sq_dist(F) only (for sampled checks at full size)."""
+    F = np.asarray(F, dtype=np.float64)
+    out = np.empty((len(rows), F.shape[0]))
+    for r, i in enumerate(rows):
+        diff = F - F[i]
+        out[r] = np.einsum("jd,jd->j", diff, diff)
+    return out
+
+
+def knn_row(Drow: np.ndarray, i: int, K: int) -> np.ndarray:
+    """N_K(theta_i) from example i's distance row (same rule as knn_sets)."""
+    idx = np.arange(len(Drow))
+    order = np.lexsort((idx, Drow))
+    return order[order != i][:K]
+
+
 def knn_sets(D: np.ndarray, K: int) -> np.ndarray:
     """N_K(theta_i) for every i, in the order the greedy recursion of P:201-209 adds
     them: row i = the K indices j != i of smallest D[i, j], ties -> smaller j."""

@@ -835,6 +835,28 @@ jtfs_status jtfs_reduce_pack(jtfs_plan_t plan, const float* partials, int64_t B,
   return JTFS_OK;
 }
 
+// ---- NEXT-3: K-NN regression (jtfs.h: jtfs_knn_workspace_size / jtfs_knn_regress) ----
+jtfs_status jtfs_knn_workspace_size(int64_t n, size_t* bytes) {
+  if (!bytes || n < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  *bytes = jtfs::knn_workspace_bytes(n);
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_knn_regress(const float* F, int64_t n, int64_t d, int64_t ldf, const double* theta,
+                             int32_t n_params, int32_t K, int32_t* nbr, double* theta_hat, double* ratio, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (n < 2 || n > 16384) return fail(JTFS_ERR_INVALID_ARG, "need 2 <= n <= 16384");
+  if (d < 1 || ldf < d || d > (int64_t)1 << 30) return fail(JTFS_ERR_INVALID_ARG, "need d >= 1 and ldf >= d");
+  if (K < 1 || K >= n) return fail(JTFS_ERR_INVALID_ARG, "need 1 <= K < n");
+  if (n_params < 0 || (n_params > 0 && !theta)) return fail(JTFS_ERR_INVALID_ARG, "theta is NULL");
+  if (!F || !nbr || !ws) return fail(JTFS_ERR_INVALID_ARG, "NULL buffer");
+  if (!aligned(ws, 256)) return fail(JTFS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (ws_bytes < jtfs::knn_workspace_bytes(n)) return fail(JTFS_ERR_WORKSPACE, "workspace too small");
+  cudaError_t e = jtfs::launch_knn(F, (int)n, (int)d, ldf, theta, n_params, K, nbr, n_params ? theta_hat : nullptr,
+                                   n_params ? ratio : nullptr, ws, (cudaStream_t)stream);
+  return e != cudaSuccess ? cuda_fail(e, "K-NN kernels") : JTFS_OK;
+}
+
 jtfs_status jtfs_debug_tap_size(jtfs_plan_t plan, int32_t tap, int64_t B, int64_t* floats) {
   if (!plan || !floats || B < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
   const jtfs::Plan& P = plan->P;

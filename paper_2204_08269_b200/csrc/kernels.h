@@ -89,6 +89,10 @@ int launch_mulog_apply(const Plan& P, const float* S, int64_t B, const float* mu
                        cudaStream_t st);
 int launch_u2_map(const Plan& P, const float* y2, int nsig, int path, int rows, int cols, float* out,
                   cudaStream_t st);
+// NEXT-3: K-NN regression (knn.cu)
+size_t knn_workspace_bytes(int64_t n);
+cudaError_t launch_knn(const float* F, int n, int d, int64_t ldf, const double* theta, int P, int K, int32_t* nbr,
+                       double* theta_hat, double* ratio, void* ws, cudaStream_t st);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 
 }  // namespace jtfs

@@ -37,6 +37,7 @@ EXPORTS = [
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
     "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions",
     "jtfs_mulog_mu", "jtfs_mulog_apply", "jtfs_forward_mulog", "jtfs_u2_map_shape", "jtfs_u2_map",
+    "jtfs_knn_workspace_size", "jtfs_knn_regress",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -101,6 +102,9 @@ _lib.jtfs_mulog_apply.argtypes = [_P, _P, C.c_int64, _P, C.c_float, _P, _P]
 _lib.jtfs_forward_mulog.argtypes = [_P, _P, C.c_int64, _P, C.c_float, _P, _P, C.c_size_t, _P]
 _lib.jtfs_u2_map_shape.argtypes = [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
 _lib.jtfs_u2_map.argtypes = [_P, _P, C.c_int64, C.c_int32, _P, _P, C.c_size_t, _P]
+_lib.jtfs_knn_workspace_size.argtypes = [C.c_int64, C.POINTER(C.c_size_t)]
+_lib.jtfs_knn_regress.argtypes = [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P, _P,
+                                  C.c_size_t, _P]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -413,6 +417,27 @@ class Plan:
         s1 = out[..., L.off_s1:L.off_s2].reshape(*out.shape[:-1], L.n1, fr)
         s2 = out[..., L.off_s2:].reshape(*out.shape[:-1], L.n_paths, L.lambda_out, fr)
         return s0, s1, s2
+
+
+def knn_regress(F, theta=None, K: int = 40, stream=None):
+    """K-NN parameter regression of feature rows F (float32 CUDA [n, d], row
+    stride may exceed d) with parameters theta (float64 CUDA [n, P] or None).
+    Returns (nbr int32 [n, K], theta_hat float64 [n, P] | None, ratio float64 [n, P] | None)."""
+    import torch
+    assert F.dtype == torch.float32 and F.is_cuda and F.dim() == 2 and F.stride(1) == 1
+    n, d = F.shape
+    P = 0 if theta is None else theta.shape[1]
+    if theta is not None:
+        assert theta.dtype == torch.float64 and theta.is_cuda and theta.is_contiguous() and theta.shape[0] == n
+    sz = C.c_size_t()
+    _check(_lib.jtfs_knn_workspace_size(n, C.byref(sz)), "jtfs_knn_workspace_size")
+    ws = torch.empty(max(int(sz.value), 1), dtype=torch.uint8, device=F.device)
+    nbr = torch.empty(n, K, dtype=torch.int32, device=F.device)
+    hat = torch.empty(n, P, dtype=torch.float64, device=F.device) if P else None
+    ratio = torch.empty(n, P, dtype=torch.float64, device=F.device) if P else None
+    _check(_lib.jtfs_knn_regress(_ptr(F), n, d, F.stride(0), _ptr(theta), P, K, _ptr(nbr), _ptr(hat), _ptr(ratio),
+                                 _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_knn_regress")
+    return nbr, hat, ratio
 
 
 def jtfs_plan(N, J, Q, J_fr, Q_fr, T, F, flags=0) -> Plan:

@@ -74,3 +74,14 @@ def test_distance_against_gram_identity():
 def test_rejects_bad_k():
     with pytest.raises(ValueError):
         Kn.knn_sets(np.zeros((4, 4)), 4)
+
+
+def test_row_helpers_equal_full_matrix():
+    rng = np.random.default_rng(4)
+    F = rng.standard_normal((30, 5))
+    D = Kn.pairwise_sq_dist(F)
+    rows = [0, 7, 29]
+    np.testing.assert_array_equal(Kn.sq_dist_rows(F, rows), D[rows])
+    nb = Kn.knn_sets(D, 6)
+    for i in rows:
+        assert np.array_equal(Kn.knn_row(D[i], i, 6), nb[i])
