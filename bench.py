@@ -21,6 +21,9 @@ paper's Scattering1D setting (J = 13, Q = 16, T = 2^11, 32 frames),
 T = 2^13; an iteration is forward + normalised-error loss + jtfs_backward + bold-driver
 step; ms per iteration (lower is better), E after 20 and 100 iterations.
 
+`--workload c2` (BASELINE configs[1]): JTFS of the 16^3 AM/FM chirp grid
+(Eq. (4)) + K = 40 nearest-neighbour regression of (f_c, f_m, gamma); signals/s.
+
 `--workload c4` (not the headline metric): latency of ONE long
 signal (bird texture, N = 2^17, J = 13) path-sharded over the ranks
 (paper_2204_08269_b200/shard.py: KD units split by LPT, partials summed onto
@@ -41,6 +44,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CFG = dict(N=2 ** 16, J=12, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
+CFG2 = dict(N=2 ** 13, J=8, Q=16, J_fr=4, Q_fr=1, T=2 ** 13, F=16)  # BASELINE configs[1], Eq. (4)
 CFG4 = dict(N=2 ** 17, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 13, F=4)
 CFGS1D = dict(N=2 ** 16, J=13, Q=16, J_fr=5, Q_fr=1, T=2 ** 11, F=4)
 CFGRS = dict(N=2 ** 16, J=12, Q=12, J_fr=5, Q_fr=1, T=2 ** 13, F=32)  # P:359, P:366, P:370 (F = 2^J_fr, R12)
@@ -273,6 +277,62 @@ def run_resynth(args, rank, world, local, dev):
     return 0
 
 
+def run_c2(args, rank, world, local, dev):
+    """c2 manifold grid (BASELINE configs[1]; NEXT-3): JTFS of the 16^3 AM/FM chirps
+    (Eq. (4)) + K = 40 nearest-neighbour regression.
+    One step = the whole grid on every rank (weak scaling); signals/s."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2204_08269_b200 import jtfs, signals
+    theta, X = signals.chirp_grid()
+    plan = jtfs.Plan(**{k: CFG2[k] for k in ("N", "J", "Q", "J_fr", "Q_fr", "T", "F")}, average_fr=False,
+                     device=local)
+    x = torch.from_numpy(X).to(dev)
+    th = torch.from_numpy(theta).to(dev)
+    out = torch.empty(x.shape[0], plan.floats_per_signal, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        plan.forward(x, out)
+        jtfs.knn_regress(out, th, 40)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        plan.forward(x, out)
+        ev[k][1].record(stream)
+        nb, hat, ratio = jtfs.knn_regress(out, th, 40)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    fwd = sum(e[0].elapsed_time(e[1]) for e in ev)
+    knn = sum(e[1].elapsed_time(e[2]) for e in ev)
+    t = torch.tensor([fwd + knn, fwd, knn], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, fwd_ms, knn_ms = (float(v) for v in t.tolist())
+    r = ratio.cpu().numpy()
+    if rank == 0:
+        n = x.shape[0]
+        print(json.dumps({
+            "metric": "c2 chirp-grid signals/s (JTFS N=2^13, J=8, Q=16, Eq. (4) + K=40 NN regression)",
+            "value": n * world * args.steps / (total_ms / 1e3), "unit": "signals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "16^3 AM/FM chirp grid (BASELINE configs[1])", "signals": n,
+                       "jtfs_ms": fwd_ms / args.steps, "knn_ms": knn_ms / args.steps,
+                       "l2": "flushed before every timed step (256 MiB write)", **CFG2},
+            "knn_error_ratio_p05_p50_p95": {nm: [round(float(v), 4) for v in np.quantile(r[:, i], [0.05, 0.5, 0.95])]
+                                            for i, nm in enumerate(("f_c", "f_m", "gamma"))}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -281,7 +341,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="signals per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "scat1d", "resynth"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "scat1d", "resynth"])
     args = ap.parse_args()
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -302,6 +362,8 @@ def main():
         dist.barrier()
     if args.workload == "c4":
         return run_c4(args, rank, world, local, dev)
+    if args.workload == "c2":
+        return run_c2(args, rank, world, local, dev)
     if args.workload == "scat1d":
         return run_scat1d(args, rank, world, local, dev)
     if args.workload == "resynth":
