@@ -67,6 +67,7 @@ struct AlphaKD {
   int tc_Nt = 0;        // time columns per tile (64 or 128)
   int tc_NBB = 2;       // fp16 B-operand tile buffers
   int tc_S = 2, tc_tpu = 1;
+  int tc_rps = 1;       // K-records per A ring stage
   int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16
   int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
   int64_t y16_off = 0;  // fp16 offset of Y16_alpha [hi|lo][K16][L] in one signal's Y16 buffer (KY output)

@@ -172,7 +172,7 @@ __device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
 constexpr uint32_t kLayoutSW128 = 2, kLayoutSW32 = 6;
 constexpr int kRec = 8192;     // one A'' K-record: 128 rows x 16 fp16 x {hi, lo}
 constexpr int kImg = 4096;     // one 128 x 16 fp16 image inside a record
-constexpr int kStage = 32768;  // one pipeline stage: up to four consecutive K-records
+constexpr int kMaxRps = 4;     // K-records per A ring stage: 1, 2 or 4 (TcParams::rps)
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -380,6 +380,7 @@ struct TcParams {
   int NBB;         // fp16 B tile buffers (1 or 2)
   int nbuf;        // TMEM accumulator buffers (512 / (2 Nt))
   int S;           // A ring stages
+  int rps;         // K-records (8 KiB) per A ring stage
   int tpu;         // tiles per work unit
   int nchunks;     // time chunks per signal (L / (Nt * tpu))
   const int32_t* chunk_sel;  // selected chunks (path sharding) or nullptr = all
@@ -406,7 +407,7 @@ constexpr int kProdWarp = 8, kMmaWarp = 9, kBWarp = 10;
 struct SmemLayout {
   uint32_t bhi[2], blo[2], ast, wt, bars, total;
 };
-__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int NF, int pool_mode) {
+__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int rps, int NF, int pool_mode) {
   SmemLayout l{};
   auto up = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
   uint32_t o = 0;
@@ -423,7 +424,7 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int 
     }
   }
   l.ast = o;
-  o += (uint32_t)S * kStage;
+  o += (uint32_t)S * rps * kRec;
   l.wt = o;  // [2][Nt][NF] taps, or [2][Nt / 32][4][NF] moment coefficients
   o += (uint32_t)(2 * Nt * (pool_mode ? NF / 8 : NF) * 4);
   l.bars = up(o, 8);
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  const SmemLayout lay = smem_layout(p.K16, p.Nt, p.NBB, p.S, NF, p.pool_mode);
+  const SmemLayout lay = smem_layout(p.K16, p.Nt, p.NBB, p.S, p.rps, NF, p.pool_mode);
   const int wfl = p.Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
   uint8_t* Ast = base + lay.ast;
   float* Wt = reinterpret_cast<float*>(base + lay.wt);  // [2][Nt][NF]
@@ -483,7 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int units = p.nsig * p.nsel * p.n_mpart;
-  const int nst = (p.nkc + 3) / 4;  // A'' stages (<= 4 records of 16 K-columns) per M-block
+  const int nst = (p.nkc + p.rps - 1) / p.rps;  // A'' stages (<= rps records of 16 K-columns) per M-block
+  const uint32_t stage_bytes = (uint32_t)(p.rps * kRec);
   // the CTA's tile sequence: unit u = blockIdx.x + i * gridDim.x, tile 0..tpu-1
   const int my_units = (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const int my_tiles = my_units * p.tpu;
@@ -534,9 +536,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int st = 0; st < nst; ++st) {
             if ((int)s == lane) {
               mbar_wait(a_empty + s, ph ^ 1);
-              const uint32_t bytes = (uint32_t)(min(4, p.nkc - 4 * st) * kRec);
+              const uint32_t bytes = (uint32_t)(min(p.rps, p.nkc - p.rps * st) * kRec);
               mbar_expect_tx(a_full + s, bytes);
-              bulk_load(Ast + s * kStage, arec + (size_t)(4 * st) * (kRec / 2), bytes, a_full + s);
+              bulk_load(Ast + s * stage_bytes, arec + (size_t)(p.rps * st) * (kRec / 2), bytes, a_full + s);
             }
             ++j;
             if (++s == (uint32_t)p.S) {
@@ -570,11 +572,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait_t(a_full + s, ph, w_a);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t dst = dA0 + (uint64_t)((s * kStage) >> 4);
+            const uint64_t dst = dA0 + (uint64_t)((s * stage_bytes) >> 4);
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int kc = 4 * st + r;
-              if (kc < p.nkc) {
+            for (int r = 0; r < kMaxRps; ++r) {
+              const int kc = p.rps * st + r;
+              if (r < p.rps && kc < p.nkc) {
                 const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
                 const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
                 const uint32_t acc0 = kc > 0 ? 1u : 0u;
@@ -777,13 +779,14 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, void* base, int rank, const 
 
 int nf_of(int nframes) { return nframes <= 8 ? 8 : nframes <= 16 ? 16 : 32; }
 size_t tc_smem(const AlphaKD& d, int nf) {
-  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, d.tc_S, nf, d.pool_mode).total;
+  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, d.tc_S, d.tc_rps, nf, d.pool_mode).total;
 }
 }  // namespace
 
 // choose the per-alpha tensor-core tiling (called by build_plan): the first of
 // (Nt, B buffers, min stages) = (128, 2, 3), (128, 2, 2), (128, 1, 3), (128, 1, 2),
-// (64, 2, 2), (64, 1, 2), (32, 1, 2) that fits, then as many A'' stages as fit (<= 6)
+// (64, 2, 2), (64, 1, 2), (32, 1, 2) that fits (min stages in units of 4 K-records),
+// then as many A'' ring stages of rps records as fit (<= 24 records)
 void plan_tc(Plan& P) {
   const int NF = nf_of(P.n_frames);
   const size_t budget = 227 * 1024;
@@ -792,16 +795,23 @@ void plan_tc(Plan& P) {
   const char* e_nt = std::getenv("JTFS_TC_NTMAX");
   const char* e_s = std::getenv("JTFS_TC_SMAX");
   const int nt_max = e_nt ? std::max(64, std::atoi(e_nt)) : 128;
-  const int s_max = e_s ? std::max(2, std::min(6, std::atoi(e_s))) : 6;
+  // A ring: stages of rps 8 KiB K-records (JTFS_TC_RPS: measurement-only override,
+  // default 4).  Measured on c3 (round 1): rps = 1 / 2 / 4 -> 2156 / 2459 / 2542
+  // signals/s -- more, smaller L2 -> smem copies in flight starve the MMA more (per-copy
+  // overhead), so stages stay at 32 KiB.  The ring holds at most 24 records (192 KiB).
+  const char* e_r = std::getenv("JTFS_TC_RPS");
+  const int rps = e_r ? (std::atoi(e_r) >= 4 ? 4 : std::atoi(e_r) >= 2 ? 2 : 1) : 4;
+  const int rec_max = e_s ? std::max(2, std::min(6, std::atoi(e_s))) * 4 : 24;
   for (auto& d : P.kd) {
     d.tc_K2 = 2 * d.K;
     d.tc_K16 = (d.tc_K2 + 15) / 16 * 16;
     d.tc_nkc = d.tc_K16 / 16;
     d.tc_nbr = (d.tc_K16 + 255) / 256;
     d.tc_BRk = (d.tc_K16 / d.tc_nbr + 7) / 8 * 8;
+    d.tc_rps = rps;
     bool ok = false;
     // Nt = 128 (MMA N = 256, the efficient shape) first; two B buffers when they fit
-    // with >= min_s2 A stages (JTFS_TC_MINS2: measurement-only override, default 2)
+    // with >= min_s2 x 4 A records (JTFS_TC_MINS2: measurement-only override, default 2)
     const char* e_m2 = std::getenv("JTFS_TC_MINS2");
     const int min_s2 = e_m2 ? std::max(2, std::atoi(e_m2)) : 2;
     const int cand[7][3] = {{128, 2, 3}, {128, 2, min_s2}, {128, 1, 3}, {128, 1, 2}, {64, 2, 2}, {64, 1, 2}, {32, 1, 2}};
@@ -809,9 +819,9 @@ void plan_tc(Plan& P) {
       if (c[0] > nt_max || c[0] > d.L) continue;
       d.tc_Nt = c[0];
       d.tc_NBB = c[1];
-      d.tc_S = c[2];
+      d.tc_S = c[2] * 4 / rps;  // the same minimum ring bytes (c[2] x 32 KiB) in rps-record stages
       if (tc_smem(d, NF) > budget) continue;
-      while (d.tc_S < s_max && tc_smem(d, NF) + tc::kStage <= budget) ++d.tc_S;
+      while ((d.tc_S + 1) * rps <= rec_max && tc_smem(d, NF) + (size_t)rps * tc::kRec <= budget) ++d.tc_S;
       ok = true;
       break;
     }
@@ -895,6 +905,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.NBB = d.tc_NBB;
     p.nbuf = std::min(4, 512 / (2 * d.tc_Nt));  // accumulator buffers of 2 Nt columns (4 barrier pairs)
     p.S = d.tc_S;
+    p.rps = d.tc_rps;
     p.tpu = d.tc_tpu;
     p.nchunks = d.nchunks;
     p.chunk_sel = sel ? sel->d_sel + sel->off[i] : nullptr;
