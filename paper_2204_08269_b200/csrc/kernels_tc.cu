@@ -313,7 +313,8 @@ __device__ __forceinline__ void mom_chunk_i(const uint32_t (&v)[32], float (&S)[
 // ---------------------------------------------------------------------------------
 // KY: one CTA per (signal, tile): max |Y''| over the K' x Nt tile -> s_Y (power of
 // two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y - hi) into the
-// planes [hi | lo][K16][L] (rows >= K' zero), 1 / s_Y into ys[tile].
+// planes [hi | lo][K16][L] (rows >= K' not written: TMA zero-fills them), 1 / s_Y
+// into ys[tile].
 // ---------------------------------------------------------------------------------
 struct KYParams {
   const float* y2;     // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
@@ -352,13 +353,12 @@ __global__ void __launch_bounds__(256) k_ky(KYParams p) {
   __half* hi = p.y16 + (int64_t)b * p.y16_stride + 2 * t0;
   __half* lo = hi + (int64_t)p.K16 * 2 * p.L;
   const int64_t rs = 2 * (int64_t)p.L;  // plane row stride
-  for (int i = threadIdx.x; i < (p.K16 / 2) * p.Nt; i += 256) {
+  // rows [K', K16) are never written: the KD tensor map declares K' rows and TMA
+  // zero-fills the out-of-bounds rows of each B box
+  for (int i = threadIdx.x; i < (p.K2 / 2) * p.Nt; i += 256) {
     const int l = i / p.Nt, c = i % p.Nt;
-    float yr = 0.f, yi = 0.f;
-    if (2 * l < p.K2) {
-      yr = __ldg(Y + (int64_t)(2 * l) * p.L + c) * s;
-      yi = __ldg(Y + (int64_t)(2 * l + 1) * p.L + c) * s;
-    }
+    const float yr = __ldg(Y + (int64_t)(2 * l) * p.L + c) * s;
+    const float yi = __ldg(Y + (int64_t)(2 * l + 1) * p.L + c) * s;
     const __half2 h0 = __floats2half2_rn(yr, yi);   // row 2l
     const float2 f0 = __half22float2(h0);
     const __half2 l0 = __floats2half2_rn(yr - f0.x, yi - f0.y);
@@ -888,7 +888,9 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
       ++launches;
     }
     CUtensorMap tmB;
-    cuuint64_t dims[4] = {(cuuint64_t)(2 * d.L), (cuuint64_t)d.tc_K16, 2, (cuuint64_t)nsig};
+    // K' = 2K rows per plane (the planes are allocated with K16 rows): the box rows
+    // beyond K' are out of bounds and arrive zero-filled (the MMA's K padding)
+    cuuint64_t dims[4] = {(cuuint64_t)(2 * d.L), (cuuint64_t)d.tc_K2, 2, (cuuint64_t)nsig};
     cuuint64_t strides[3] = {(cuuint64_t)d.L * 4, (cuuint64_t)d.tc_K16 * d.L * 4, (cuuint64_t)P.y16_total * 2};
     cuuint32_t box[4] = {64, (cuuint32_t)d.tc_BRk, 1, 1};
     if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 4, dims, strides, box,
