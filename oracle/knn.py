@@ -83,3 +83,37 @@ def knn_regress(F: np.ndarray, theta: np.ndarray, K: int = 40):
     nb = knn_sets(D, K)
     theta_hat = theta[nb].mean(axis=1)
     return nb, theta_hat, theta_hat / theta
+
+
+# ----------------------------------------------------------------------------
+# Isomap (Fig. 3): the manifold embedding built on the same K = 40
+# neighbour graph (Tenenbaum et al. 2000, cited at P:157)
+# ----------------------------------------------------------------------------
+def isomap(F: np.ndarray, K: int = 40, n_components: int = 3):
+    """Isomap of the rows of F, the algorithm the paper applies: "Isomap
+    assembles a geodesic distance matrix by using neighborhood relationships from
+    high-dimensional Euclidean distances", 40 nearest neighbours, three components.
+    Steps (reading R25, the standard algorithm of the cited reference):
+      1. neighbour graph: edge (i, j) of length ||F_i - F_j|| if j in N_K(i) or i in N_K(j)
+         (N_K as in knn_sets);
+      2. geodesic distances G = all-pairs shortest paths on that graph (library routine);
+      3. classical MDS: B = -1/2 H (G o G) H, H = I - 11^T / n;
+      4. embedding = top n_components eigenvectors of B scaled by sqrt(eigenvalue).
+    Returns (embedding [n, c], eigenvalues [c]); raises if the graph is disconnected."""
+    from scipy.sparse.csgraph import shortest_path
+    D = pairwise_sq_dist(F)
+    nb = knn_sets(D, K)
+    n = D.shape[0]
+    W = np.zeros((n, n))
+    for i in range(n):
+        for j in nb[i]:
+            W[i, j] = W[j, i] = np.sqrt(D[i, j])
+    G = shortest_path(W, method="D", directed=False)
+    if not np.all(np.isfinite(G)):
+        raise ValueError("neighbour graph is disconnected")
+    H = np.eye(n) - np.ones((n, n)) / n
+    B = -0.5 * H @ (G * G) @ H
+    w, V = np.linalg.eigh(B)
+    order = np.argsort(w)[::-1][:n_components]
+    w, V = w[order], V[:, order]
+    return V * np.sqrt(np.maximum(w, 0.0)), w

@@ -85,3 +85,54 @@ def test_row_helpers_equal_full_matrix():
     nb = Kn.knn_sets(D, 6)
     for i in rows:
         assert np.array_equal(Kn.knn_row(D[i], i, 6), nb[i])
+
+
+# ---- Isomap (NEXT-3) ----
+def _align(E, R):
+    """Per-component sign alignment of E to R (eigenvector signs are arbitrary)."""
+    s = np.sign(np.sum(E * R, axis=0))
+    s[s == 0] = 1
+    return E * s
+
+
+def test_isomap_of_points_on_a_line_recovers_the_arc_length():
+    # collinear points: every geodesic is the Euclidean distance along the line, so
+    # the first coordinate is the centred position (exact), the others vanish
+    t = np.sort(np.random.default_rng(6).uniform(0, 10, 60))
+    F = np.outer(t, [0.6, 0.8, 0.0])
+    E, w = Kn.isomap(F, K=5, n_components=1)
+    ref = (t - t.mean())[:, None]
+    np.testing.assert_allclose(_align(E, ref), ref, atol=1e-9)
+    np.testing.assert_allclose(w[0], np.sum((t - t.mean()) ** 2), rtol=1e-9)
+
+
+def test_isomap_complete_graph_is_classical_mds():
+    # K = n - 1: geodesics = Euclidean distances; classical MDS recovers a centred
+    # point cloud up to an orthogonal map: equal Gram matrices
+    rng = np.random.default_rng(7)
+    P = rng.standard_normal((30, 3)) * np.array([5.0, 2.0, 0.5])
+    F = P @ np.linalg.qr(rng.standard_normal((3, 3)))[0].T
+    E, w = Kn.isomap(F, K=29, n_components=3)
+    Pc = P - P.mean(0)
+    np.testing.assert_allclose(E @ E.T, Pc @ Pc.T, atol=1e-9)
+    np.testing.assert_allclose(np.sort(w)[::-1], np.sort(np.linalg.eigvalsh(Pc.T @ Pc))[::-1], rtol=1e-9)
+
+
+def test_isomap_unrolls_a_helix_by_arc_length():
+    # a helix is a 1-D manifold curled in 3-D: with a small K the geodesic distance is
+    # the arc length, so the top Isomap coordinate is monotone in the curve parameter
+    t = np.linspace(0, 4 * np.pi, 200)
+    F = np.stack([np.cos(t), np.sin(t), 0.3 * t], axis=1)
+    E, _ = Kn.isomap(F, K=4, n_components=1)
+    c = np.corrcoef(E[:, 0], t)[0, 1]
+    assert abs(c) > 0.999, c
+    # the Euclidean embedding (complete graph) does not unroll it
+    Ee, _ = Kn.isomap(F, K=199, n_components=1)
+    assert abs(np.corrcoef(Ee[:, 0], t)[0, 1]) < abs(c)
+
+
+def test_isomap_disconnected_graph_raises():
+    F = np.concatenate([np.zeros((5, 2)), np.ones((5, 2)) * 100]) + \
+        np.random.default_rng(0).standard_normal((10, 2)) * 0.01
+    with pytest.raises(ValueError):
+        Kn.isomap(F, K=2)
