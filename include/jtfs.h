@@ -317,6 +317,24 @@ JTFS_API jtfs_status jtfs_knn_regress(const float* F, int64_t n, int64_t d, int6
                                       int32_t n_params, int32_t K, int32_t* nbr, double* theta_hat,
                                       double* ratio, void* ws, size_t ws_bytes, void* stream);
 
+/* Isomap of the same feature set (Fig. 3; Tenenbaum et al. 2000, cited at
+ * P:157) on the K-NN graph above: edges (i, j) of length ||F_i - F_j|| for j in N_K(i)
+ * or i in N_K(j); geodesic distances = all-pairs shortest paths (blocked Floyd-Warshall,
+ * fp64); classical MDS B = -1/2 H (G o G) H; the top n_components eigenpairs of B by a
+ * fixed-length subspace iteration with Rayleigh-Ritz (reading R25).  Each eigenvector's
+ * sign is fixed so that its entry of largest magnitude is positive.
+ *   F, n, d, ldf, K  as jtfs_knn_regress (2 <= n <= 16384, 1 <= K < n)
+ *   n_components     1 .. 8 (the paper uses 3)
+ *   emb              device fp64 [n][n_components]: eigenvector * sqrt(max(eigenvalue, 0))
+ *   eigvals          device fp64 [n_components], descending
+ *   ws               device, >= jtfs_isomap_workspace_size(n, K) bytes, 256-byte aligned
+ * SYNCHRONOUS (reads back a connectivity flag): JTFS_ERR_INVALID_ARG if the neighbour
+ * graph is disconnected (outputs then undefined). */
+JTFS_API jtfs_status jtfs_isomap_workspace_size(int64_t n, int32_t K, size_t* bytes);
+JTFS_API jtfs_status jtfs_isomap(const float* F, int64_t n, int64_t d, int64_t ldf, int32_t K,
+                                 int32_t n_components, double* emb, double* eigvals, void* ws, size_t ws_bytes,
+                                 void* stream);
+
 /* Debug taps for kernel-level tests (device outputs, synchronous).
  *   tap 0: X_hat   -> out complex (float2) [B][N_pad]
  *   tap 1: U1      -> out fp32 [B][sum_lambda L1(lambda)]   (rows in lambda order)

@@ -857,6 +857,30 @@ jtfs_status jtfs_knn_regress(const float* F, int64_t n, int64_t d, int64_t ldf, 
   return e != cudaSuccess ? cuda_fail(e, "K-NN kernels") : JTFS_OK;
 }
 
+jtfs_status jtfs_isomap_workspace_size(int64_t n, int32_t K, size_t* bytes) {
+  if (!bytes || n < 0 || K < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  *bytes = jtfs::isomap_workspace_bytes(n, K);
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_isomap(const float* F, int64_t n, int64_t d, int64_t ldf, int32_t K, int32_t n_components,
+                        double* emb, double* eigvals, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 2 || n > 16384) return fail(JTFS_ERR_INVALID_ARG, "need 2 <= n <= 16384");
+  if (d < 1 || ldf < d || d > (int64_t)1 << 30) return fail(JTFS_ERR_INVALID_ARG, "need d >= 1 and ldf >= d");
+  if (K < 1 || K >= n) return fail(JTFS_ERR_INVALID_ARG, "need 1 <= K < n");
+  if (n_components < 1 || n_components > 8 || n_components > n)
+    return fail(JTFS_ERR_INVALID_ARG, "need 1 <= n_components <= min(8, n)");
+  if (!F || !emb || !eigvals || !ws) return fail(JTFS_ERR_INVALID_ARG, "NULL buffer");
+  if (!aligned(ws, 256)) return fail(JTFS_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (ws_bytes < jtfs::isomap_workspace_bytes(n, K)) return fail(JTFS_ERR_WORKSPACE, "workspace too small");
+  int disc = 0;
+  cudaError_t e = jtfs::launch_isomap(F, (int)n, (int)d, ldf, K, n_components, emb, eigvals, ws,
+                                      (cudaStream_t)stream, &disc);
+  if (e != cudaSuccess) return cuda_fail(e, "Isomap kernels");
+  if (disc) return fail(JTFS_ERR_INVALID_ARG, "the K-NN graph is disconnected (infinite geodesic distances)");
+  return JTFS_OK;
+}
+
 jtfs_status jtfs_debug_tap_size(jtfs_plan_t plan, int32_t tap, int64_t B, int64_t* floats) {
   if (!plan || !floats || B < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
   const jtfs::Plan& P = plan->P;

@@ -93,6 +93,9 @@ int launch_u2_map(const Plan& P, const float* y2, int nsig, int path, int rows, 
 size_t knn_workspace_bytes(int64_t n);
 cudaError_t launch_knn(const float* F, int n, int d, int64_t ldf, const double* theta, int P, int K, int32_t* nbr,
                        double* theta_hat, double* ratio, void* ws, cudaStream_t st);
+size_t isomap_workspace_bytes(int64_t n, int K);
+cudaError_t launch_isomap(const float* F, int n, int d, int64_t ldf, int K, int c, double* emb, double* evals,
+                          void* ws, cudaStream_t st, int* disconnected);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
 
 }  // namespace jtfs

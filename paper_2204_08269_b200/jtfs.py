@@ -37,7 +37,7 @@ EXPORTS = [
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
     "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions",
     "jtfs_mulog_mu", "jtfs_mulog_apply", "jtfs_forward_mulog", "jtfs_u2_map_shape", "jtfs_u2_map",
-    "jtfs_knn_workspace_size", "jtfs_knn_regress",
+    "jtfs_knn_workspace_size", "jtfs_knn_regress", "jtfs_isomap_workspace_size", "jtfs_isomap",
 ]
 STAGES = ["KA_pad_fft", "KB_first_order", "KS_phi_avg", "KC_second_order", "KD_joint", "KE_pool_pack"]
 
@@ -105,6 +105,8 @@ _lib.jtfs_u2_map.argtypes = [_P, _P, C.c_int64, C.c_int32, _P, _P, C.c_size_t, _
 _lib.jtfs_knn_workspace_size.argtypes = [C.c_int64, C.POINTER(C.c_size_t)]
 _lib.jtfs_knn_regress.argtypes = [_P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P, _P,
                                   C.c_size_t, _P]
+_lib.jtfs_isomap_workspace_size.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]
+_lib.jtfs_isomap.argtypes = [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, C.c_size_t, _P]
 _lib.jtfs_status_string.argtypes = [C.c_int]
 _lib.jtfs_status_string.restype = C.c_char_p
 _lib.jtfs_last_error.argtypes = []
@@ -438,6 +440,23 @@ def knn_regress(F, theta=None, K: int = 40, stream=None):
     _check(_lib.jtfs_knn_regress(_ptr(F), n, d, F.stride(0), _ptr(theta), P, K, _ptr(nbr), _ptr(hat), _ptr(ratio),
                                  _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_knn_regress")
     return nbr, hat, ratio
+
+
+def isomap(F, K: int = 40, n_components: int = 3, stream=None):
+    """Isomap of feature rows F (float32 CUDA [n, d], row stride may exceed d).
+    Returns (embedding float64 [n, n_components], eigenvalues float64 [n_components]).
+    Synchronous; raises JTFSError if the K-NN graph is disconnected."""
+    import torch
+    assert F.dtype == torch.float32 and F.is_cuda and F.dim() == 2 and F.stride(1) == 1
+    n, d = F.shape
+    sz = C.c_size_t()
+    _check(_lib.jtfs_isomap_workspace_size(n, K, C.byref(sz)), "jtfs_isomap_workspace_size")
+    ws = torch.empty(max(int(sz.value), 1), dtype=torch.uint8, device=F.device)
+    emb = torch.empty(n, n_components, dtype=torch.float64, device=F.device)
+    ev = torch.empty(n_components, dtype=torch.float64, device=F.device)
+    _check(_lib.jtfs_isomap(_ptr(F), n, d, F.stride(0), K, n_components, _ptr(emb), _ptr(ev), _ptr(ws), ws.numel(),
+                            _stream_handle(stream)), "jtfs_isomap")
+    return emb, ev
 
 
 def jtfs_plan(N, J, Q, J_fr, Q_fr, T, F, flags=0) -> Plan:

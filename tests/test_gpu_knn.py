@@ -80,3 +80,51 @@ def test_knn_rejects_bad_args(jt):
         jt.knn_regress(F, None, K=10)
     with pytest.raises(jt.JTFSError):
         jt.knn_regress(F[:1], None, K=1)
+
+
+# ---- Isomap ----
+def _iso(jt, F, K, c):
+    import torch
+    Fd = torch.from_numpy(np.ascontiguousarray(F, dtype=np.float32)).cuda()
+    E, w = jt.isomap(Fd, K, c)
+    return E.cpu().numpy(), w.cpu().numpy()
+
+
+def _align(E, R):
+    s = np.sign(np.sum(E * R, axis=0))
+    s[s == 0] = 1
+    return E * s
+
+
+@pytest.mark.parametrize("n,K", [(500, 10), (130, 7)])
+def test_isomap_vs_oracle_anisotropic_box(jt, n, K):
+    # points of an anisotropic 3-D box (well separated spectrum) rotated into 40 dims
+    rng = np.random.default_rng(n)
+    P = rng.uniform(-1, 1, size=(n, 3)) * np.array([10.0, 4.0, 1.5])
+    R = np.linalg.qr(rng.standard_normal((40, 40)))[0][:, :3]
+    F = (P @ R.T + 0.01 * rng.standard_normal((n, 40))).astype(np.float32)
+    E, w = _iso(jt, F, K, 3)
+    Eo, wo = Kn.isomap(F, K, 3)
+    np.testing.assert_allclose(w, wo, rtol=1e-9)
+    np.testing.assert_allclose(_align(E, Eo), Eo, atol=1e-7 * np.abs(Eo).max())
+    # deterministic, sign convention: largest-magnitude entry of each eigenvector positive
+    E2, _ = _iso(jt, F, K, 3)
+    assert np.array_equal(E, E2)
+    assert np.all(E[np.argmax(np.abs(E), axis=0), range(3)] > 0)
+
+
+def test_isomap_helix_vs_oracle(jt):
+    t = np.linspace(0, 4 * np.pi, 300)
+    F = np.stack([np.cos(t), np.sin(t), 0.3 * t], axis=1).astype(np.float32)
+    E, w = _iso(jt, F, 4, 2)
+    Eo, wo = Kn.isomap(F, 4, 2)
+    np.testing.assert_allclose(w, wo, rtol=1e-9)
+    np.testing.assert_allclose(_align(E, Eo), Eo, atol=1e-7 * np.abs(Eo).max())
+    assert abs(np.corrcoef(E[:, 0], t)[0, 1]) > 0.999
+
+
+def test_isomap_disconnected_graph_is_an_error(jt):
+    rng = np.random.default_rng(0)
+    F = np.concatenate([rng.standard_normal((40, 3)), 1000 + rng.standard_normal((40, 3))]).astype(np.float32)
+    with pytest.raises(jt.JTFSError):
+        _iso(jt, F, 5, 3)

@@ -38,3 +38,28 @@ def test_knn_error_ratios_on_the_chirp_grid_match_fig4():
     nbh = nb.cpu().numpy()
     assert not np.any(nbh == np.arange(len(theta))[:, None])
     np.testing.assert_allclose(hat.cpu().numpy(), theta[nbh].mean(axis=1), rtol=1e-13)
+
+
+def test_isomap_components_align_with_the_three_parameters():
+    # Fig. 3(d): "the dataset of AM/FM signals is represented as a 3-D mesh
+    # where the principal components align independently with f_c, f_m and gamma".
+    # Reading R26: each parameter has its own Isomap component with |Spearman rho| >= 0.8,
+    # and every other (component, parameter) pair has |rho| <= 0.3.
+    import torch
+    from scipy.stats import spearmanr
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test run without a visible CUDA device")
+    from paper_2204_08269_b200 import jtfs as jt
+    theta, X = signals.chirp_grid()
+    plan = jt.Plan(**C2)
+    S = plan.forward(torch.from_numpy(X).cuda())
+    E, w = jt.isomap(S, K=40, n_components=3)
+    E = E.cpu().numpy()
+    assert np.all(np.diff(w.cpu().numpy()) <= 0)
+    rho = np.array([[abs(spearmanr(E[:, k], theta[:, p]).correlation) for p in range(3)] for k in range(3)])
+    best = rho.argmax(axis=0)                       # component of each parameter
+    assert sorted(best) == [0, 1, 2], rho
+    assert np.all(rho[best, range(3)] >= 0.8), rho
+    mask = np.ones((3, 3), bool)
+    mask[best, range(3)] = False
+    assert np.all(rho[mask] <= 0.3), rho

@@ -29,3 +29,13 @@ for k, F in feats.items():
     nb, hat, ratio = jt.knn_regress(F, th, 40)
     res[k] = q(ratio.cpu().numpy())
     print(k, json.dumps(res[k]), flush=True)
+
+# Isomap of the raw records: Spearman correlation of each component with each parameter
+import time
+from scipy.stats import spearmanr
+torch.cuda.synchronize(); t0 = time.perf_counter()
+E, w = jt.isomap(S, 40, 3)
+torch.cuda.synchronize(); print("isomap s", round(time.perf_counter() - t0, 3), "eig", w.cpu().numpy())
+E = E.cpu().numpy()
+for k in range(3):
+    print("component", k, [round(float(spearmanr(E[:, k], theta[:, p]).correlation), 3) for p in range(3)])
