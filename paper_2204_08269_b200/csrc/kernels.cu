@@ -509,11 +509,12 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
     for (int idx = threadIdx.x; idx < p.lam_out * nf; idx += blockDim.x) {
       const int q = idx / nf, m = idx % nf;
       float acc = 0.f;
-      for (int l = 0; l < p.n1; ++l) {
-        int d = ((q << p.k_phiphi) - l) % p.N_fr;
-        if (d < 0) d += p.N_fr;
-        acc = fmaf(__ldg(p.hphiF + d), yphi[l * p.NPT + p.frame0 + m], acc);
-      }
+      // circular tap index d = (q 2^k - l) mod N_fr, q 2^k < N_fr: two wrap-free ranges
+      const int rp = q << p.k_phiphi;
+      const float* ym = yphi + p.frame0 + m;
+      const int l1 = min(p.n1, rp + 1);
+      for (int l = 0; l < l1; ++l) acc = fmaf(__ldg(p.hphiF + (rp - l)), ym[l * p.NPT], acc);
+      for (int l = l1; l < p.n1; ++l) acc = fmaf(__ldg(p.hphiF + (rp - l + p.N_fr)), ym[l * p.NPT], acc);
       outp[idx] = p.mu ? mulog_val(acc, p.mu_eps * __ldg(p.mu + pi)) : acc;
     }
     return;
@@ -531,10 +532,16 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
       const int r = idx / p.NPT, n = idx % p.NPT;
       const int rp = p.rprime[f.rp_off + r] << f.k;
       float2 z = make_float2(0.f, 0.f);
-      for (int l = 0; l < p.n1; ++l) {
-        int d = (rp - l) % p.N_fr;
-        if (d < 0) d += p.N_fr;
-        const float2 hv = __ldg(h + d);
+      // circular tap index d = (r' 2^k - l) mod N_fr, r' 2^k < N_fr: two wrap-free ranges
+      const int l1 = min(p.n1, rp + 1);
+      for (int l = 0; l < l1; ++l) {
+        const float2 hv = __ldg(h + (rp - l));
+        const float yv = ys[l * p.NPT + n];
+        z.x = fmaf(hv.x, yv, z.x);
+        z.y = fmaf(hv.y, yv, z.y);
+      }
+      for (int l = l1; l < p.n1; ++l) {
+        const float2 hv = __ldg(h + (rp - l + p.N_fr));
         const float yv = ys[l * p.NPT + n];
         z.x = fmaf(hv.x, yv, z.x);
         z.y = fmaf(hv.y, yv, z.y);
@@ -545,11 +552,11 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
     for (int idx = threadIdx.x; idx < f.nrows * nf; idx += blockDim.x) {
       const int r = idx / nf, m = idx % nf;
       float acc = 0.f;
-      for (int n = 0; n < p.NPT; ++n) {
-        int d = (p.frame0 + m - n) % p.NPT;
-        if (d < 0) d += p.NPT;
-        acc = fmaf(__ldg(p.gT + d), u2[r * p.NPT + n], acc);
-      }
+      // d = (frame0 + m - n) mod NPT with frame0 + m < NPT: two wrap-free ranges
+      const int base = p.frame0 + m;
+      const float* ur = u2 + r * p.NPT;
+      for (int n = 0; n <= base; ++n) acc = fmaf(__ldg(p.gT + (base - n)), ur[n], acc);
+      for (int n = base + 1; n < p.NPT; ++n) acc = fmaf(__ldg(p.gT + (base - n + p.NPT)), ur[n], acc);
       Pm[idx] = acc;
     }
     __syncthreads();
@@ -558,19 +565,52 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
     const DevAlpha a = p.alphas[P.alpha_slot];
     const float* part = p.part + (int64_t)b * p.part_stride + a.part_off;
     const int64_t cstride = (int64_t)p.Mpad * nf;
-    for (int idx = threadIdx.x; idx < f.nrows * nf; idx += blockDim.x) {
-      const float* src = part + (int64_t)f.row0 * nf + idx;  // (row0 + r) * nf + m
-      float acc = 0.f;
-      int c = 0;
-      for (; c + 8 <= a.nchunks; c += 8) {  // 8 loads in flight, sums in fixed order
-        float v[8];
+    const int nout = f.nrows * nf;
+    if ((nf & 3) == 0) {
+      // 16-byte loads (the block's rows are contiguous in every slice; row0 * nf * 4 and
+      // the slice stride are multiples of 16 B): 4 outputs per thread, 8 slices in flight
+      const int64_t cs4 = cstride / 4;
+      const float4* src4 = reinterpret_cast<const float4*>(part + (int64_t)f.row0 * nf);
+      for (int v = threadIdx.x; v < nout / 4; v += blockDim.x) {
+        const float4* s = src4 + v;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int c = 0;
+        for (; c + 8 <= a.nchunks; c += 8) {  // sums in fixed (slice) order per output
+          float4 x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (c + j) * cstride);
+          for (int j = 0; j < 8; ++j) x[j] = __ldg(s + (c + j) * cs4);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc += v[j];
+          for (int j = 0; j < 8; ++j) {
+            acc.x += x[j].x;
+            acc.y += x[j].y;
+            acc.z += x[j].z;
+            acc.w += x[j].w;
+          }
+        }
+        for (; c < a.nchunks; ++c) {
+          const float4 x = __ldg(s + c * cs4);
+          acc.x += x.x;
+          acc.y += x.y;
+          acc.z += x.z;
+          acc.w += x.w;
+        }
+        reinterpret_cast<float4*>(Pm)[v] = acc;
       }
-      for (; c < a.nchunks; ++c) acc += __ldg(src + c * cstride);
-      Pm[idx] = acc;
+    } else {
+      for (int idx = threadIdx.x; idx < nout; idx += blockDim.x) {
+        const float* src = part + (int64_t)f.row0 * nf + idx;  // (row0 + r) * nf + m
+        float acc = 0.f;
+        int c = 0;
+        for (; c + 8 <= a.nchunks; c += 8) {  // 8 loads in flight, sums in fixed order
+          float v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = __ldg(src + (c + j) * cstride);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc += v[j];
+        }
+        for (; c < a.nchunks; ++c) acc += __ldg(src + c * cstride);
+        Pm[idx] = acc;
+      }
     }
     __syncthreads();
   }
