@@ -68,6 +68,19 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def _kd_traffic():
+    """dram__bytes_read + dram__bytes_write of one alpha-0 KD launch (64 signals) from the
+    committed ncu --set full capture (profiles/kd_traffic.json); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "kd_traffic.json")) as f:
+            k = json.load(f)
+        return {"bytes_per_launch": k["dram_bytes_read"] + k["dram_bytes_write"],
+                "algorithmic_bytes_per_launch": k["algorithmic_bytes_read"] + k["algorithmic_bytes_write"],
+                "launch": k["kernel"], "source": k["source"]}
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -459,7 +472,7 @@ def main():
                          "kernel": "KD stage (k_ky fp16 split + k_kd_tc: tcgen05 kind::f16 lambda contraction "
                                    "+ |.| + phi_T pooling)",
                          "achieved": kd_alg, "peak": f16_peak, "unit": "TFLOP/s",
-                         "frac": (kd_alg / f16_peak) if kd_alg else None, "traffic": None,
+                         "frac": (kd_alg / f16_peak) if kd_alg else None, "traffic": _kd_traffic(),
                          "peak_source": f"dense fp16 = {src} bf16_tflops_sustained (same nominal rate as bf16)",
                          "algorithmic_flops_per_signal": cost["KD_joint"][0],
                          "algorithmic_basis": "canonical FFT-along-lambda count of the exact operator (DESIGN.md 5)",
