@@ -49,6 +49,8 @@ void free_device(jtfs::Plan& P) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(P.device);
+    if (P.kd_side_stream) cudaStreamDestroy((cudaStream_t)P.kd_side_stream);
+    P.kd_side_stream = nullptr;
     for (void* p : P.allocations) cudaFree(p);
     cudaSetDevice(cur);
   }

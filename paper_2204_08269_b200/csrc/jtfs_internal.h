@@ -162,6 +162,10 @@ struct Plan {
   std::vector<void*> allocations;
 
   int mb = 16;                 // signals per micro-batch
+  // a second stream for the KD launches of the slower alphas (kernels_tc.cu), created
+  // with the device tables; fork / join events are created per call
+  void* kd_side_stream = nullptr;
+  int kd_side_from = 1 << 30;  // first active-alpha index launched on the side stream
 
   // ---- profiling (the only mutable state; see jtfs_profile_enable) ----
   bool prof = false;

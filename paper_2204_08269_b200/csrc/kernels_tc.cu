@@ -845,6 +845,20 @@ void plan_tc(Plan& P) {
 
 cudaError_t tc_setup_device(Plan& P) {
   if (P.kd_impl != 1) return cudaSuccess;
+  // The persistent KD launches of the slow alphas (few work units) leave SMs idle; they
+  // run on a second stream, overlapping the tails of the fast alphas' launches.
+  // JTFS_KD_SPLIT (measurement only): first alpha index on the side stream (<= 0: none).
+  {
+    const char* e = std::getenv("JTFS_KD_SPLIT");
+    const int split = e ? std::atoi(e) : 5;
+    if (split > 0 && split < (int)P.kd.size()) {
+      cudaStream_t s = nullptr;
+      cudaError_t es = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (es != cudaSuccess) return es;
+      P.kd_side_stream = (void*)s;
+      P.kd_side_from = split;
+    }
+  }
   const int NF = nf_of(P.n_frames);
   size_t mx = 0;
   for (auto& d : P.kd) mx = std::max(mx, tc_smem(d, NF));
@@ -866,10 +880,22 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   int launches = 0;
+  *err = 0;
+  cudaStream_t main_st = st;
+  cudaStream_t side = (cudaStream_t)P.kd_side_stream;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (side) {
+    // per-call events: concurrent forwards on one plan stay correctly paired
+    cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+    cudaEventRecord(ev_fork, main_st);
+    cudaStreamWaitEvent(side, ev_fork, 0);
+  }
   for (size_t i = 0; i < P.kd.size(); ++i) {
     const auto& d = P.kd[i];
     const int nsel = sel ? sel->cnt[i] : d.nchunks;
     if (nsel == 0) continue;
+    st = (side && (int)i >= P.kd_side_from) ? side : main_st;  // KY + KD of this alpha
     // ---- KY: fp16 split of the Y'' tiles ----
     {
       tc::KYParams q{};
@@ -896,7 +922,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 4, dims, strides, box,
                 CU_TENSOR_MAP_SWIZZLE_128B)) {
       *err = 1;
-      return launches;
+      break;  // the join below still orders the side stream before the caller's
     }
     tc::TcParams p{};
     p.K16 = d.tc_K16;
@@ -960,7 +986,12 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
                    h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3);
     }
   }
-  *err = 0;
+  if (side) {
+    cudaEventRecord(ev_join, side);
+    cudaStreamWaitEvent(main_st, ev_join, 0);
+    cudaEventDestroy(ev_fork);  // released once the recorded work has completed
+    cudaEventDestroy(ev_join);
+  }
   return launches;
 }
 
