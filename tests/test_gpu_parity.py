@@ -193,3 +193,32 @@ def test_edge_cases(jt):
     ws = torch.empty(plan.workspace_size(1), dtype=torch.uint8, device="cuda")
     st = lib.jtfs_forward(plan.handle, xb.data_ptr(), 1, out.data_ptr(), ws.data_ptr(), 64, None)
     assert st == jt.JTFS_ERR_WORKSPACE
+
+
+P42 = dict(N=2 ** 16, J=13, Q=16, J_fr=6, T=2 ** 11, F=4)   # Sec. 4.2 preset: 44 x 32 per path
+
+
+def test_paper_preset_sampled_paths(jt):
+    # the paper's convnet setting (32 frames: the NF = 32 tensor-core KD variant); oracle on a
+    # sample of paths of one note, the S0 / S1 rows in full
+    prm = O.Params(**P42)
+    X = signals.notes(2, seed0=2000)
+    plan, out = _run(jt, P42, X)
+    s = O.schedule(prm)
+    assert (s.lam_out, s.n_frames) == (44, 32)
+    P = len(s.paths)
+    sample = sorted({0, 7, 63, 64, P // 2, P - 20, P - 9, P - 8, P - 2, P - 1})
+    O.set_workers(8)
+    _check_signal(plan, out[1], X[1].astype(np.float64), prm, paths=sample)
+
+
+def test_kd_tensor_core_matches_simt_paper_preset(jt, monkeypatch):
+    import torch
+    X = signals.notes(2, seed0=91)
+    x = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    monkeypatch.setenv("JTFS_KD", "simt")
+    a = jt.Plan(**P42).forward(x).cpu().numpy().astype(np.float64)
+    monkeypatch.setenv("JTFS_KD", "tc")
+    b = jt.Plan(**P42).forward(x).cpu().numpy().astype(np.float64)
+    for i in range(len(X)):
+        assert np.linalg.norm(a[i] - b[i]) <= 1e-5 * np.linalg.norm(a[i])
