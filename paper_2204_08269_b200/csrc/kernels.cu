@@ -14,6 +14,8 @@
 // the exact identity IDFT_L(X)[n d] = (1/d) IDFT_{L/d}(fold X)[n].
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 #include "fft.cuh"
 #include "jtfs_internal.h"
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
 // ---------------------------------------------------------------------------------
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
 __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restrict__ tmp,
-                                               const typename P::CT* __restrict__ Wtab) {
+                                               const typename P::CT* __restrict__ Wtab, int rho0) {
   using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
   constexpr int LS = pad_row(La), EPT = G * La / NT;
@@ -254,9 +256,9 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
     for (int t = threadIdx.x; t < Lb; t += NT) Whi[t] = __ldg(Wtab + tw_offset(LOG2B) + t);
   }
   constexpr int CPB = Lb / G;  // column groups per big row
-  const int rho = blockIdx.x / CPB;
+  const int rho = rho0 + (int)(blockIdx.x / CPB);  // rows of this launch's group
   const int nb0 = (blockIdx.x % CPB) * G;
-  CT* out = tmp + (int64_t)rho * L;
+  CT* out = tmp + (int64_t)(rho - rho0) * L;
   // column g of this block = big-row column nb0 + g; consecutive threads take
   // consecutive columns (coalesced gathers and scatters), first / last pass fused
   auto ld = [&](int g, int na) -> CT { return prob.load(rho, na * Lb + nb0 + g); };
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
 
 template <int LOG2A, int LOG2B, int G, int NT, int DIR, class P>
 __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __restrict__ tmp,
-                                               const typename P::CT* __restrict__ Wtab) {
+                                               const typename P::CT* __restrict__ Wtab, int rho0) {
   using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
   constexpr int LS = pad_row(Lb), EPT = G * Lb / NT;
@@ -279,9 +281,9 @@ __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __r
   CT* Ws = smem + G * LS;
   stage_twiddles<LOG2B, NT>(Ws, Wtab + tw_offset(LOG2B));
   constexpr int RPB = La / G;
-  const int rho = blockIdx.x / RPB;
+  const int rho = rho0 + (int)(blockIdx.x / RPB);
   const int ka0 = (blockIdx.x % RPB) * G;
-  const CT* in = tmp + (int64_t)rho * L;
+  const CT* in = tmp + (int64_t)(rho - rho0) * L;
   // rows (ka0 + g) of the intermediate are contiguous: the first pass (row-major
   // threads) is fused with the loads; the last pass (column-major threads: consecutive
   // ka, i.e. consecutive output bins ka + La kb) with the stores
@@ -774,8 +776,22 @@ void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, con
                          227 * 1024);
     attr = true;
   }
-  k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA><<<nbig * (Lb / GA), NT, sma, st>>>(pa, tmp, W);
-  k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB><<<nbig * (La / GB), NT, smb, st>>>(pb, tmp, W);
+  // optional row groups whose intermediate stays L2-resident between the two passes
+  // (JTFS_FFT4_GROUP_MB, measurement only; 0 = one group, the default).  Measured on c3
+  // (round 1): 32 / 64 / 96 MiB groups made KB 16.5 -> 20.3 / 18.5 / 18.4 ms per step --
+  // the passes are not HBM-bound (pass A: issue 62 %, smem 53 %), so the extra launches
+  // and tails cost more than the DRAM round trip of the intermediate.
+  static const int group_mb = [] {
+    const char* e = std::getenv("JTFS_FFT4_GROUP_MB");
+    return e ? std::atoi(e) : 0;
+  }();
+  int grp = nbig;
+  if (group_mb > 0) grp = std::max(1, (int)(((int64_t)group_mb << 20) / ((int64_t)La * Lb * (int64_t)sizeof(CT))));
+  for (int r0 = 0; r0 < nbig; r0 += grp) {
+    const int nr = std::min(grp, nbig - r0);
+    k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA><<<nr * (Lb / GA), NT, sma, st>>>(pa, tmp, W, r0);
+    k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB><<<nr * (La / GB), NT, smb, st>>>(pb, tmp, W, r0);
+  }
 }
 
 template <class F>
