@@ -487,6 +487,8 @@ def main():
             "stages_ms": {k: round(v[0], 3) for k, v in prof.items()},
             "stage_share": stage_share,
             "kd_ms_per_alpha": [round(v, 3) for v in kd_alpha_ms],
+            "kd_ms_per_alpha_note": "summed over the timed steps; alphas >= 5 run on a second stream "
+                                    "concurrently with the fast alphas, so their times include waiting for SMs",
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(1)
