@@ -222,3 +222,27 @@ def test_kd_tensor_core_matches_simt_paper_preset(jt, monkeypatch):
     b = jt.Plan(**P42).forward(x).cpu().numpy().astype(np.float64)
     for i in range(len(X)):
         assert np.linalg.norm(a[i] - b[i]) <= 1e-5 * np.linalg.norm(a[i])
+
+
+def test_forward_is_cuda_graph_capturable(jt):
+    # jtfs_forward only enqueues work (the KD side stream joins through events), so a
+    # CUDA graph capture replays the same bytes
+    import torch
+    kw = dict(N=2 ** 13, J=8, Q=16, J_fr=4, T=2 ** 13, F=16, average_fr=False)
+    plan = jt.Plan(**kw)
+    x = torch.from_numpy(signals.notes(5, N=2 ** 13, seed0=5)).cuda()
+    out = torch.empty(5, plan.floats_per_signal, device="cuda")
+    plan.forward(x, out)
+    ref = out.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.forward(x, out)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.forward(x, out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
