@@ -84,11 +84,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// wait + accumulate the waited cycles into acc (instrumentation)
+// wait (+ accumulate the waited cycles into acc when instrumented: JTFS_TC_PROF selects
+// the PROF = true kernel instantiation; the clock reads are compiled out otherwise)
+template <bool PROF>
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long long& acc) {
-  const long long t0 = clock64();
-  mbar_wait(bar, parity);
-  acc += clock64() - t0;
+  if constexpr (PROF) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+template <bool PROF>
+__device__ __forceinline__ long long clk() {
+  if constexpr (PROF) return clock64();
+  return 0;
 }
 
 // ---- TMA ----
@@ -433,7 +444,7 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int 
   return l;
 }
 
-template <int NF, int MAXSLOT>
+template <int NF, int MAXSLOT, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_kd_tc(const __grid_constant__ CUtensorMap tmB, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -553,23 +564,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== MMA issuer (warp-wide loop, one elected lane issues) =====================
     uint32_t s = 0, ph = 0, cnt = 0;
     long long w_b = 0, w_acc = 0, w_a = 0;
-    const long long t_start = clock64();
+    const long long t_start = clk<PROF>();
     const uint32_t idesc = idesc_f16(2 * p.Nt);  // N = 2 Nt: (re, im) interleaved per time column
     const uint32_t colstride = (uint32_t)(p.K16 * 128);
     const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 256, kLayoutSW32);
     for (int gt = 0; gt < my_tiles; ++gt) {
       const int bi = gt % p.NBB;
-      mbar_wait_t(b_full + bi, (uint32_t)(gt / p.NBB) & 1u, w_b);
+      mbar_wait_t<PROF>(b_full + bi, (uint32_t)(gt / p.NBB) & 1u, w_b);
       tc_fence_after();
       const uint64_t dBh = sdesc(smem_u32(base + lay.bhi[bi]), colstride, 1024, kLayoutSW128);
       const uint64_t dBl = sdesc(smem_u32(base + lay.blo[bi]), colstride, 1024, kLayoutSW128);
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
         const uint32_t ab = cnt % (uint32_t)p.nbuf, use = cnt / (uint32_t)p.nbuf;
-        mbar_wait_t(acc_empty + ab, (use + 1) & 1, w_acc);
+        mbar_wait_t<PROF>(acc_empty + ab, (use + 1) & 1, w_acc);
         tc_fence_after();
         const uint32_t dd = tmem_base + ab * 2u * (uint32_t)p.Nt;
         for (int st = 0; st < nst; ++st) {
-          mbar_wait_t(a_full + s, ph, w_a);
+          mbar_wait_t<PROF>(a_full + s, ph, w_a);
           tc_fence_after();
           if (elect_one()) {
             const uint64_t dst = dA0 + (uint64_t)((s * stage_bytes) >> 4);
@@ -599,8 +610,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) mma_commit(b_empty + bi);
       __syncwarp();
     }
-    if (p.prof && lane == 0) {
-      atomicAdd(p.prof + 0, (unsigned long long)(clock64() - t_start));
+    if (PROF && p.prof && lane == 0) {
+      atomicAdd(p.prof + 0, (unsigned long long)(clk<PROF>() - t_start));
       atomicAdd(p.prof + 1, (unsigned long long)w_b);
       atomicAdd(p.prof + 2, (unsigned long long)w_acc);
       atomicAdd(p.prof + 3, (unsigned long long)w_a);
@@ -611,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;      // TMEM lane quarter (warp_id % 4)
     const int cbeg = eset * (p.Nt / 2);
     long long e_w = 0, e_acc = 0, e_math = 0;
-    const long long e_start = clock64();
+    const long long e_start = clk<PROF>();
     uint32_t cnt = 0;
     float2 accr[MAXSLOT][NF / 2];  // pooled partials of my rows (one per M-block of the part)
     for (int gt = 0; gt < my_tiles; ++gt) {
@@ -628,14 +639,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int m = 0; m < NF / 2; ++m) accr[k][m] = make_float2(0.f, 0.f);
       }
       const int wi = gt & 1;
-      mbar_wait_t(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
+      mbar_wait_t<PROF>(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
       const float inv = __ldg(p.ys + (int64_t)b * p.ys_stride + chunk * p.tpu + tile);
       const float* wt = Wt + wi * wfl + cbeg * NF;
 #pragma unroll 1
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
         const uint32_t ab = cnt % (uint32_t)p.nbuf;
-        mbar_wait_t(acc_full + ab, (cnt / (uint32_t)p.nbuf) & 1u, e_acc);
-        const long long tm0 = clock64();
+        mbar_wait_t<PROF>(acc_full + ab, (cnt / (uint32_t)p.nbuf) & 1u, e_acc);
+        const long long tm0 = clk<PROF>();
         tc_fence_after();
         // accumulator columns 2t / 2t+1 = Re / Im of time column t; this set's time
         // columns [cbeg, cbeg + Nt/2) start at TMEM column 2 cbeg
@@ -693,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_chunk_i<NF>(v, wt + c0 * NF, part);
           }
         }
-        e_math += clock64() - tm0;
+        e_math += clk<PROF>() - tm0;
         // warp-uniform branch to the M-block's slot (a predicated loop over all
         // MAXSLOT slots would issue MAXSLOT x NF FMAs)
         switch (mb) {
@@ -730,8 +741,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (p.prof && lane == 0) {
-      atomicAdd(p.prof + 4, (unsigned long long)(clock64() - e_start));
+    if (PROF && p.prof && lane == 0) {
+      atomicAdd(p.prof + 4, (unsigned long long)(clk<PROF>() - e_start));
       atomicAdd(p.prof + 5, (unsigned long long)e_w);
       atomicAdd(p.prof + 6, (unsigned long long)e_acc);
       atomicAdd(p.prof + 7, (unsigned long long)e_math);
@@ -863,10 +874,12 @@ cudaError_t tc_setup_device(Plan& P) {
   size_t mx = 0;
   for (auto& d : P.kd) mx = std::max(mx, tc_smem(d, NF));
   cudaError_t e = cudaSuccess;
-  if (NF == 8) e = cudaFuncSetAttribute(tc::k_kd_tc<8, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  else if (NF == 16)
-    e = cudaFuncSetAttribute(tc::k_kd_tc<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-  else e = cudaFuncSetAttribute(tc::k_kd_tc<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  auto set = [&](auto kern) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+  };
+  if (NF == 8) { set(tc::k_kd_tc<8, 9, false>); set(tc::k_kd_tc<8, 9, true>); }
+  else if (NF == 16) { set(tc::k_kd_tc<16, 4, false>); set(tc::k_kd_tc<16, 4, true>); }
+  else { set(tc::k_kd_tc<32, 2, false>); set(tc::k_kd_tc<32, 2, true>); }
   return e;
 }
 
@@ -969,9 +982,15 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
       cudaEventRecord(e0, st);
       P.prof_kd[i].push_back({(void*)e0, (void*)e1});
     }
-    if (NF == 8) tc::k_kd_tc<8, 9><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-    else if (NF == 16) tc::k_kd_tc<16, 4><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-    else tc::k_kd_tc<32, 2><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+    if (do_prof) {
+      if (NF == 8) tc::k_kd_tc<8, 9, true><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+      else if (NF == 16) tc::k_kd_tc<16, 4, true><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+      else tc::k_kd_tc<32, 2, true><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+    } else {
+      if (NF == 8) tc::k_kd_tc<8, 9, false><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+      else if (NF == 16) tc::k_kd_tc<16, 4, false><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+      else tc::k_kd_tc<32, 2, false><<<grid, tc::kThreads, sm, st>>>(tmB, p);
+    }
     ++launches;
     if (P.prof) cudaEventRecord(e1, st);
     if (do_prof) {
