@@ -81,6 +81,15 @@ def _kd_traffic():
         return None
 
 
+def _path_roofline(signals_per_s_per_gpu, clocks):
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 128 * 2 * mhz * 1e6 / 1e12  # FP32 FMA lanes x 2 flop x clock (TFLOP/s)
+    ach = 21.5e9 * signals_per_s_per_gpu / 1e12
+    return {"basis": "SURVEY 8(d) canonical 21.5 GFLOP per c3 signal", "achieved_tflops": round(ach, 2),
+            "fp32_simt_peak_tflops": round(peak, 2), "clock_mhz": mhz, "frac": round(ach / peak, 4),
+            "note": "the contraction runs on the tensor cores, so the path can exceed the SIMT roofline"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -482,6 +491,10 @@ def main():
                          "executed_basis": "3 fp16 products (hi.hi, hi.lo, lo.hi) x re/im x 2 Mpad K16 L per alpha"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
                     "d2h_bytes_per_step": int(oh.numel() * 4)},
+            # SURVEY §8(d) report item 2: the whole path against the FP32 SIMT roofline with
+            # the survey's canonical count (21.5 GFLOP per c3 signal: per-alpha cheaper of the
+            # direct / FFT-along-lambda forms + first order), at the measured median SM clock
+            "path_roofline": _path_roofline(value / max(world, 1), clocks),
             "gpu_launches": launches,
             "clocks": clocks,
             "stages_ms": {k: round(v[0], 3) for k, v in prof.items()},
