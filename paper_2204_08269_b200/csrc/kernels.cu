@@ -30,9 +30,9 @@ namespace dev {
 __device__ __forceinline__ float2 fold_value(const float2* __restrict__ src, const FoldRow& d,
                                              const float* __restrict__ bandvals, int i, int L) {
   // first alias t0 = (i - m0) mod L handled without a loop (the common case has at
-  // most one alias, so the loads of several bins can be in flight together)
-  int t = (i - d.m0) % L;
-  if (t < 0) t += L;
+  // most one alias, so the loads of several bins can be in flight together); L is a
+  // power of two (every FFT length), so the residue is a mask, not a division
+  int t = (i - d.m0) & (L - 1);
   float2 acc = make_float2(0.f, 0.f);
   if (t < d.len) {
     int p = d.m0 + t;
