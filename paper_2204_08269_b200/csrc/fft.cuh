@@ -28,9 +28,42 @@ template <class CT>
 __device__ __forceinline__ CT cadd(CT a, CT b) { return CxT<CT>::make(a.x + b.x, a.y + b.y); }
 template <class CT>
 __device__ __forceinline__ CT csub(CT a, CT b) { return CxT<CT>::make(a.x - b.x, a.y - b.y); }
+// fp32: one packed FP32x2 instruction (FADD2) per complex add / subtract -- the compiler
+// does not pair float2 adds by itself; each lane rounds exactly like add.rn.f32
+template <>
+__device__ __forceinline__ float2 cadd<float2>(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+template <>
+__device__ __forceinline__ float2 csub<float2>(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 template <class CT>
 __device__ __forceinline__ CT cmul(CT a, CT b) {
   return CxT<CT>::make(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// fp32: a b = a b.x + (a.y, a.x) (-b.y, b.y) as FMUL2 + FFMA2 -- ptxas folds the lane
+// swap, the one-lane negation and the broadcasts into operand modifiers (2 instructions
+// instead of 4; each lane is one rounded product + one fused multiply-add)
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+template <>
+__device__ __forceinline__ float2 cmul<float2>(float2 a, float2 b) {
+  unsigned long long t, r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk2(a.y, a.x)), "l"(pk2(-b.y, b.y)));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.x)), "l"(t));
+  return *reinterpret_cast<float2*>(&r);
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 
@@ -64,7 +97,7 @@ __device__ __forceinline__ CT rot16(CT a, int j) {
   if (j == 4) return DIR < 0 ? CxT<CT>::make(a.y, -a.x) : CxT<CT>::make(-a.y, a.x);
   const R c = (R)c16(j);
   const R s = (R)(DIR * c16(j < 4 ? 4 - j : j - 4));
-  return CxT<CT>::make(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+  return cmul(a, CxT<CT>::make(c, s));
 }
 
 // Shared-memory index padding: one pad element after every 16 (breaks the bank

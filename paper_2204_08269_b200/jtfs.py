@@ -13,7 +13,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjtfs.so")
+# JTFS_LIB: path of an alternative in-tree build (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("JTFS_LIB") or os.path.join(_HERE, "libjtfs.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2204_08269_b200.build` "
