@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
                                                const typename P::CT* __restrict__ Wtab, int rho0) {
   using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
-  constexpr int LS = pad_row(La), EPT = G * La / NT;
+  constexpr int LS = pad_row(La);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* smem = reinterpret_cast<CT*>(smem_raw);
   CT* Ws = smem + G * LS;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __r
                                                const typename P::CT* __restrict__ Wtab, int rho0) {
   using CT = typename P::CT;
   constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
-  constexpr int LS = pad_row(Lb), EPT = G * Lb / NT;
+  constexpr int LS = pad_row(Lb);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CT* smem = reinterpret_cast<CT*>(smem_raw);
   CT* Ws = smem + G * LS;

@@ -103,15 +103,6 @@ __device__ __forceinline__ long long clk() {
 }
 
 // ---- TMA ----
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2, int c3) {
   asm volatile(
@@ -145,14 +136,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -166,10 +149,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // ties the loaded registers to a point after tcgen05.wait::ld (volatile asm order), so
 // the compiler cannot hoist their uses above the wait
-__device__ __forceinline__ void reg_fence16(uint32_t (&v)[16]) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(v[i]));
-}
 __device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(v[i]));
@@ -230,66 +209,6 @@ __device__ __forceinline__ bool elect_one() {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-
-// epilogue of 16 time columns of one M-block: |Z| from the lane's re / im
-// accumulators (packed FP32x2 squares), phi_T pooling into the NF frame partials
-__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
-  unsigned long long r;
-  const unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
-  const unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ua), "l"(ub));
-  return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  const unsigned long long ua = *reinterpret_cast<unsigned long long*>(&a);
-  const unsigned long long ub = *reinterpret_cast<unsigned long long*>(&b);
-  const unsigned long long uc = *reinterpret_cast<unsigned long long*>(&c);
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(ua), "l"(ub), "l"(uc));
-  return *reinterpret_cast<float2*>(&r);
-}
-template <int NF>
-__device__ __forceinline__ void epi_chunk(const uint32_t (&vr)[16], const uint32_t (&vi)[16], const float* wt,
-                                          float2 (&part)[NF / 2]) {
-#pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    const float2 re = make_float2(__uint_as_float(vr[j]), __uint_as_float(vr[j + 1]));
-    const float2 im = make_float2(__uint_as_float(vi[j]), __uint_as_float(vi[j + 1]));
-    const float2 sq = ffma2v(im, im, fmul2(re, re));
-    const float mag[2] = {sqrt_fast(sq.x), sqrt_fast(sq.y)};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float4* w4 = reinterpret_cast<const float4*>(wt + (j + h) * NF);
-#pragma unroll
-      for (int m4 = 0; m4 < NF / 4; ++m4) {
-        const float4 w = w4[m4];
-        part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mag[h], part[2 * m4 + 0]);
-        part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mag[h], part[2 * m4 + 1]);
-      }
-    }
-  }
-}
-
-// moment form of the phi_T pooling over 16 columns J0..J0+15 of a 32-column
-// block: S_k += |Z_j| u_j^k, u_j = (j - 15.5) / 16 (exact in fp32), k = 0..3
-template <int J0>
-__device__ __forceinline__ void mom_chunk(const uint32_t (&vr)[16], const uint32_t (&vi)[16], float (&S)[4]) {
-#pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    const float2 re = make_float2(__uint_as_float(vr[j]), __uint_as_float(vr[j + 1]));
-    const float2 im = make_float2(__uint_as_float(vi[j]), __uint_as_float(vi[j + 1]));
-    const float2 sq = ffma2v(im, im, fmul2(re, re));
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float mag = sqrt_fast(h ? sq.y : sq.x);
-      const float u = ((float)(J0 + j + h) - 15.5f) * 0.0625f;
-      S[0] += mag;
-      S[1] = fmaf(mag, u, S[1]);
-      S[2] = fmaf(mag, u * u, S[2]);
-      S[3] = fmaf(mag, u * u * u, S[3]);
-    }
-  }
-}
 
 // interleaved (re, im) accumulator columns: 16 time columns per 32 TMEM columns
 template <int NF>
