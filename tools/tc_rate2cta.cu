@@ -15,6 +15,9 @@
 // rate; with a 2-stage bulk-copy A ring, cta_group::1 reaches 94 % but cta_group::2 only
 // 42 %: the peer's copies reach the leader's barrier through a relay arrive, whose latency
 // a 2-stage ring cannot hide -- a KD port needs a deeper ring (or TMA .cta_group::2 loads).
+//   mode 3: cta_group::1, 6 x N = 128 per K chunk into two accumulators (the layout a
+//           spin-pair factorisation needs): 72 % without / 67 % with the ring -- each
+//           N = 128 MMA reads 8 KB of smem per 64 cycles, the full port.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -o tools/tc_rate2cta tools/tc_rate2cta.cu && tools/tc_rate2cta
 #include <cuda_runtime.h>
 
@@ -51,6 +54,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   __shared__ uint64_t bar, afull[2], gbar[2], lfull[2];
   __shared__ uint32_t tslot;
   const uint32_t rank = MODE == 2 ? cta_rank() : 0;
+  constexpr int NN = MODE == 3 ? 128 : 256;  // MMA N
   // A images (64 KB) = 1 + rank, B images (hi at 64 KB, lo at 128 KB) = 1 + 2 rank
   const uint32_t av = rank ? 0x40004000u : 0x3c003c00u;   // fp16 2.0 / 1.0
   const uint32_t bv = rank ? 0x42004200u : 0x3c003c00u;   // fp16 3.0 / 1.0
@@ -84,7 +88,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   long long t0 = clock64();
   if (threadIdx.x < 32 && rank == 0) {
     const int M = MODE == 2 ? 256 : 128;
-    const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    const uint32_t idesc = (1u << 4) | (1u << 16) | ((uint32_t)(NN >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     const uint32_t a0 = smem_u32(base), bh0 = smem_u32(base + 65536), bl0 = smem_u32(base + 131072);
     // B image per CTA: K16 x (N per CTA) MN-major SW128: 64-column groups of nkc*16 rows x 128 B
     const uint32_t colstride = (uint32_t)(nkc * 16 * 128);
@@ -104,6 +108,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
         const uint64_t da = sdesc(rec, 16, 256, 6), dal = sdesc(rec + 4096, 16, 256, 6);
         const uint64_t bh = sdesc(bh0 + kc * 2048, colstride, 1024, 2), bl = sdesc(bl0 + kc * 2048, colstride, 1024, 2);
         const uint32_t acc = c > 0;
+#define MMA3(D, A, B, ACC)                                                                                    \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" :: \
+                   "r"(D), "l"(A), "l"(B), "r"(idesc), "r"(ACC))
         if (MODE == 2) {
 #define MMA2(A, B, ACC)                                                                                       \
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" :: \
@@ -111,6 +118,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
           MMA2(da, bh, acc);
           MMA2(da, bl, 1u);
           MMA2(dal, bh, 1u);
+        } else if (MODE == 3) {
+          // two N = 128 accumulators (columns [0,128) and [128,256)), A images of 4 KB each
+          MMA3(tmem, da, bh, acc);
+          MMA3(tmem, da, bl, 1u);
+          MMA3(tmem, dal, bh, 1u);
+          MMA3(tmem + 128, sdesc(rec + 8192 * 0 + 2048, 16, 256, 6), bh, acc);
+          MMA3(tmem + 128, sdesc(rec + 2048, 16, 256, 6), bl, 1u);
+          MMA3(tmem + 128, sdesc(rec + 4096 + 2048, 16, 256, 6), bh, 1u);
         } else {
 #define MMA1(A, B, ACC)                                                                                       \
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" :: \
@@ -199,17 +214,19 @@ int main() {
   cudaMalloc(&chk, 16 * 4);
   cudaFuncSetAttribute(k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   cudaFuncSetAttribute(k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+  cudaFuncSetAttribute(k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   uint8_t* gsrc;
   cudaMalloc(&gsrc, 64 * 32768 + 65536);
   cudaMemset(gsrc, 0, 64 * 32768 + 65536);
   for (int ring = 0; ring < 2; ++ring)
   for (int nkc : {3, 7}) {
-    for (int mode = 1; mode <= 2; ++mode) {
+    for (int mode = 1; mode <= 3; ++mode) {
       for (int total : {100, 2400}) {
         if (ring && total == 100) continue;
         cudaMemset(chk, 0, 64);
         if (mode == 1) k<1><<<148, 128, 200000>>>(total, nkc, d, chk, gsrc, ring);
-        else k<2><<<148, 128, 200000>>>(total, nkc, d, chk, gsrc, ring);
+        else if (mode == 2) k<2><<<148, 128, 200000>>>(total, nkc, d, chk, gsrc, ring);
+        else k<3><<<148, 128, 200000>>>(total, nkc, d, chk, gsrc, ring);
         cudaError_t e = cudaDeviceSynchronize();
         const int nrec = mode == 2 ? 74 : 148;
         long long h[148];
@@ -220,7 +237,7 @@ int main() {
         for (int i = 0; i < nrec; ++i) avg += h[i];
         avg /= nrec;
         printf("ring %d mode %d (%s) nkc %d chunks %d: %s  %.1f cycles per K chunk (ideal 384) -> %.0f%%\n", ring,
-               mode, mode == 1 ? "cta_group::1 M=128" : "cta_group::2 M=256", nkc, total, cudaGetErrorString(e),
+               mode, mode == 1 ? "cta_group::1 M=128 3xN=256" : mode == 2 ? "cta_group::2 M=256 3xN=256" : "cta_group::1 M=128 6xN=128", nkc, total, cudaGetErrorString(e),
                avg / total, 100.0 * 384.0 * total / avg);
         if (total == 100)
           printf("   check (48 n = %d): cta0 lane0 col0 %.0f col128 %.0f | cta1 lane0 col0 %.0f col128 %.0f\n",
