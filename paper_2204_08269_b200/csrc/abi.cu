@@ -147,7 +147,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
 }
 
 struct WsPtrs {
-  float2 *xhat, *tmp, *u1hat;
+  float2 *xhat, *tmp, *tmp2, *u1hat;
   float *u1, *yphi, *y2, *ys, *part;
   uint16_t* y16;
   int32_t* sel;
@@ -160,6 +160,7 @@ WsPtrs carve(const jtfs::Plan& P, void* ws, int64_t mb) {
   WsPtrs w{};
   w.xhat = (float2*)c; c += L.xhat;
   w.tmp = (float2*)c; c += L.tmp;
+  w.tmp2 = (float2*)c; c += L.tmp2;
   w.u1 = (float*)c; c += L.u1;
   w.u1hat = (float2*)c; c += L.u1hat;
   w.yphi = (float*)c; c += L.yphi;
@@ -230,7 +231,7 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   layout_of(P, &lay);
   { StageScope s(P, 0, st); s.done(launch_pad_fft(P, x, nb, w.xhat, w.tmp, st)); }
   if (upto_stage == 0) return "";
-  { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st)); }
+  { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st, w.tmp2)); }
   {
     StageScope s(P, 2, st);
     s.done(launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, out, lay.floats_per_signal, lay.off_s0, lay.off_s1,
@@ -526,7 +527,7 @@ jtfs_status jtfs_u2_map(jtfs_plan_t plan, const float* x, int64_t B, int32_t pat
   for (int64_t b0 = 0; b0 < B; b0 += mb) {
     const int nb = (int)std::min<int64_t>(mb, B - b0);
     jtfs::launch_pad_fft(P, x + b0 * P.N, nb, w.xhat, w.tmp, st);
-    jtfs::launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st);
+    jtfs::launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st, w.tmp2);
     jtfs::launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st);
     jtfs::launch_u2_map(P, w.y2, nb, path, rows, cols, out + b0 * (int64_t)rows * cols, st);
   }
@@ -711,7 +712,7 @@ jtfs_status jtfs_scattering1d(jtfs_plan_t plan, const float* x, int64_t B, float
     const float* xb = x + b0 * P.N;
     float* ob = out + b0 * lay.floats_per_signal;
     { StageScope sc(P, 0, st); sc.done(jtfs::launch_pad_fft(P, xb, nb, w.xhat, w.tmp, st)); }
-    { StageScope sc(P, 1, st); sc.done(jtfs::launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st)); }
+    { StageScope sc(P, 1, st); sc.done(jtfs::launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, false, st, w.tmp2)); }
     {
       StageScope sc(P, 2, st);
       sc.done(jtfs::launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, ob, lay.floats_per_signal, lay.off_s0,

@@ -180,7 +180,7 @@ int ilog2_exact(int64_t v);  // -1 if not a power of two
 
 // workspace layout (per micro-batch of mb signals), in bytes
 struct WsLayout {
-  size_t xhat, tmp, u1, u1hat, yphi, y2, y16, ys, part, sel, flag, total;
+  size_t xhat, tmp, tmp2, u1, u1hat, yphi, y2, y16, ys, part, sel, flag, total;
 };
 WsLayout ws_layout(const Plan& p, int64_t mb);
 

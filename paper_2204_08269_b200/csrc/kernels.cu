@@ -293,6 +293,56 @@ __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __r
 }
 
 // ---------------------------------------------------------------------------------
+// KB middle stage for four-step lengths (L = La Lb): the inverse DFT's pass B (rows ka of
+// the pass-A intermediate, length Lb over kb), the modulus |.| / L1 of the scalogram row,
+// and the forward DFT's first pass -- fused through shared memory, so U1 never leaves
+// the chip.  The forward DFT is factorised the other way round (n = na' + La nb',
+// k = kb' + Lb ka''): the G inverse-DFT outputs of this CTA, U1[ka + La kb] for its G
+// values ka and every kb, are exactly the G columns na' = ka of the forward transform.
+// Stage 2 is a length-Lb FFT over nb' per column, times W_L^{na' kb'}, written as rows
+// kb' of length La; k_fft4_b<LOG2B, LOG2A> (ProbRealFwd) finishes with the length-La pass.
+// ---------------------------------------------------------------------------------
+template <int LOG2A, int LOG2B, int G, int NT>
+__global__ void __launch_bounds__(NT) k_fft4_mid(ProbFold prob, const float2* __restrict__ tmp_in,
+                                                 float2* __restrict__ tmp_out, const float2* __restrict__ Wtab,
+                                                 int rho0) {
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
+  constexpr int LS = pad_row(Lb);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* s1 = reinterpret_cast<float2*>(smem_raw);
+  float2* s2 = s1 + G * LS;
+  float2* Ws = s2 + G * LS;        // per-pass twiddles of length Lb (both directions)
+  float2* Wlo = Ws + Lb;           // W_L^t, t < Lb
+  float2* Whi = Wlo + Lb;          // W_La^t, t < La  (= W_L^{Lb t})
+  stage_twiddles<LOG2B, NT>(Ws, Wtab + tw_offset(LOG2B));
+  {
+    const float2* WL = Wtab + tw_offset(LOG2A + LOG2B);
+    for (int t = threadIdx.x; t < Lb; t += NT) Wlo[t] = __ldg(WL + t);
+    for (int t = threadIdx.x; t < La; t += NT) Whi[t] = __ldg(Wtab + tw_offset(LOG2A) + t);
+  }
+  constexpr int RPB = La / G;
+  const int rho = rho0 + (int)(blockIdx.x / RPB);
+  const int ka0 = (blockIdx.x % RPB) * G;
+  const float2* in = tmp_in + (int64_t)(rho - rho0) * L;
+  float2* out = tmp_out + (int64_t)(rho - rho0) * L;
+  const float sc = prob.rows[rho % prob.nrows].scale;
+  __syncthreads();  // twiddle tables
+  // stage 1: inverse DFT over kb of rows ka0 + g; U1 = |.| sc into s2 row g, element kb
+  auto ld1 = [&](int g, int e) -> float2 { return in[(ka0 + g) * Lb + e]; };
+  auto st1 = [&](int g, int kb, float2 v) { s2[g * LS + padx(kb)] = make_float2(sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc, 0.f); };
+  fft_fused<LOG2B, G, NT, +1, LS, true, true, true, float2, decltype(ld1), decltype(st1), false>(s1, Ws, ld1, st1);
+  __syncthreads();
+  // stage 2: forward DFT over nb' of columns na' = ka0 + g, twiddle W_L^{na' kb'}, rows kb'
+  auto ld2 = [&](int, int) -> float2 { return make_float2(0.f, 0.f); };  // unused: input in s2
+  auto st2 = [&](int g, int kb, float2 v) {
+    const int x = kb * (ka0 + g);
+    const float2 tw = cmul(Wlo[x & (Lb - 1)], Whi[x >> LOG2B]);
+    out[kb * La + ka0 + g] = cmul(v, tw);
+  };
+  fft_fused<LOG2B, G, NT, -1, LS, true, false, true>(s2, Ws, ld2, st2);
+}
+
+// ---------------------------------------------------------------------------------
 // KS: phi_T averaging at rate T by folding the band-limited spectrum to NPT bins.
 // One warp per (signal, row).  row < 0 denotes S0 (source X_hat on the N_pad grid).
 // ---------------------------------------------------------------------------------
@@ -794,6 +844,37 @@ void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, con
   }
 }
 
+// KB four-step with the fused middle stage: inverse pass A (ProbFold) -> k_fft4_mid ->
+// forward pass B' (k_fft4_b<LOG2B, LOG2A>, ProbRealFwd).  tmp2: a second intermediate.
+template <int LOG2L>
+void launch_fft4_u1(const ProbFold& pf, const ProbRealFwd& prf, int nbig, float2* tmp, float2* tmp2,
+                    const float2* W, cudaStream_t st) {
+  constexpr int ELEMS = 4096;
+  constexpr int LOG2A = (LOG2L + 1) / 2, LOG2B = LOG2L / 2;
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B;
+  constexpr int GA0 = ELEMS / La;
+  constexpr int GA = (GA0 < 16 && 16 <= Lb && La >= 256) ? 16 : GA0;  // as launch_fft4
+  constexpr int GM = ELEMS / Lb;   // middle stage: rows ka per CTA
+  constexpr int GB = ELEMS / La;   // final pass: rows kb' (length La) per CTA
+  constexpr int NT = ELEMS / 8;
+  static_assert(GA >= 1 && GM >= 1 && GB >= 1 && GM <= La && GB <= Lb, "four-step tile");
+  const size_t sma = ((size_t)GA * pad_row(La) + 2 * La + Lb) * sizeof(float2);
+  const size_t smm = ((size_t)2 * GM * pad_row(Lb) + 2 * Lb + La) * sizeof(float2);
+  const size_t smb = ((size_t)GB * pad_row(La) + La) * sizeof(float2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft4_a<LOG2A, LOG2B, GA, NT, +1, ProbFold>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(k_fft4_mid<LOG2A, LOG2B, GM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_fft4_b<LOG2B, LOG2A, GB, NT, -1, ProbRealFwd>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  k_fft4_a<LOG2A, LOG2B, GA, NT, +1, ProbFold><<<nbig * (Lb / GA), NT, sma, st>>>(pf, tmp, W, 0);
+  k_fft4_mid<LOG2A, LOG2B, GM, NT><<<nbig * (La / GM), NT, smm, st>>>(pf, tmp, tmp2, W, 0);
+  k_fft4_b<LOG2B, LOG2A, GB, NT, -1, ProbRealFwd><<<nbig * (Lb / GB), NT, smb, st>>>(prf, tmp2, W, 0);
+}
+
 template <class F>
 void dispatch_log2(int lg, F&& f) {
   switch (lg) {
@@ -827,12 +908,13 @@ int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2
 }
 
 int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,
-                       bool keep_u1, cudaStream_t st) {
+                       bool keep_u1, cudaStream_t st, float2* tmp2) {
   const float2* W = (const float2*)P.d_twiddle;
   const int ltw = ilog2_exact(P.N_tw);
   int n = 0;
+  const bool fuse = tmp2 && !keep_u1 && !std::getenv("JTFS_KB_UNFUSED");  // env: measurement only
   for (const auto& g : P.u1_groups) {
-    n += g.log2L <= 12 ? 1 : 4;
+    n += g.log2L <= 12 ? 1 : (fuse ? 3 : 4);
     const int nr = (int)g.rows.size();
     ProbFold pf{xhat, P.N_pad, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, u1, nullptr, P.u1_total};
     ProbRealFwd prf{u1, u1hat, P.u1_total, g.d_rows, nr};
@@ -840,6 +922,9 @@ int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, f
       constexpr int LG = decltype(c)::value;
       if constexpr (LG <= 12) {
         launch_u1_fused<LG>(pf, u1hat, keep_u1 ? u1 : nullptr, nsig * nr, W, ltw, st);
+      } else if (fuse) {
+        ProbRealFwd prf2 = prf;  // reads nothing from U1 (its input comes from tmp2)
+        launch_fft4_u1<LG>(pf, prf2, nsig * nr, tmp, tmp2, W, st);
       } else {
         launch_fft4<LG, +1>(pf, pf, nsig * nr, tmp, W, ltw, st);
         launch_fft4<LG, -1>(prf, prf, nsig * nr, tmp, W, ltw, st);

@@ -60,8 +60,10 @@ struct KEParams {
 };
 
 int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2* tmp, cudaStream_t st);
+// tmp2 (optional): a second four-step intermediate; with it (and keep_u1 false) the
+// lengths > 4096 run the fused inverse-DFT / modulus / forward-DFT middle stage
 int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,
-                        bool keep_u1, cudaStream_t st);
+                        bool keep_u1, cudaStream_t st, float2* tmp2 = nullptr);
 int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int nsig, float* yphi, float* out,
                       int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
                       const Band* d_band_L1, cudaStream_t st);

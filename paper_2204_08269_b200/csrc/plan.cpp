@@ -695,6 +695,13 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   for (const auto& g : p.y2_groups)
     if (g.log2L > 12) tmp = std::max(tmp, g.rows.size() * ((size_t)8 << g.log2L));
   w.tmp = al((size_t)mb * tmp);
+  // second four-step intermediate of the fused first-order middle stage (k_fft4_mid)
+  {
+    size_t t2 = 0;
+    for (const auto& g : p.u1_groups)
+      if (g.log2L > 12) t2 = std::max(t2, g.rows.size() * ((size_t)8 << g.log2L));
+    w.tmp2 = al((size_t)mb * t2);
+  }
   w.u1 = al((size_t)mb * p.u1_total * 4);
   w.u1hat = al((size_t)mb * p.u1_total * 8);
   w.yphi = al((size_t)mb * p.n1 * p.NPT * 4);
@@ -708,7 +715,7 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
     w.sel = al(nsel * 4);
   }
   w.flag = 256;
-  w.total = w.xhat + w.tmp + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.sel + w.flag;
+  w.total = w.xhat + w.tmp + w.tmp2 + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.sel + w.flag;
   return w;
 }
 
