@@ -342,6 +342,112 @@ __global__ void __launch_bounds__(NT) k_fft4_mid(ProbFold prob, const float2* __
   fft_fused<LOG2B, G, NT, -1, LS, true, false, true>(s2, Ws, ld2, st2);
 }
 
+// Real-pair variant: two scalogram rows (lambda = 2j, 2j + 1 of the group) share one
+// complex forward DFT, z = U1_a + i U1_b; k_fft4_fin2 separates the spectra with
+// U_a[k] = (Z[k] + conj Z[-k]) / 2, U_b[k] = (Z[k] - conj Z[-k]) / 2i.  Grid: (signal, pair, ka block).
+template <int LOG2A, int LOG2B, int G, int NT>
+__global__ void __launch_bounds__(NT) k_fft4_mid2(ProbFold prob, const float2* __restrict__ tmp_in,
+                                                  float2* __restrict__ tmp_out, const float2* __restrict__ Wtab) {
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;
+  constexpr int LS = pad_row(Lb);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* s1 = reinterpret_cast<float2*>(smem_raw);
+  float2* s2 = s1 + G * LS;
+  float2* Ws = s2 + G * LS;
+  float2* Wlo = Ws + Lb;
+  float2* Whi = Wlo + Lb;
+  stage_twiddles<LOG2B, NT>(Ws, Wtab + tw_offset(LOG2B));
+  {
+    const float2* WL = Wtab + tw_offset(LOG2A + LOG2B);
+    for (int t = threadIdx.x; t < Lb; t += NT) Wlo[t] = __ldg(WL + t);
+    for (int t = threadIdx.x; t < La; t += NT) Whi[t] = __ldg(Wtab + tw_offset(LOG2A) + t);
+  }
+  constexpr int RPB = La / G;
+  const int nr = prob.nrows, npair = (nr + 1) >> 1;
+  const int q = (int)(blockIdx.x / RPB);  // pair id = b * npair + j
+  const int ka0 = (blockIdx.x % RPB) * G;
+  const int b = q / npair, j = q % npair;
+  const bool two = 2 * j + 1 < nr;
+  float2* out = tmp_out + (int64_t)q * L;
+  __syncthreads();  // twiddle tables
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    float* s2f = reinterpret_cast<float*>(s2) + h;  // component h (re: row 2j, im: row 2j + 1)
+    if (h == 1 && !two) {
+      for (int idx = threadIdx.x; idx < G * Lb; idx += NT) s2f[2 * ((idx / Lb) * LS + padx(idx % Lb))] = 0.f;
+      break;
+    }
+    const int rho = b * nr + 2 * j + h;
+    const float2* in = tmp_in + (int64_t)rho * L;
+    const float sc = prob.rows[2 * j + h].scale;
+    auto ld1 = [&](int g, int e) -> float2 { return in[(ka0 + g) * Lb + e]; };
+    auto st1 = [&](int g, int kb, float2 v) { s2f[2 * (g * LS + padx(kb))] = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc; };
+    fft_fused<LOG2B, G, NT, +1, LS, true, true, true, float2, decltype(ld1), decltype(st1), false>(s1, Ws, ld1, st1);
+    __syncthreads();
+  }
+  __syncthreads();
+  auto ld2 = [&](int, int) -> float2 { return make_float2(0.f, 0.f); };  // unused: input in s2
+  auto st2 = [&](int g, int kb, float2 v) {
+    const int x = kb * (ka0 + g);
+    const float2 tw = cmul(Wlo[x & (Lb - 1)], Whi[x >> LOG2B]);
+    out[kb * La + ka0 + g] = cmul(v, tw);
+  };
+  fft_fused<LOG2B, G, NT, -1, LS, true, false, true>(s2, Ws, ld2, st2);
+}
+
+// Final pass of the real-pair forward DFT: rows kb' (length La over na') of the packed
+// intermediate, G rows per CTA chosen closed under kb' <-> Lb - kb' (rows 0 and Lb/2 pair
+// with themselves), FFT in shared memory, then the two spectra are separated bin by bin.
+template <int LOG2A, int LOG2B, int G, int NT>
+__global__ void __launch_bounds__(NT) k_fft4_fin2(ProbRealFwd prob, const float2* __restrict__ tmp,
+                                                  const float2* __restrict__ Wtab) {
+  constexpr int La = 1 << LOG2A, Lb = 1 << LOG2B, L = La * Lb;  // rows kb' < Lb of length La
+  constexpr int LS = pad_row(La);
+  constexpr int H = G / 2;
+  static_assert(G % 2 == 0 && G <= Lb, "paired rows");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* s = reinterpret_cast<float2*>(smem_raw);
+  float2* Ws = s + G * LS;
+  stage_twiddles<LOG2A, NT>(Ws, Wtab + tw_offset(LOG2A));
+  constexpr int CPP = Lb / G;  // CTAs per pair
+  const int q = (int)(blockIdx.x / CPP);
+  const int c = blockIdx.x % CPP;
+  const int nr = prob.nrows, npair = (nr + 1) >> 1;
+  const int b = q / npair, j = q % npair;
+  const bool two = 2 * j + 1 < nr;
+  const float2* in = tmp + (int64_t)q * L;
+  // slot g -> row: g < H: A = c H + g; g >= H: Lb - A (A = 0 -> Lb / 2)
+  auto row_of = [&](int g) -> int {
+    const int a = c * H + (g < H ? g : g - H);
+    return g < H ? a : (a == 0 ? Lb / 2 : Lb - a);
+  };
+  __syncthreads();
+  auto ld = [&](int g, int e) -> float2 { return in[row_of(g) * La + e]; };
+  auto st = [&](int, int, float2) {};  // results stay in shared memory
+  fft_fused<LOG2A, G, NT, -1, LS, false, true, false, float2, decltype(ld), decltype(st), false>(s, Ws, ld, st);
+  float2* ua = prob.u1hat + (int64_t)b * prob.stride + prob.rows[2 * j].dst_off;
+  float2* ub = two ? prob.u1hat + (int64_t)b * prob.stride + prob.rows[2 * j + 1].dst_off : nullptr;
+  for (int idx = threadIdx.x; idx < G * La; idx += NT) {
+    const int g = idx % G, e = idx / G;
+    const int r = row_of(g);
+    int gp, ep;
+    if (r == 0) {
+      gp = g;
+      ep = (La - e) & (La - 1);
+    } else if (r == Lb / 2) {
+      gp = g;
+      ep = La - 1 - e;
+    } else {
+      gp = g < H ? g + H : g - H;
+      ep = La - 1 - e;
+    }
+    const float2 z = s[g * LS + padx(e)], zp = s[gp * LS + padx(ep)];
+    const int k = r + Lb * e;
+    ua[k] = make_float2(0.5f * (z.x + zp.x), 0.5f * (z.y - zp.y));
+    if (ub) ub[k] = make_float2(0.5f * (z.y + zp.y), -0.5f * (z.x - zp.x));
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // KS: phi_T averaging at rate T by folding the band-limited spectrum to NPT bins.
 // One warp per (signal, row).  row < 0 denotes S0 (source X_hat on the N_pad grid).
@@ -871,8 +977,25 @@ void launch_fft4_u1(const ProbFold& pf, const ProbRealFwd& prf, int nbig, float2
     attr = true;
   }
   k_fft4_a<LOG2A, LOG2B, GA, NT, +1, ProbFold><<<nbig * (Lb / GA), NT, sma, st>>>(pf, tmp, W, 0);
-  k_fft4_mid<LOG2A, LOG2B, GM, NT><<<nbig * (La / GM), NT, smm, st>>>(pf, tmp, tmp2, W, 0);
-  k_fft4_b<LOG2B, LOG2A, GB, NT, -1, ProbRealFwd><<<nbig * (Lb / GB), NT, smb, st>>>(prf, tmp2, W, 0);
+  static const bool unpaired = std::getenv("JTFS_KB_UNPAIRED") != nullptr;  // measurement only
+  if (unpaired) {
+    k_fft4_mid<LOG2A, LOG2B, GM, NT><<<nbig * (La / GM), NT, smm, st>>>(pf, tmp, tmp2, W, 0);
+    k_fft4_b<LOG2B, LOG2A, GB, NT, -1, ProbRealFwd><<<nbig * (Lb / GB), NT, smb, st>>>(prf, tmp2, W, 0);
+    return;
+  }
+  // real pairs: rows (2j, 2j + 1) of the group share one complex forward DFT
+  static bool attr2 = false;
+  constexpr int GF = GB < 2 ? 2 : GB;
+  const size_t smf = ((size_t)GF * pad_row(La) + La) * sizeof(float2);
+  if (!attr2) {
+    cudaFuncSetAttribute(k_fft4_mid2<LOG2A, LOG2B, GM, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_fft4_fin2<LOG2A, LOG2B, GF, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr2 = true;
+  }
+  const int nsig = nbig / pf.nrows, npair = (pf.nrows + 1) / 2;
+  k_fft4_mid2<LOG2A, LOG2B, GM, NT><<<nsig * npair * (La / GM), NT, smm, st>>>(pf, tmp, tmp2, W);
+  k_fft4_fin2<LOG2A, LOG2B, GF, NT><<<nsig * npair * (Lb / GF), NT, smf, st>>>(prf, tmp2, W);
 }
 
 template <class F>
