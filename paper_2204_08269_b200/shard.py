@@ -64,3 +64,50 @@ def forward_sharded(plan, x, group=None, stream=None):
         return None
     plan.reduce_pack(partials, out, stream=stream)
     return out
+
+
+# ---- batch sharding (configs c3 / c5): signals are independent ----
+def batch_slice(B: int, world: int, rank: int):
+    """Contiguous signal range [b0, b1) of `rank`: the first B % world ranks get one extra."""
+    if world < 1 or not 0 <= rank < world or B < 0:
+        raise ValueError("bad batch split")
+    q, r = divmod(B, world)
+    b0 = rank * q + min(rank, r)
+    return b0, b0 + q + (1 if rank < r else 0)
+
+
+def gather_outputs(local_out, B: int, group=None):
+    """The optional collective of the batch-sharded path: all ranks' fp32 records
+    (rank r holds batch_slice(B, world, r)) gathered into one [B, floats] tensor on every
+    rank with all_gather_into_tensor (ranks' slices padded to the largest one)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return local_out
+    rank = dist.get_rank(group)
+    fps = local_out.shape[1]
+    cnt = max(b1 - b0 for b0, b1 in (batch_slice(B, world, r) for r in range(world)))
+    send = torch.zeros(cnt, fps, dtype=local_out.dtype, device=local_out.device)
+    b0, b1 = batch_slice(B, world, rank)
+    send[: b1 - b0] = local_out
+    recv = torch.empty(world * cnt, fps, dtype=local_out.dtype, device=local_out.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    parts = []
+    for r in range(world):
+        a, b = batch_slice(B, world, r)
+        parts.append(recv[r * cnt: r * cnt + (b - a)])
+    return torch.cat(parts, dim=0)
+
+
+def forward_batch_sharded(plan, x_full, group=None, gather: bool = True, stream=None):
+    """Batch-sharded forward: rank r transforms its contiguous slice of x_full (CUDA
+    float32 [B, N]) with no data-path collective; with `gather` the records are
+    all-gathered (one NCCL all_gather_into_tensor).  Outputs are byte-identical to a
+    single-GPU forward (the per-signal computation does not depend on B or the split)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    b0, b1 = batch_slice(x_full.shape[0], world, rank)
+    out = plan.forward(x_full[b0:b1].contiguous(), stream=stream)
+    return gather_outputs(out, x_full.shape[0], group) if gather else out

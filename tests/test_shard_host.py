@@ -104,3 +104,51 @@ def test_exchange_partials_gloo_world2(jt):
         assert p.exitcode == 0
     want = _fill(n_units, seg, range(n_units)).tobytes()
     assert got == want                                          # byte-identical to one rank
+
+
+def test_batch_slice_partitions():
+    for B in (0, 1, 7, 256, 4097):
+        for world in (1, 2, 3, 8):
+            sl = [shard.batch_slice(B, world, r) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == B
+            assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+            sizes = [b - a for a, b in sl]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard.batch_slice(4, 2, 2)
+
+
+def _gather_worker(rank, world, port, B, fps, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b0, b1 = shard.batch_slice(B, world, rank)
+        full = torch.arange(B * fps, dtype=torch.float32).reshape(B, fps)
+        got = shard.gather_outputs(full[b0:b1].clone(), B)
+        q.put((rank, got.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [7, 8])
+def test_gather_outputs_gloo_world2(B):
+    # the optional all_gather of the batch-sharded records (ragged split)
+    import torch.multiprocessing as mp
+    fps = 5
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, B, fps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.arange(B * fps, dtype=np.float32).tobytes()
+    assert res[0] == want and res[1] == want
