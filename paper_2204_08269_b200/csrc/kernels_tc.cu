@@ -363,7 +363,9 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int 
   return l;
 }
 
-template <int NF, int MAXSLOT, bool PROF>
+// NTC: the tile width Nt as a compile-time constant (32 / 64 / 128: the epilogue's column
+// loops unroll completely), or 0 = p.Nt at run time (the instrumented variant)
+template <int NF, int MAXSLOT, bool PROF, int NTC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_kd_tc(const __grid_constant__ CUtensorMap tmB, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -573,11 +575,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 part[NF / 2];
 #pragma unroll
         for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
-        const int half = p.Nt / 2;
+        const int half = (NTC ? NTC : p.Nt) / 2;
         if (p.pool_mode == 1) {
           // moment form: per 32-column block S_k = sum_j |Z_j| u_j^k (k <= 3, u_j
           // compile-time), then part += G_k S_k with the block's 4 x NF coefficients
           const float* gco = Wt + wi * wfl + (cbeg / 32) * 4 * NF;
+#pragma unroll
           for (int c0 = 0; c0 < half; c0 += 32) {
             float S[4] = {0.f, 0.f, 0.f, 0.f};
             {
@@ -610,6 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
           }
         } else {
+#pragma unroll
           for (int c0 = 0; c0 < half; c0 += 16) {
             uint32_t v[32];
             tmem_ld32(tb + 2 * c0, v);
@@ -796,9 +800,13 @@ cudaError_t tc_setup_device(Plan& P) {
   auto set = [&](auto kern) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
   };
-  if (NF == 8) { set(tc::k_kd_tc<8, 9, false>); set(tc::k_kd_tc<8, 9, true>); }
-  else if (NF == 16) { set(tc::k_kd_tc<16, 4, false>); set(tc::k_kd_tc<16, 4, true>); }
-  else { set(tc::k_kd_tc<32, 2, false>); set(tc::k_kd_tc<32, 2, true>); }
+#define JTFS_SET_KD(NF_, MS_)                                                                      \
+  set(tc::k_kd_tc<NF_, MS_, false, 128>); set(tc::k_kd_tc<NF_, MS_, false, 64>);                  \
+  set(tc::k_kd_tc<NF_, MS_, false, 32>); set(tc::k_kd_tc<NF_, MS_, true, 0>);
+  if (NF == 8) { JTFS_SET_KD(8, 9) }
+  else if (NF == 16) { JTFS_SET_KD(16, 4) }
+  else { JTFS_SET_KD(32, 2) }
+#undef JTFS_SET_KD
   return e;
 }
 
@@ -901,15 +909,16 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
       cudaEventRecord(e0, st);
       P.prof_kd[i].push_back({(void*)e0, (void*)e1});
     }
-    if (do_prof) {
-      if (NF == 8) tc::k_kd_tc<8, 9, true><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-      else if (NF == 16) tc::k_kd_tc<16, 4, true><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-      else tc::k_kd_tc<32, 2, true><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-    } else {
-      if (NF == 8) tc::k_kd_tc<8, 9, false><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-      else if (NF == 16) tc::k_kd_tc<16, 4, false><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-      else tc::k_kd_tc<32, 2, false><<<grid, tc::kThreads, sm, st>>>(tmB, p);
-    }
+    auto go = [&](auto kern) { kern<<<grid, tc::kThreads, sm, st>>>(tmB, p); };
+#define JTFS_GO_KD(NF_, MS_)                                                                        \
+  if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 0>);                                                 \
+  else if (d.tc_Nt == 128) go(tc::k_kd_tc<NF_, MS_, false, 128>);                                  \
+  else if (d.tc_Nt == 64) go(tc::k_kd_tc<NF_, MS_, false, 64>);                                    \
+  else go(tc::k_kd_tc<NF_, MS_, false, 32>);
+    if (NF == 8) { JTFS_GO_KD(8, 9) }
+    else if (NF == 16) { JTFS_GO_KD(16, 4) }
+    else { JTFS_GO_KD(32, 2) }
+#undef JTFS_GO_KD
     ++launches;
     if (P.prof) cudaEventRecord(e1, st);
     if (do_prof) {
