@@ -730,7 +730,8 @@ void plan_tc(Plan& P) {
   const char* e_s = std::getenv("JTFS_TC_SMAX");
   const int nt_max = e_nt ? std::max(64, std::atoi(e_nt)) : 128;
   // A ring: stages of rps 8 KiB K-records (JTFS_TC_RPS: measurement-only override,
-  // default 4).  Measured on c3 (round 1): rps = 1 / 2 / 4 -> 2156 / 2459 / 2542
+  // default: per alpha, equal stages of <= 4 records, see below).  Measured on c3 (round 1),
+  // uniform rps = 1 / 2 / 4 -> 2156 / 2459 / 2542
   // signals/s -- more, smaller L2 -> smem copies in flight starve the MMA more (per-copy
   // overhead), so stages stay at 32 KiB.  The ring holds at most 24 records (192 KiB).
   const char* e_r = std::getenv("JTFS_TC_RPS");
@@ -742,7 +743,13 @@ void plan_tc(Plan& P) {
     d.tc_nkc = d.tc_K16 / 16;
     d.tc_nbr = (d.tc_K16 + 255) / 256;
     d.tc_BRk = (d.tc_K16 / d.tc_nbr + 7) / 8 * 8;
-    d.tc_rps = rps;
+    // records per stage: JTFS_TC_RPS if set, else stages as equal as possible with <= 4
+    // records (nkc = 5 -> 3 + 2, not 4 + 1: a 1-record stage is consumed in 3 MMAs, too
+    // fast for the next 4-record copy into its slot)
+    {
+      const int nst = (d.tc_nkc + 3) / 4;
+      d.tc_rps = e_r ? rps : (d.tc_nkc + nst - 1) / nst;
+    }
     bool ok = false;
     // Nt = 128 (MMA N = 256, the efficient shape) first; two B buffers when they fit
     // with >= min_s2 x 4 A records (JTFS_TC_MINS2: measurement-only override, default 2)
