@@ -246,3 +246,24 @@ def test_forward_is_cuda_graph_capturable(jt):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_forward_host_buffers_and_batch_sharded_helper(jt):
+    # jtfs_forward_host (the e2e entry point of bench.py: pinned host in / out, copies on
+    # the stream) and shard.forward_batch_sharded (single process: no collective) give the
+    # same bytes as jtfs_forward
+    import torch
+    from paper_2204_08269_b200 import shard
+    plan = jt.Plan(**C1)
+    X = np.concatenate([_c1_inputs(), signals.white(3, 2 ** 10, seed=21)]).astype(np.float32)
+    x = torch.from_numpy(X).cuda()
+    ref = plan.forward(x).cpu()
+    xh = torch.from_numpy(X).pin_memory()
+    oh = torch.empty(ref.shape, dtype=torch.float32).pin_memory()
+    xd = torch.empty_like(x)
+    od = torch.empty(ref.shape, dtype=torch.float32, device="cuda")
+    plan.forward_host(xh, oh, xd, od)
+    assert torch.equal(oh, ref)
+    got = shard.forward_batch_sharded(plan, x).cpu()
+    assert torch.equal(got, ref)
+    assert shard.batch_slice(len(X), 1, 0) == (0, len(X))
