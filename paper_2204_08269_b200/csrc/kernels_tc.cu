@@ -760,9 +760,9 @@ void plan_tc(Plan& P) {
       if (c[0] > nt_max || c[0] > d.L) continue;
       d.tc_Nt = c[0];
       d.tc_NBB = c[1];
-      d.tc_S = c[2] * 4 / rps;  // the same minimum ring bytes (c[2] x 32 KiB) in rps-record stages
+      d.tc_S = e_r ? c[2] * 4 / rps : c[2];  // minimum ring: c[2] stages (of tc_rps records)
       if (tc_smem(d, NF) > budget) continue;
-      while ((d.tc_S + 1) * rps <= rec_max && tc_smem(d, NF) + (size_t)rps * tc::kRec <= budget) ++d.tc_S;
+      while ((d.tc_S + 1) * d.tc_rps <= rec_max && tc_smem(d, NF) + (size_t)d.tc_rps * tc::kRec <= budget) ++d.tc_S;
       ok = true;
       break;
     }
