@@ -771,7 +771,8 @@ void plan_tc(Plan& P) {
     if (ok) {
       const int64_t sig = (P.prm.flags & JTFS_LATENCY) ? 1 : P.mb;  // signals per KD launch
       int64_t target = sig * P.tc_n_mpart * d.L / (4 * 148);
-      int ch = 4096;
+      const char* e_ch = std::getenv("JTFS_TC_CHUNKMAX");  // measurement only
+      int ch = e_ch ? std::max(64, std::atoi(e_ch)) : 4096;
       while (ch > d.tc_Nt && ch > target) ch /= 2;  // (JTFS_LATENCY: one signal per launch)
       d.chunk = std::min(ch, d.L);
       if (d.chunk < d.tc_Nt) d.chunk = d.tc_Nt;
