@@ -50,6 +50,11 @@ typedef enum {
 /* flags */
 #define JTFS_CHECK_FINITE 1u   /* forward scans x for NaN/Inf first (one device sync) */
 #define JTFS_LATENCY 2u        /* size KD work units for one signal per forward (c4, path sharding) */
+/* validation / measurement flags (never needed for production use; every output byte
+ * is a function of (params incl. flags, x) -- the library reads no environment): */
+#define JTFS_KD_SIMT 4u        /* KD on the FP32 SIMT validation kernel instead of tcgen05 */
+#define JTFS_POOL_EXACT 8u     /* KD epilogue with the exact phi_T taps (no cubic-moment form) */
+#define JTFS_KD_PROF 16u       /* instrumented KD: per-role wait cycles to stderr (syncs per launch) */
 
 /* pad modes (reading R6) */
 #define JTFS_PAD_REFLECT 0     /* numpy 'reflect' to N_pad = 2N, centred */
@@ -69,7 +74,7 @@ typedef struct jtfs_plan_s* jtfs_plan_t;  /* opaque; immutable after creation */
  *   average_fr  1: Eq. (3) (Phi_{T,F}); 0: Eq. (4) (Phi_T only)
  *   pad_mode    JTFS_PAD_REFLECT or JTFS_PAD_PERIODIC
  *   device      CUDA device ordinal; -1 = host-only plan (queries only, no forward)
- *   flags       JTFS_CHECK_FINITE | JTFS_LATENCY
+ *   flags       JTFS_CHECK_FINITE | JTFS_LATENCY (| validation flags above)
  */
 typedef struct {
   int32_t N, J, Q, Q2, T, J_fr, Q_fr, F;

@@ -247,10 +247,6 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
     s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, w.y16, w.ys, nb, part, st, &err, o.sel)
                           : launch_kd(P, w.y2, nb, part, st, o.sel));
     if (err) return "tcgen05 KD: cuTensorMapEncodeTiled failed for the Y2 tensor map";
-    if (std::getenv("JTFS_DEBUG_SYNC")) {
-      cudaError_t e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return std::string("KD: ") + cudaGetErrorString(e);
-    }
   }
   if (o.skip_ke) return "";
   KEParams kp{};

@@ -71,7 +71,7 @@ struct AlphaKD {
   int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16
   int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
   int64_t y16_off = 0;  // fp16 offset of Y16_alpha [hi|lo][K16][L] in one signal's Y16 buffer (KY output)
-  int64_t ys_off = 0;   // float offset of the per-tile inverse Y scales (L / 64 slots) in one signal's ys
+  int64_t ys_off = 0;   // float offset of the per-tile inverse Y scales (L / 32 slots) in one signal's ys
   int64_t wtab_off = 0; // float offset of the phi_T pooling table in wtab
   int pool_mode = 0;    // 0: taps [L][NF]; 1: cubic-moment coefficients [L/32][4][NF] (kernels_tc.cu)
   int nslices = 0;      // KD partial slices per signal and alpha (time chunks x epilogue sets)
@@ -107,7 +107,7 @@ struct Plan {
   int64_t y2_total = 0;          // complex elements of Y2 per signal
   int M = 0, Mpad = 0;           // joint-stage rows per alpha
   int tc_n_mpart = 1, tc_n_mblk = 1;  // M-parts per KD work unit, 128-row M-blocks per part
-  int kd_impl = 1;               // 1: tcgen05 (default), 0: SIMT (JTFS_KD=simt, validation)
+  int kd_impl = 1;               // 1: tcgen05 (default), 0: SIMT (plan flag JTFS_KD_SIMT, validation)
   std::vector<FrFilter> fr;      // frequential filters: theta=-1 (beta), theta=+1 (beta), phi_F
   std::vector<jtfs_path_t> paths;
   std::vector<int> path_filter;  // path -> fr index (or -1)
@@ -185,7 +185,7 @@ struct WsLayout {
 WsLayout ws_layout(const Plan& p, int64_t mb);
 
 // tensor-core KD planning / device setup (kernels_tc.cu)
-void plan_tc(Plan& P);
+std::string plan_tc(Plan& P);  // "" or why an alpha cannot be tiled
 
 // algorithmic per-signal cost per stage (jtfs_cost)
 void stage_cost(const Plan& p, double flops[6], double bytes[6]);

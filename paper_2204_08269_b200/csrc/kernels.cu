@@ -932,19 +932,12 @@ void launch_fft4(const PA& pa, const PB& pb, int nbig, typename PA::CT* tmp, con
                          227 * 1024);
     attr = true;
   }
-  // optional row groups whose intermediate stays L2-resident between the two passes
-  // (JTFS_FFT4_GROUP_MB, measurement only; 0 = one group, the default).  Measured on c3
-  // (round 1): 32 / 64 / 96 MiB groups made KB 16.5 -> 20.3 / 18.5 / 18.4 ms per step --
-  // the passes are not HBM-bound (pass A: issue 62 %, smem 53 %), so the extra launches
-  // and tails cost more than the DRAM round trip of the intermediate.
-  static const int group_mb = [] {
-    const char* e = std::getenv("JTFS_FFT4_GROUP_MB");
-    return e ? std::atoi(e) : 0;
-  }();
-  int grp = nbig;
-  if (group_mb > 0) grp = std::max(1, (int)(((int64_t)group_mb << 20) / ((int64_t)La * Lb * (int64_t)sizeof(CT))));
-  for (int r0 = 0; r0 < nbig; r0 += grp) {
-    const int nr = std::min(grp, nbig - r0);
+  // One launch pair over all rows.  (Measured on c3, round 1: splitting the rows into
+  // 32 / 64 / 96 MiB groups whose intermediate stays L2-resident made KB 16.5 -> 20.3 /
+  // 18.5 / 18.4 ms per step -- the passes are not HBM-bound, so the extra launches and
+  // tails cost more than the DRAM round trip of the intermediate.)
+  {
+    const int r0 = 0, nr = nbig;
     k_fft4_a<LOG2A, LOG2B, GA, NT, DIR, PA><<<nr * (Lb / GA), NT, sma, st>>>(pa, tmp, W, r0);
     k_fft4_b<LOG2A, LOG2B, GB, NT, DIR, PB><<<nr * (La / GB), NT, smb, st>>>(pb, tmp, W, r0);
   }
@@ -977,12 +970,6 @@ void launch_fft4_u1(const ProbFold& pf, const ProbRealFwd& prf, int nbig, float2
     attr = true;
   }
   k_fft4_a<LOG2A, LOG2B, GA, NT, +1, ProbFold><<<nbig * (Lb / GA), NT, sma, st>>>(pf, tmp, W, 0);
-  static const bool unpaired = std::getenv("JTFS_KB_UNPAIRED") != nullptr;  // measurement only
-  if (unpaired) {
-    k_fft4_mid<LOG2A, LOG2B, GM, NT><<<nbig * (La / GM), NT, smm, st>>>(pf, tmp, tmp2, W, 0);
-    k_fft4_b<LOG2B, LOG2A, GB, NT, -1, ProbRealFwd><<<nbig * (Lb / GB), NT, smb, st>>>(prf, tmp2, W, 0);
-    return;
-  }
   // real pairs: rows (2j, 2j + 1) of the group share one complex forward DFT
   static bool attr2 = false;
   constexpr int GF = GB < 2 ? 2 : GB;
@@ -1035,7 +1022,7 @@ int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, f
   const float2* W = (const float2*)P.d_twiddle;
   const int ltw = ilog2_exact(P.N_tw);
   int n = 0;
-  const bool fuse = tmp2 && !keep_u1 && !std::getenv("JTFS_KB_UNFUSED");  // env: measurement only
+  const bool fuse = tmp2 && !keep_u1;
   for (const auto& g : P.u1_groups) {
     n += g.log2L <= 12 ? 1 : (fuse ? 3 : 4);
     const int nr = (int)g.rows.size();

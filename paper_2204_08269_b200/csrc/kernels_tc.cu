@@ -84,7 +84,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// wait (+ accumulate the waited cycles into acc when instrumented: JTFS_TC_PROF selects
+// wait (+ accumulate the waited cycles into acc when instrumented: the JTFS_KD_PROF plan flag selects
 // the PROF = true kernel instantiation; the clock reads are compiled out otherwise)
 template <bool PROF>
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long long& acc) {
@@ -318,7 +318,7 @@ struct TcParams {
   int n_mpart, n_mblk;  // M-parts and 128-row M-blocks per part
   int L, nframes, Mpad;
   int nsig;
-  unsigned long long* prof;  // measurement only (JTFS_TC_PROF): per-role wait-cycle counters or nullptr
+  unsigned long long* prof;  // measurement only (JTFS_KD_PROF flag): per-role wait-cycle counters or nullptr
   const uint16_t* A;   // A''_alpha records [Mpad / 128][nkc] x 16 KiB
   const float* ainv;   // 1 / s_m per row [Mpad]
   const float* wtab;   // phi_T pooling table: taps [L][NF] (pool_mode 0) or cubic moments [L/32][4][NF] (1)
@@ -719,80 +719,81 @@ size_t tc_smem(const AlphaKD& d, int nf) {
 
 // choose the per-alpha tensor-core tiling (called by build_plan): the first of
 // (Nt, B buffers, min stages) = (128, 2, 3), (128, 2, 2), (128, 1, 3), (128, 1, 2),
-// (64, 2, 2), (64, 1, 2), (32, 1, 2) that fits (min stages in units of 4 K-records),
-// then as many A'' ring stages of rps records as fit (<= 24 records)
-void plan_tc(Plan& P) {
+// (64, 2, 2), (64, 1, 2), (32, 1, 2) that fits, then as many A'' ring stages of rps
+// records as fit (<= 24 records).  Every choice is a function of the plan alone (no
+// environment knobs: output bytes depend only on (plan, x)).  Returns "" or the reason
+// an alpha cannot be tiled (the plan then fails unless JTFS_KD_SIMT was requested).
+std::string plan_tc(Plan& P) {
   const int NF = nf_of(P.n_frames);
   const size_t budget = 227 * 1024;
   P.tc_n_mblk = P.Mpad / 128 / P.tc_n_mpart;
-  // tuning overrides (measurement only): largest tile width / number of A'' stages
-  const char* e_nt = std::getenv("JTFS_TC_NTMAX");
-  const char* e_s = std::getenv("JTFS_TC_SMAX");
-  const int nt_max = e_nt ? std::max(64, std::atoi(e_nt)) : 128;
-  // A ring: stages of rps 8 KiB K-records (JTFS_TC_RPS: measurement-only override,
-  // default: per alpha, equal stages of <= 4 records, see below).  Measured on c3 (round 1),
-  // uniform rps = 1 / 2 / 4 -> 2156 / 2459 / 2542
-  // signals/s -- more, smaller L2 -> smem copies in flight starve the MMA more (per-copy
-  // overhead), so stages stay at 32 KiB.  The ring holds at most 24 records (192 KiB).
-  const char* e_r = std::getenv("JTFS_TC_RPS");
-  const int rps = e_r ? (std::atoi(e_r) >= 4 ? 4 : std::atoi(e_r) >= 2 ? 2 : 1) : 4;
-  const int rec_max = e_s ? std::max(2, std::min(6, std::atoi(e_s))) * 4 : 24;
+  // A ring stages of rps 8 KiB K-records, as equal as possible with <= 4 records per
+  // stage (nkc = 5 -> 3 + 2, not 4 + 1: a 1-record stage is consumed in 3 MMAs, too fast
+  // for the next 4-record copy into its slot).  Measured on c3 (round 1): uniform
+  // rps = 1 / 2 / 4 -> 2156 / 2459 / 2542 signals/s (per-copy overhead), so stages stay
+  // at <= 32 KiB.  The ring holds at most 24 records (192 KiB).
+  constexpr int rec_max = 24;
   for (auto& d : P.kd) {
     d.tc_K2 = 2 * d.K;
     d.tc_K16 = (d.tc_K2 + 15) / 16 * 16;
     d.tc_nkc = d.tc_K16 / 16;
     d.tc_nbr = (d.tc_K16 + 255) / 256;
     d.tc_BRk = (d.tc_K16 / d.tc_nbr + 7) / 8 * 8;
-    // records per stage: JTFS_TC_RPS if set, else stages as equal as possible with <= 4
-    // records (nkc = 5 -> 3 + 2, not 4 + 1: a 1-record stage is consumed in 3 MMAs, too
-    // fast for the next 4-record copy into its slot)
     {
       const int nst = (d.tc_nkc + 3) / 4;
-      d.tc_rps = e_r ? rps : (d.tc_nkc + nst - 1) / nst;
+      d.tc_rps = (d.tc_nkc + nst - 1) / nst;
     }
-    bool ok = false;
     // Nt = 128 (MMA N = 256, the efficient shape) first; two B buffers when they fit
-    // with >= min_s2 x 4 A records (JTFS_TC_MINS2: measurement-only override, default 2)
-    const char* e_m2 = std::getenv("JTFS_TC_MINS2");
-    const int min_s2 = e_m2 ? std::max(2, std::atoi(e_m2)) : 2;
-    const int cand[7][3] = {{128, 2, 3}, {128, 2, min_s2}, {128, 1, 3}, {128, 1, 2}, {64, 2, 2}, {64, 1, 2}, {32, 1, 2}};
-    for (const auto& c : cand) {
-      if (c[0] > nt_max || c[0] > d.L) continue;
-      d.tc_Nt = c[0];
-      d.tc_NBB = c[1];
-      d.tc_S = e_r ? c[2] * 4 / rps : c[2];  // minimum ring: c[2] stages (of tc_rps records)
-      if (tc_smem(d, NF) > budget) continue;
-      while ((d.tc_S + 1) * d.tc_rps <= rec_max && tc_smem(d, NF) + (size_t)d.tc_rps * tc::kRec <= budget) ++d.tc_S;
-      ok = true;
-      break;
+    // with >= 2 stages of A records.  The moment-form epilogue needs Nt >= 64 (32-column
+    // blocks of each set's Nt / 2 columns): a narrower tile falls back to the exact taps.
+    auto choose = [&]() {
+      const int cand[7][3] = {{128, 2, 3}, {128, 2, 2}, {128, 1, 3}, {128, 1, 2}, {64, 2, 2}, {64, 1, 2}, {32, 1, 2}};
+      for (const auto& c : cand) {
+        if (c[0] > d.L) continue;
+        d.tc_Nt = c[0];
+        d.tc_NBB = c[1];
+        d.tc_S = c[2];
+        if (tc_smem(d, NF) > budget) continue;
+        while ((d.tc_S + 1) * d.tc_rps <= rec_max && tc_smem(d, NF) + (size_t)d.tc_rps * tc::kRec <= budget)
+          ++d.tc_S;
+        return true;
+      }
+      return false;
+    };
+    bool ok = choose();
+    if (ok && d.pool_mode && d.tc_Nt < 64) {
+      d.pool_mode = 0;
+      ok = choose();
     }
+    if (!ok) return "tensor-core KD: no tile of alpha " + std::to_string(d.alpha) + " fits shared memory";
     // time chunk per work unit: the largest power of two <= 4096 that still gives
-    // about 4 units per SM for a full micro-batch (partials are per chunk)
-    if (ok) {
-      const int64_t sig = (P.prm.flags & JTFS_LATENCY) ? 1 : P.mb;  // signals per KD launch
-      int64_t target = sig * P.tc_n_mpart * d.L / (4 * 148);
-      const char* e_ch = std::getenv("JTFS_TC_CHUNKMAX");  // measurement only
-      int ch = e_ch ? std::max(64, std::atoi(e_ch)) : 4096;
-      while (ch > d.tc_Nt && ch > target) ch /= 2;  // (JTFS_LATENCY: one signal per launch)
-      d.chunk = std::min(ch, d.L);
-      if (d.chunk < d.tc_Nt) d.chunk = d.tc_Nt;
-      d.nchunks = d.L / d.chunk;
-      d.tc_tpu = d.chunk / d.tc_Nt;
-    }
-    // the moment-form epilogue works on 32-column blocks of each set's Nt / 2 columns
-    if (!ok || d.L < 64 || d.chunk % d.tc_Nt || d.tc_nbr * d.tc_BRk < d.tc_K16 || (d.pool_mode && d.tc_Nt < 64))
-      P.kd_impl = 0;
+    // about 4 units per SM for a full micro-batch (partials are per chunk; measured on
+    // c3, round 1: 4096 / 8192 / 16384-column chunks equal within noise)
+    const int64_t sig = (P.prm.flags & JTFS_LATENCY) ? 1 : P.mb;  // signals per KD launch
+    const int64_t target = sig * P.tc_n_mpart * d.L / (4 * 148);
+    int ch = 4096;
+    while (ch > d.tc_Nt && ch > target) ch /= 2;  // (JTFS_LATENCY: one signal per launch)
+    d.chunk = std::min(ch, d.L);
+    if (d.chunk < d.tc_Nt) d.chunk = d.tc_Nt;
+    d.nchunks = d.L / d.chunk;
+    d.tc_tpu = d.chunk / d.tc_Nt;
+    // the KY / KD per-tile scale slots (plan.cpp sizes L / 32 per alpha and signal)
+    if (d.L / d.tc_Nt > std::max(1, d.L / 32)) return "internal: tensor-core KD tile scales exceed their slots";
+    if (d.L < 64) return "tensor-core KD: alpha " + std::to_string(d.alpha) + " has fewer than 64 time columns";
+    if (d.chunk % d.tc_Nt || d.nchunks * d.chunk != d.L) return "internal: tensor-core KD chunking";
+    if (d.tc_nbr * d.tc_BRk < d.tc_K16) return "internal: tensor-core KD B boxes";
   }
+  return "";
 }
 
 cudaError_t tc_setup_device(Plan& P) {
   if (P.kd_impl != 1) return cudaSuccess;
   // The persistent KD launches of the slow alphas (few work units) leave SMs idle; they
   // run on a second stream, overlapping the tails of the fast alphas' launches.
-  // JTFS_KD_SPLIT (measurement only): first alpha index on the side stream (<= 0: none).
+  // The first 5 active alphas (the long, fast ones: >= 90 % of KD's work in c3) run on
+  // the caller's stream, the rest on the side stream.
   {
-    const char* e = std::getenv("JTFS_KD_SPLIT");
-    const int split = e ? std::atoi(e) : 5;
+    const int split = 5;
     if (split > 0 && split < (int)P.kd.size()) {
       cudaStream_t s = nullptr;
       cudaError_t es = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
@@ -899,7 +900,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.ys = ys + d.ys_off;
     p.ys_stride = P.ys_total;
     static unsigned long long* prof = nullptr;
-    const bool do_prof = std::getenv("JTFS_TC_PROF") != nullptr;
+    const bool do_prof = (P.prm.flags & JTFS_KD_PROF) != 0;  // measurement-only plan flag
     if (do_prof && !prof) cudaMalloc(&prof, 16 * 8);
     if (do_prof) cudaMemsetAsync(prof, 0, 16 * 8, st);
     p.prof = do_prof ? prof : nullptr;

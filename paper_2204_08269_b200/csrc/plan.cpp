@@ -176,8 +176,17 @@ static std::vector<double> gauss_vec(double s, int L, int n) {
   return v;
 }
 
+// phi_T pooling weight of time column t for retained frame m of alpha's grid
+static double pool_tap(const Plan& P, const AlphaKD& d, int m, int64_t t) {
+  if (m >= P.n_frames) return 0.0;
+  int64_t i = ((int64_t)(P.frame0 + m) * d.D - t) % d.L;
+  if (i < 0) i += d.L;
+  return (double)P.g[d.g_off + i];
+}
+
 std::string build_plan(const jtfs_params& p, Plan& P) {
   P.prm = p;
+  std::vector<std::vector<float>> mom_tabs;  // per alpha: moment-form pooling table (if eligible)
   // ---- validation ----
   const int log2N = ilog2_exact(p.N);
   if (log2N < 4) return "N must be a power of two >= 16";
@@ -395,8 +404,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     P.tc_n_mpart = (mblocks + max_mblk - 1) / max_mblk;
     P.tc_n_mblk = (mblocks + P.tc_n_mpart - 1) / P.tc_n_mpart;
     P.Mpad = P.tc_n_mblk * P.tc_n_mpart * 128;
-    const char* e = std::getenv("JTFS_KD");
-    P.kd_impl = (e && std::strcmp(e, "simt") == 0) ? 0 : 1;
+    P.kd_impl = (p.flags & JTFS_KD_SIMT) ? 0 : 1;  // SIMT KD only on explicit request (validation)
   }
   // frequential taps h_f = IDFT_{N_fr}(f_hat) (fp64)
   std::vector<std::vector<std::complex<double>>> htap(P.fr.size());
@@ -508,26 +516,23 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     d.nchunks = d.L / d.chunk;
   }
   // KY output (fp16 hi/lo planes, rows padded to 16), per-tile scale slots (tiles
-  // of >= 64 columns) and the phi_T taps table [L][NF] of the tensor-core KD
+  // of >= 32 columns) and the phi_T pooling tables of the tensor-core KD (built after
+  // plan_tc, which decides the tile width the moment form needs)
   {
     const int NF = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
     P.y16_total = 0;
     P.ys_total = 0;
     P.wtab.clear();
-    for (auto& d : P.kd) {
+    mom_tabs.assign(P.kd.size(), {});
+    for (size_t ai = 0; ai < P.kd.size(); ++ai) {
+      auto& d = P.kd[ai];
       const int K16 = (2 * d.K + 15) / 16 * 16;
       d.y16_off = P.y16_total;
       P.y16_total += (int64_t)2 * K16 * 2 * d.L;  // [hi | lo][K16][2L]: complex block along N
       d.ys_off = P.ys_total;
-      P.ys_total += std::max(1, d.L / 64);
-      d.wtab_off = (int64_t)P.wtab.size();
+      P.ys_total += std::max(1, d.L / 32);  // one slot per tile; tiles have >= 32 columns (plan_tc checks)
       const float* g = P.g.data() + d.g_off;
-      auto tap = [&](int m, int64_t t) -> double {
-        if (m >= P.n_frames) return 0.0;
-        int64_t i = ((int64_t)(P.frame0 + m) * d.D - t) % d.L;
-        if (i < 0) i += d.L;
-        return (double)g[i];
-      };
+      auto tap = [&](int m, int64_t t) -> double { return pool_tap(P, d, m, t); };
       // phi_T pooling in moment form where it is exact to fp32 (kernels_tc.cu,
       // DESIGN.md §6): over each 32-column block, every frame's tap sequence is
       // replaced by its least-squares cubic in u_j = (j - 15.5) / 16 (coefficients
@@ -535,7 +540,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       // the evaluated cubic deviates from the fp32 taps by <= 2^-22 of that block's
       // largest tap (the taps' own fp32 rounding is 2^-24), plus 2^-40 max |g|.
       d.pool_mode = 0;
-      if (d.L % 32 == 0 && !std::getenv("JTFS_POOL_EXACT")) {  // env: measurement / validation only
+      if (d.L % 32 == 0 && !(p.flags & JTFS_POOL_EXACT)) {  // flag: validation of the moment form
         double gmax = 0;
         for (int t = 0; t < d.L; ++t) gmax = std::max(gmax, std::abs((double)g[t]));
         // normal equations of the cubic fit (same for every block)
@@ -597,12 +602,9 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
         }
         if (ok) {
           d.pool_mode = 1;
-          P.wtab.insert(P.wtab.end(), tab.begin(), tab.end());
+          mom_tabs[ai] = std::move(tab);
         }
       }
-      if (d.pool_mode == 0)
-        for (int t = 0; t < d.L; ++t)
-          for (int m = 0; m < NF; ++m) P.wtab.push_back((float)tap(m, t));
     }
   }
   // micro-batch: one micro-batch's workspace <= 16 GiB (HBM is 180 GB; larger
@@ -615,7 +617,26 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     const size_t per = ws_layout(P, 1).total;
     P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ws_budget / std::max<size_t>(per, 1)));
   }
-  plan_tc(P);
+  if (P.kd_impl == 1) {
+    const std::string e = plan_tc(P);
+    if (!e.empty()) return e + " (JTFS_KD_SIMT selects the SIMT validation KD)";
+  }
+  // phi_T pooling tables per alpha: cubic-moment coefficients where plan_tc kept the
+  // moment form, else the exact taps [L][NF]
+  {
+    const int NF = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
+    for (size_t ai = 0; ai < P.kd.size(); ++ai) {
+      auto& d = P.kd[ai];
+      d.wtab_off = (int64_t)P.wtab.size();
+      if (d.pool_mode == 1 && P.kd_impl == 1) {
+        P.wtab.insert(P.wtab.end(), mom_tabs[ai].begin(), mom_tabs[ai].end());
+      } else {
+        d.pool_mode = 0;
+        for (int t = 0; t < d.L; ++t)
+          for (int m = 0; m < NF; ++m) P.wtab.push_back((float)pool_tap(P, d, m, t));
+      }
+    }
+  }
   P.part_total = 0;
   for (auto& d : P.kd) {
     d.nslices = d.nchunks * (P.kd_impl == 1 ? 2 : 1);  // tcgen05 KD: one slice per epilogue set
@@ -710,8 +731,8 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   w.ys = al((size_t)mb * p.ys_total * 4);
   w.part = al((size_t)mb * p.part_total * 4);
   {
-    size_t nsel = 0;  // jtfs_forward_units' chunk lists (at most one id per 64-column chunk)
-    for (const auto& d : p.kd) nsel += (size_t)std::max(1, d.L / 64);
+    size_t nsel = 0;  // jtfs_forward_units' chunk lists (at most one id per chunk)
+    for (const auto& d : p.kd) nsel += (size_t)std::max(1, d.L / 32);  // chunks >= 32 columns
     w.sel = al(nsel * 4);
   }
   w.flag = 256;

@@ -26,6 +26,7 @@ JTFS_OK, JTFS_ERR_INVALID_ARG, JTFS_ERR_UNSUPPORTED, JTFS_ERR_OOM = 0, 1, 2, 3
 JTFS_ERR_CUDA, JTFS_ERR_WORKSPACE, JTFS_ERR_NONFINITE = 4, 5, 6
 JTFS_CHECK_FINITE = 1
 JTFS_LATENCY = 2
+JTFS_KD_SIMT, JTFS_POOL_EXACT, JTFS_KD_PROF = 4, 8, 16   # validation / measurement plan flags
 JTFS_PAD_REFLECT, JTFS_PAD_PERIODIC = 0, 1
 PATH_SPIN, PATH_PSI_T_PHI_F, PATH_PHI_T_PSI_F, PATH_PHI_T_PHI_F = 0, 1, 2, 3
 
@@ -235,12 +236,22 @@ class Plan:
         return [ms[i] for i in range(n)]
 
     # ---- compute (torch tensors on the plan's device) ----
-    def workspace(self, batch: int):
+    def workspace(self, batch: int, stream=None):
+        """The cached workspace of `stream` (one per stream: forwards on different streams
+        never share buffers; a buffer that grows is released only through the caching
+        allocator's stream-ordered free, on the stream that used it)."""
         import torch
         need = self.workspace_size(batch)
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
-        return self._ws
+        key = _stream_handle(stream)
+        if self._ws is None:
+            self._ws = {}
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < need:
+            if ws is not None and stream is not None:
+                ws.record_stream(stream if isinstance(stream, torch.cuda.Stream) else torch.cuda.current_stream())
+            ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._ws[key] = ws
+        return ws
 
     def forward(self, x, out=None, stream=None):
         """x: float32 CUDA tensor [B, N] (contiguous) -> out [B, floats_per_signal]."""
@@ -249,7 +260,7 @@ class Plan:
         B = x.shape[0]
         if out is None:
             out = torch.empty(B, self.floats_per_signal, dtype=torch.float32, device=x.device)
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_forward(self._h, _ptr(x), B, _ptr(out), _ptr(ws), ws.numel(),
                                  _stream_handle(stream)), "jtfs_forward")
         return out
@@ -257,7 +268,7 @@ class Plan:
     def forward_host(self, x_host, out_host, x_dev, out_dev, stream=None):
         """End to end through the C ABI with HOST buffers (pinned torch CPU tensors)."""
         B = x_host.shape[0]
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_forward_host(self._h, _ptr(x_host), B, _ptr(out_host), _ptr(x_dev), _ptr(out_dev),
                                       _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_forward_host")
         return out_host
@@ -282,7 +293,7 @@ class Plan:
         """KA..KC + S0/S1 into out + KD partials of the listed units (others zeroed)."""
         B = x.shape[0]
         ids = (C.c_int32 * max(len(unit_ids), 1))(*[int(i) for i in unit_ids])
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_forward_units(self._h, _ptr(x), B, ids, len(unit_ids), _ptr(partials), _ptr(out),
                                        _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_forward_units")
         return partials, out
@@ -290,7 +301,7 @@ class Plan:
     def reduce_pack(self, partials, out, stream=None):
         """phi_F pooling + phi paths + packing of S2 from summed partials (same workspace)."""
         B = partials.shape[0]
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_reduce_pack(self._h, _ptr(partials), B, _ptr(out), _ptr(ws), ws.numel(),
                                      _stream_handle(stream)), "jtfs_reduce_pack")
         return out
@@ -339,7 +350,7 @@ class Plan:
         lay = self.scat1d_layout
         if out is None:
             out = torch.empty(B, lay.floats_per_signal, dtype=torch.float32, device=x.device)
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_scattering1d(self._h, _ptr(x), B, _ptr(out), _ptr(ws), ws.numel(),
                                       _stream_handle(stream)), "jtfs_scattering1d")
         return out
@@ -357,7 +368,7 @@ class Plan:
         n = C.c_int64()
         _check(_lib.jtfs_debug_tap_size(self._h, tap, B, C.byref(n)), "jtfs_debug_tap_size")
         out = torch.empty(int(n.value), dtype=torch.float32, device=x.device)
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_debug_tap(self._h, tap, _ptr(x), B, _ptr(out), out.numel(), _ptr(ws), ws.numel(),
                                    _stream_handle(None)), "jtfs_debug_tap")
         return out
@@ -389,7 +400,7 @@ class Plan:
         B = x.shape[0]
         if out is None:
             out = torch.empty(B, self.floats_per_signal, dtype=torch.float32, device=x.device)
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_forward_mulog(self._h, _ptr(x), B, _ptr(mu), float(eps), _ptr(out), _ptr(ws),
                                        ws.numel(), _stream_handle(stream)), "jtfs_forward_mulog")
         return out
@@ -407,7 +418,7 @@ class Plan:
         B = x.shape[0]
         if out is None:
             out = torch.empty(B, rows, cols, dtype=torch.float32, device=x.device)
-        ws = self.workspace(B)
+        ws = self.workspace(B, stream)
         _check(_lib.jtfs_u2_map(self._h, _ptr(x), B, path, _ptr(out), _ptr(ws), ws.numel(),
                                 _stream_handle(stream)), "jtfs_u2_map")
         return out

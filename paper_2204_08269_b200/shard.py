@@ -55,15 +55,26 @@ def forward_sharded(plan, x, group=None, stream=None):
     units = plan.units()
     mine = lpt_assign([u["cost"] for u in units], world)[rank]
     B = x.shape[0]
-    partials = torch.empty(B, plan.partials_size, dtype=torch.float32, device=x.device)
-    out = torch.empty(B, plan.floats_per_signal, dtype=torch.float32, device=x.device)
-    plan.forward_units(x, mine, partials, out, stream=stream)
-    if world > 1:
-        exchange_partials(partials, group=group, dst=0)
-    if rank != 0:
-        return None
-    plan.reduce_pack(partials, out, stream=stream)
+    # every step (KD, the NCCL reduce, KE) is ordered on ONE stream: torch's collectives
+    # run on the current stream, so a caller's stream becomes the current one here
+    with torch.cuda.stream(stream) if stream is not None else _nullctx():
+        partials = torch.empty(B, plan.partials_size, dtype=torch.float32, device=x.device)
+        out = torch.empty(B, plan.floats_per_signal, dtype=torch.float32, device=x.device)
+        plan.forward_units(x, mine, partials, out)
+        if world > 1:
+            exchange_partials(partials, group=group, dst=0)
+        if rank != 0:
+            return None
+        plan.reduce_pack(partials, out)
     return out
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 # ---- batch sharding (configs c3 / c5): signals are independent ----
@@ -108,6 +119,8 @@ def forward_batch_sharded(plan, x_full, group=None, gather: bool = True, stream=
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    import torch
     b0, b1 = batch_slice(x_full.shape[0], world, rank)
-    out = plan.forward(x_full[b0:b1].contiguous(), stream=stream)
-    return gather_outputs(out, x_full.shape[0], group) if gather else out
+    with torch.cuda.stream(stream) if stream is not None else _nullctx():  # forward and gather on one stream
+        out = plan.forward(x_full[b0:b1].contiguous())
+        return gather_outputs(out, x_full.shape[0], group) if gather else out

@@ -13,6 +13,11 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
-def pytest_collection_modifyitems(config, items):
-    # gpu tests must never silently pass on a CPU box: if no GPU is visible they fail loudly
-    pass
+@pytest.fixture(autouse=True)
+def _gpu_tests_need_a_gpu(request):
+    """A selected `gpu` test fails loudly (never skips or silently passes) when no CUDA
+    device is visible: there is no CPU fallback of the path to test instead."""
+    if request.node.get_closest_marker("gpu") is not None:
+        import torch
+        if not torch.cuda.is_available():
+            pytest.fail("gpu test selected but no CUDA device is visible (run with -m 'not gpu' on a CPU box)")

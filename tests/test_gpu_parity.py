@@ -150,14 +150,13 @@ def test_c3_full_size_sampled_paths(jt):
 
 @pytest.mark.parametrize("kw", [C1, dict(N=2 ** 13, J=8, Q=16, J_fr=4, T=2 ** 13, F=16, average_fr=False),
                                 dict(N=2 ** 16, J=12, Q=16, J_fr=5, T=2 ** 13, F=4)], ids=["c1", "c2", "c3"])
-def test_kd_tensor_core_matches_simt(jt, kw, monkeypatch):
-    # the tcgen05 3xTF32 contraction against the FP32 SIMT one on the same inputs
+def test_kd_tensor_core_matches_simt(jt, kw):
+    # consistency (not parity) check: the tcgen05 fp16-split contraction against the FP32
+    # SIMT validation kernel (plan flag JTFS_KD_SIMT) on the same inputs
     import torch
     X = signals.notes(2, N=kw["N"], seed0=77) if kw["N"] >= 2 ** 13 else _c1_inputs()
     x = torch.from_numpy(np.ascontiguousarray(X)).cuda()
-    monkeypatch.setenv("JTFS_KD", "simt")
-    a = jt.Plan(**kw).forward(x).cpu().numpy().astype(np.float64)
-    monkeypatch.setenv("JTFS_KD", "tc")
+    a = jt.Plan(**kw, flags=jt.JTFS_KD_SIMT).forward(x).cpu().numpy().astype(np.float64)
     b = jt.Plan(**kw).forward(x).cpu().numpy().astype(np.float64)
     for i in range(len(X)):
         assert np.linalg.norm(a[i] - b[i]) <= 1e-5 * np.linalg.norm(a[i])
@@ -212,13 +211,11 @@ def test_paper_preset_sampled_paths(jt):
     _check_signal(plan, out[1], X[1].astype(np.float64), prm, paths=sample)
 
 
-def test_kd_tensor_core_matches_simt_paper_preset(jt, monkeypatch):
+def test_kd_tensor_core_matches_simt_paper_preset(jt):
     import torch
     X = signals.notes(2, seed0=91)
     x = torch.from_numpy(np.ascontiguousarray(X)).cuda()
-    monkeypatch.setenv("JTFS_KD", "simt")
-    a = jt.Plan(**P42).forward(x).cpu().numpy().astype(np.float64)
-    monkeypatch.setenv("JTFS_KD", "tc")
+    a = jt.Plan(**P42, flags=jt.JTFS_KD_SIMT).forward(x).cpu().numpy().astype(np.float64)
     b = jt.Plan(**P42).forward(x).cpu().numpy().astype(np.float64)
     for i in range(len(X)):
         assert np.linalg.norm(a[i] - b[i]) <= 1e-5 * np.linalg.norm(a[i])
