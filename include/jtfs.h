@@ -354,6 +354,26 @@ JTFS_API jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* 
 /* Size in floats of a debug tap for B signals. */
 JTFS_API jtfs_status jtfs_debug_tap_size(jtfs_plan_t plan, int32_t tap, int64_t B, int64_t* floats);
 
+/* Joint stage alone (validation of KD + KE, SURVEY §4 T4 invariants and stage parity):
+ * Eqs. (1)-(3) / (4) from a given Y2 and Y_phi instead of from x.
+ *   y2    device fp32 [B][...] in the layout of debug tap 2 (per alpha a (2K) x L_alpha
+ *         planar block, rows 2 lambda / 2 lambda + 1 = Re / Im Y2_alpha[lambda])
+ *   yphi  device fp32 [B][n1][N_pad/T] in the layout of debug tap 3
+ *   out   device fp32 [B][floats_per_signal]: S0 / S1 zero, S2 = the joint stage
+ * B <= one micro-batch; workspace as for jtfs_forward; asynchronous on `stream`. */
+JTFS_API jtfs_status jtfs_debug_joint(jtfs_plan_t plan, const float* y2, const float* yphi, int64_t B,
+                             float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* The FFT engine alone on contiguous complex rows: out[r] = DFT of in[r]
+ * (dir -1: sum_n x[n] e^{-2 pi i n k / L}) or the unnormalised inverse (dir +1), L = 2^log2L.
+ *   fp64 = 0: float2 rows (the fp32 engine of KB / KC, both directions, L <= N_pad);
+ *   fp64 = 1: double2 rows (the fp64 engine of KA, forward only).
+ * in / out device, 16-B aligned, rows x L elements; tmp: device scratch of rows x L
+ * elements (the four-step intermediate).  Asynchronous on `stream`. */
+JTFS_API jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir, int32_t fp64,
+                           const void* in, void* out, int64_t rows, void* tmp, size_t tmp_bytes,
+                           void* stream);
+
 /* Host copy of a sampled filter spectrum as the plan generated it (fp64), for
  * cross-checking the plan generator against the oracle's independent one.
  *   bank 1: psi_lambda, 2: psi_alpha, 3: psi_beta (theta=-1), 4: phi_T, 5: phi_F

@@ -220,6 +220,7 @@ struct RunOpts {
   bool skip_ke = false;
   const float* mu = nullptr;  // fused mu-log in KE (jtfs_forward_mulog)
   float mu_eps = 0.f;
+  bool joint_only = false;  // jtfs_debug_joint: Y2 / Y_phi already in the workspace, run KD + KE only
 };
 
 void fill_ke_params(jtfs::Plan& P, jtfs::KEParams& kp, const float* part, const float* yphi, float* out);
@@ -229,17 +230,19 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   using namespace jtfs;
   jtfs_layout_t lay;
   layout_of(P, &lay);
-  { StageScope s(P, 0, st); s.done(launch_pad_fft(P, x, nb, w.xhat, w.tmp, st)); }
-  if (upto_stage == 0) return "";
-  { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st, w.tmp2)); }
-  {
-    StageScope s(P, 2, st);
-    s.done(launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, out, lay.floats_per_signal, lay.off_s0, lay.off_s1,
-                            P.d_u1_off, P.d_k1, P.d_band_L1, st));
+  if (!o.joint_only) {
+    { StageScope s(P, 0, st); s.done(launch_pad_fft(P, x, nb, w.xhat, w.tmp, st)); }
+    if (upto_stage == 0) return "";
+    { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st, w.tmp2)); }
+    {
+      StageScope s(P, 2, st);
+      s.done(launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, out, lay.floats_per_signal, lay.off_s0, lay.off_s1,
+                              P.d_u1_off, P.d_k1, P.d_band_L1, st));
+    }
+    if (upto_stage == 1) return "";
+    { StageScope s(P, 3, st); s.done(launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
+    if (upto_stage == 2) return "";
   }
-  if (upto_stage == 1) return "";
-  { StageScope s(P, 3, st); s.done(launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
-  if (upto_stage == 2) return "";
   {
     StageScope s(P, 4, st);
     int err = 0;
@@ -926,6 +929,50 @@ jtfs_status jtfs_debug_tap(jtfs_plan_t plan, int32_t tap, const float* x, int64_
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "debug tap launch");
   return JTFS_OK;
+}
+
+jtfs_status jtfs_debug_joint(jtfs_plan_t plan, const float* y2, const float* yphi, int64_t B, float* out, void* ws,
+                             size_t ws_bytes, void* stream) {
+  jtfs_status s = check_forward_args(plan, y2, B, out, ws, ws_bytes);
+  if (s != JTFS_OK || B == 0) return s;
+  jtfs::Plan& P = plan->P;
+  if (B > P.mb) return fail(JTFS_ERR_INVALID_ARG, "debug_joint takes at most one micro-batch");
+  if (!yphi || !aligned(yphi, 16)) return fail(JTFS_ERR_INVALID_ARG, "yphi NULL or misaligned");
+  DeviceGuard guard(P.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  WsPtrs w = carve(P, ws, B);
+  jtfs_layout_t lay;
+  layout_of(P, &lay);
+  cudaError_t e = cudaMemcpyAsync(w.y2, y2, (size_t)B * P.y2_total * 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(w.yphi, yphi, (size_t)B * P.n1 * P.NPT * 4, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out, 0, (size_t)B * lay.floats_per_signal * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "debug_joint copies");
+  RunOpts o;
+  o.joint_only = true;
+  const std::string err = run_microbatch(P, nullptr, (int)B, out, w, false, 99, st, o);
+  if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
+  e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
+}
+
+jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir, int32_t fp64, const void* in, void* out,
+                           int64_t rows, void* tmp, size_t tmp_bytes, void* stream) {
+  if (!plan) return fail(JTFS_ERR_INVALID_ARG, "plan is NULL");
+  jtfs::Plan& P = plan->P;
+  if (P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");
+  if (log2L < 1 || (1LL << log2L) > P.N_tw) return fail(JTFS_ERR_INVALID_ARG, "need 2 <= 2^log2L <= N_pad");
+  if (dir != -1 && dir != 1) return fail(JTFS_ERR_INVALID_ARG, "dir must be -1 or +1");
+  if (fp64 && dir != -1) return fail(JTFS_ERR_UNSUPPORTED, "the fp64 engine is forward only (KA)");
+  if (rows < 0 || rows > (1 << 30)) return fail(JTFS_ERR_INVALID_ARG, "bad row count");
+  if (rows == 0) return JTFS_OK;
+  if (!in || !out || !aligned(in, 16) || !aligned(out, 16)) return fail(JTFS_ERR_INVALID_ARG, "NULL or misaligned");
+  const size_t need = (size_t)rows * ((size_t)1 << log2L) * (fp64 ? 16 : 8);
+  if (!tmp || tmp_bytes < need) return fail(JTFS_ERR_WORKSPACE, "tmp must hold rows x L complex");
+  DeviceGuard guard(P.device);
+  jtfs::launch_debug_fft(P, log2L, dir, fp64 != 0, in, out, (int)rows, tmp, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
 }
 
 jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap) {

@@ -119,6 +119,16 @@ struct ProbRealFwd {  // U1 (real) -> U1hat
   }
 };
 
+template <class T>
+struct ProbPlain {  // jtfs_debug_fft: contiguous complex rows in -> rows out (the bare FFT engine)
+  using CT = T;
+  const T* in;
+  T* out;
+  int L;
+  __device__ T load(int rho, int i) const { return in[(int64_t)rho * L + i]; }
+  __device__ void store(int rho, int o, T v) const { out[(int64_t)rho * L + o] = v; }
+};
+
 // ---------------------------------------------------------------------------------
 // single-CTA FFT of G rows per block
 // ---------------------------------------------------------------------------------
@@ -998,6 +1008,35 @@ void dispatch_log2(int lg, F&& f) {
   }
 }
 }  // namespace
+
+// jtfs_debug_fft: the FFT engine on plain rows (fp32: both directions, lengths 2^1..2^18;
+// fp64: forward, 2^1..2^18), with the plan's twiddle tables (L <= N_pad)
+int launch_debug_fft(const Plan& P, int log2L, int dir, bool fp64, const void* in, void* out, int nrows, void* tmp,
+                     cudaStream_t st) {
+  const int ltw = ilog2_exact(P.N_tw);
+  int n = 0;
+  dispatch_log2(log2L, [&](auto c) {
+    constexpr int LG = decltype(c)::value;
+    if (fp64) {
+      ProbPlain<double2> pr{(const double2*)in, (double2*)out, 1 << LG};
+      const double2* W = (const double2*)P.d_twiddle64;
+      if constexpr (LG <= 11) launch_rows<LG, -1>(pr, nrows, W, ltw, st);
+      else launch_fft4<LG, -1>(pr, pr, nrows, (double2*)tmp, W, ltw, st);
+    } else {
+      ProbPlain<float2> pr{(const float2*)in, (float2*)out, 1 << LG};
+      const float2* W = (const float2*)P.d_twiddle;
+      if constexpr (LG <= 12) {
+        if (dir < 0) launch_rows<LG, -1>(pr, nrows, W, ltw, st);
+        else launch_rows<LG, +1>(pr, nrows, W, ltw, st);
+      } else {
+        if (dir < 0) launch_fft4<LG, -1>(pr, pr, nrows, (float2*)tmp, W, ltw, st);
+        else launch_fft4<LG, +1>(pr, pr, nrows, (float2*)tmp, W, ltw, st);
+      }
+    }
+    n = LG <= (fp64 ? 11 : 12) ? 1 : 2;
+  });
+  return n;
+}
 
 int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2* tmp, cudaStream_t st) {
   // fp64 DFT of the padded signal: a fp32 FFT's roundoff is proportional to the

@@ -33,7 +33,7 @@ PATH_SPIN, PATH_PSI_T_PHI_F, PATH_PHI_T_PSI_F, PATH_PHI_T_PHI_F = 0, 1, 2, 3
 EXPORTS = [
     "jtfs_plan", "jtfs_plan_create", "jtfs_plan_destroy", "jtfs_layout", "jtfs_paths",
     "jtfs_lambda_xi", "jtfs_workspace_size", "jtfs_forward", "jtfs_forward_host",
-    "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_cost", "jtfs_profile_enable",
+    "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_debug_joint", "jtfs_debug_fft", "jtfs_cost", "jtfs_profile_enable",
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
@@ -84,6 +84,8 @@ _lib.jtfs_forward.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_forward_host.argtypes = [_P, _P, C.c_int64, _P, _P, _P, _P, C.c_size_t, _P]
 _lib.jtfs_debug_tap.argtypes = [_P, C.c_int32, _P, C.c_int64, _P, C.c_int64, _P, C.c_size_t, _P]
 _lib.jtfs_debug_tap_size.argtypes = [_P, C.c_int32, C.c_int64, C.POINTER(C.c_int64)]
+_lib.jtfs_debug_joint.argtypes = [_P, _P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
+_lib.jtfs_debug_fft.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_int64, _P, C.c_size_t, _P]
 _lib.jtfs_debug_filter.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
 _lib.jtfs_cost.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32]
 _lib.jtfs_profile_enable.argtypes = [_P, C.c_int32]
@@ -371,6 +373,33 @@ class Plan:
         ws = self.workspace(B, stream)
         _check(_lib.jtfs_debug_tap(self._h, tap, _ptr(x), B, _ptr(out), out.numel(), _ptr(ws), ws.numel(),
                                    _stream_handle(None)), "jtfs_debug_tap")
+        return out
+
+    def debug_joint(self, y2, yphi, out=None, stream=None):
+        """Joint stage (KD + KE) from given Y2 (tap-2 layout, float32 CUDA [B, 2 y2_total])
+        and Y_phi (tap-3 layout, [B, n1 * N_pad/T]) -> out [B, floats_per_signal]."""
+        import torch
+        assert y2.dtype == torch.float32 and y2.is_cuda and y2.is_contiguous() and y2.dim() == 2
+        assert yphi.dtype == torch.float32 and yphi.is_cuda and yphi.is_contiguous()
+        B = y2.shape[0]
+        if out is None:
+            out = torch.empty(B, self.floats_per_signal, dtype=torch.float32, device=y2.device)
+        ws = self.workspace(B, stream)
+        _check(_lib.jtfs_debug_joint(self._h, _ptr(y2), _ptr(yphi), B, _ptr(out), _ptr(ws), ws.numel(),
+                                     _stream_handle(stream)), "jtfs_debug_joint")
+        return out
+
+    def debug_fft(self, x, dir: int = -1, stream=None):
+        """The FFT engine on rows of x (complex64 -> fp32 engine, complex128 -> fp64 engine)."""
+        import torch
+        assert x.is_cuda and x.is_contiguous() and x.dim() == 2 and x.dtype in (torch.complex64, torch.complex128)
+        rows, L = x.shape
+        lg = L.bit_length() - 1
+        out = torch.empty_like(x)
+        tmp = torch.empty_like(x)
+        _check(_lib.jtfs_debug_fft(self._h, lg, dir, int(x.dtype == torch.complex128), _ptr(x), _ptr(out), rows,
+                                   _ptr(tmp), tmp.numel() * tmp.element_size(), _stream_handle(stream)),
+               "jtfs_debug_fft")
         return out
 
     # ---- NEXT-4: mu-log (Eqs. (adalog:mu), (adalog), P:284-296) and the Fig. 1 map ----

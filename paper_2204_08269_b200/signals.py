@@ -75,6 +75,14 @@ def note(N: int = 2 ** 16, fs: float = 22050.0, seed: int = 1000) -> np.ndarray:
     return (0.9 * y / np.max(np.abs(y))).astype(np.float32)
 
 
+def note_glissando(seed: int) -> float:
+    """The glissando rate (octaves/s, 0 = none) that note(seed=seed) draws -- the same
+    draws in the same order as note(), so tests can pick glissandi (Fig. 1b)."""
+    rng = np.random.default_rng(seed)
+    rng.uniform(), rng.uniform(), rng.uniform(4, 7), rng.uniform(0, 30)
+    return rng.uniform(-1, 1) if rng.uniform() < 0.2 else 0.0
+
+
 def notes(B: int, N: int = 2 ** 16, fs: float = 22050.0, seed0: int = 1000) -> np.ndarray:
     """Config c3 batch: seeds seed0 + i."""
     return np.stack([note(N, fs, seed0 + i) for i in range(B)])

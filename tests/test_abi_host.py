@@ -154,3 +154,22 @@ def test_u2_map_shape_matches_oracle(jt, name):
                 plan.u2_map_shape(pi)
     with pytest.raises(jt.JTFSError):
         plan.u2_map_shape(len(s.paths))
+
+
+def test_library_reads_no_environment():
+    # output bytes are a function of (plan params incl. flags, x) only: no source of the
+    # library consults the process environment (env-dependent outputs)
+    csrc = os.path.join(ROOT, "paper_2204_08269_b200", "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in src, f
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+def test_every_benchmarked_config_plans_on_the_tensor_cores(jt, name):
+    # plan creation runs the tensor-core tiling (plan_tc); a config it cannot tile is an
+    # explicit error unless JTFS_KD_SIMT is requested -- never a silent second backend
+    p = hostplan(jt, **CFGS[name])
+    assert p.floats_per_signal > 0
+    q = hostplan(jt, **CFGS[name], flags=jt.JTFS_KD_SIMT)
+    assert q.floats_per_signal == p.floats_per_signal

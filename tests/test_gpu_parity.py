@@ -264,3 +264,134 @@ def test_forward_host_buffers_and_batch_sharded_helper(jt):
     got = shard.forward_batch_sharded(plan, x).cpu()
     assert torch.equal(got, ref)
     assert shard.batch_slice(len(X), 1, 0) == (0, len(X))
+
+
+# ---- joint stage alone (jtfs_debug_joint): stage parity and SURVEY §4 T4 invariants ----
+def _y2_layout(s):
+    """[(alpha, K, L, float offset)] of the tap-2 / debug_joint Y2 layout."""
+    out, off = [], 0
+    for a in s.alphas:
+        K, L = len(s.adm[a]), s.N_pad >> s.k_alpha[a]
+        out.append((a, K, L, off))
+        off += 2 * K * L
+    return out, off
+
+
+def _pack_y2(s, Y2):
+    lay, total = _y2_layout(s)
+    flat = np.zeros(total, dtype=np.float32)
+    for a, K, L, off in lay:
+        blk = np.empty((2 * K, L), dtype=np.float32)
+        blk[0::2] = Y2[a].real
+        blk[1::2] = Y2[a].imag
+        flat[off:off + 2 * K * L] = blk.ravel()
+    return flat
+
+
+def _random_y2(s, rng):
+    Y2 = {}
+    for a in s.alphas:
+        K, L = len(s.adm[a]), s.N_pad >> s.k_alpha[a]
+        scale = np.exp(rng.uniform(-2, 2, size=(K, 1)))        # rows of different magnitudes
+        Y2[a] = ((rng.standard_normal((K, L)) + 1j * rng.standard_normal((K, L))) * scale)
+        Y2[a] = Y2[a].astype(np.complex64).astype(np.complex128)
+    Yphi = rng.standard_normal((s.n1, s.N_pad // s.p.T)).astype(np.float32).astype(np.float64)
+    return Y2, Yphi
+
+
+def _joint_gpu(jt, plan, s, Y2s, Yphis):
+    import torch
+    y2 = torch.from_numpy(np.stack([_pack_y2(s, Y2) for Y2 in Y2s])).cuda()
+    yp = torch.from_numpy(np.stack([Yp.astype(np.float32).ravel() for Yp in Yphis])).cuda()
+    out = plan.debug_joint(y2, yp)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("variant", ["eq3", "eq4"])
+def test_joint_stage_parity_random_y2(jt, variant):
+    # KD + KE against the oracle's joint stage (steps O7-O9) on random complex Y2 whose
+    # rows span 4 decades -- stage-level parity independent of KA..KC
+    kw = dict(C1, average_fr=(variant == "eq3"))
+    prm = O.Params(**kw)
+    s = O.schedule(prm)
+    rng = np.random.default_rng(11)
+    ins = [_random_y2(s, rng) for _ in range(3)]
+    plan = jt.Plan(**kw)
+    out = _joint_gpu(jt, plan, s, [y for y, _ in ins], [p for _, p in ins])
+    for b, (Y2, Yphi) in enumerate(ins):
+        maps = O.joint_stage(Y2, Yphi, s)
+        _, _, s2 = plan.unpack(out[b])
+        o = [maps[i] for i in range(len(s.paths))]
+        e = path_errors(list(s2), o)
+        assert e.max() <= TOL, (float(e.max()), int(np.argmax(e)))
+
+
+@pytest.mark.parametrize("variant", ["eq3", "eq4"])
+def test_joint_separable_grid_equal_spins(jt, variant):
+    # T4: Y2_alpha[lambda][t] = a[lambda] b_alpha[t] with a REAL gives |psi_{beta,+1} *_lambda Y2|
+    # = |psi_{beta,-1} *_lambda Y2| exactly (h_{+1} = conj h_{-1}, R10), so the two spins'
+    # S2 maps of every (alpha, beta) coincide (P:74-75)
+    kw = dict(C1, average_fr=(variant == "eq3"))
+    s = O.schedule(O.Params(**kw))
+    rng = np.random.default_rng(5)
+    a_prof = rng.standard_normal(s.n1)
+    Y2 = {}
+    for a in s.alphas:
+        K, L = len(s.adm[a]), s.N_pad >> s.k_alpha[a]
+        b = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+        Y2[a] = np.outer(a_prof[:K], b)
+    Yphi = np.zeros((s.n1, s.N_pad // s.p.T))
+    plan = jt.Plan(**kw)
+    _, _, s2 = plan.unpack(_joint_gpu(jt, plan, s, [Y2], [Yphi])[0])
+    paths = plan.paths()
+    idx = {(k, th, a, b): i for i, (k, th, a, b, *_r) in enumerate(paths)}
+    for (k, th, a, b), i in idx.items():
+        if k == jt.PATH_SPIN and th == -1:
+            j = idx[(k, +1, a, b)]
+            ref = np.linalg.norm(s2[i]) + 1e-30
+            assert np.linalg.norm(s2[i] - s2[j]) <= 1e-5 * ref, (a, b)
+
+
+def test_joint_lambda_reversal_swaps_spins(jt):
+    # T4: reversing the admissible rows, Y2'[lambda] = Y2[K-1-lambda], maps Z_theta(Y2')[r]
+    # to Z_{-theta}(Y2)[K-1-r] on the circular lambda grid (h_theta[n] = h_{-theta}[-n], R9/R10);
+    # Eq. (4) keeps every row at full rate, so S2'(theta)[r] = S2(-theta)[K-1-r], r < K
+    kw = dict(C1, average_fr=False)
+    s = O.schedule(O.Params(**kw))
+    rng = np.random.default_rng(8)
+    a0 = s.alphas[0]
+    Y2, Y2r = {}, {}
+    for a in s.alphas:
+        K, L = len(s.adm[a]), s.N_pad >> s.k_alpha[a]
+        Y2[a] = (rng.standard_normal((K, L)) + 1j * rng.standard_normal((K, L))) if a == a0 else np.zeros((K, L))
+        Y2r[a] = Y2[a][::-1].copy()
+    Yphi = np.zeros((s.n1, s.N_pad // s.p.T))
+    plan = jt.Plan(**kw)
+    out = _joint_gpu(jt, plan, s, [Y2, Y2r], [Yphi, Yphi])
+    _, _, s2 = plan.unpack(out[0])
+    _, _, s2r = plan.unpack(out[1])
+    K = len(s.adm[a0])
+    paths = plan.paths()
+    idx = {(k, th, a, b): i for i, (k, th, a, b, *_r) in enumerate(paths)}
+    checked = 0
+    for (k, th, a, b), i in idx.items():
+        if k == jt.PATH_SPIN and a == a0:
+            j = idx[(k, -th, a, b)]
+            got, ref = s2r[i][:K], s2[j][:K][::-1]
+            assert np.linalg.norm(got - ref) <= 1e-5 * (np.linalg.norm(ref) + 1e-30), (th, b)
+            checked += 1
+    assert checked == 2 * plan.layout.n_beta
+
+
+def test_c3_batch_independence_bench_launch(jt):
+    # the bench's 256-signal launch (4 micro-batches of 64) gives each signal the same bytes
+    # as a forward of that signal alone (per-signal work decomposition independent of B)
+    import torch
+    kw = dict(N=2 ** 16, J=12, Q=16, J_fr=5, T=2 ** 13, F=4)
+    plan = jt.Plan(**kw)
+    X = torch.from_numpy(signals.notes(256, seed0=1000)).cuda()
+    full = plan.forward(X)
+    for b in (0, 1, 63, 64, 130, 255):
+        one = plan.forward(X[b:b + 1].contiguous())
+        assert torch.equal(full[b:b + 1].view(torch.int32), one.view(torch.int32)), b
