@@ -24,6 +24,9 @@ step; ms per iteration (lower is better), E after 20 and 100 iterations.
 `--workload c2` (BASELINE configs[1]): JTFS of the 16^3 AM/FM chirp grid
 (Eq. (4)) + K = 40 nearest-neighbour regression of (f_c, f_m, gamma); signals/s.
 
+`--workload c5` (BASELINE configs[4]): the c3 plan on white-noise batches of 64 ... 4096
+signals per GPU (`--c5-batches`), one JSON line per batch size.
+
 `--workload c4` (not the headline metric): latency of ONE long
 signal (bird texture, N = 2^17, J = 13) path-sharded over the ranks
 (paper_2204_08269_b200/shard.py: KD units split by LPT, partials summed onto
@@ -68,25 +71,34 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+# the canonical algorithmic count of the c3 path -- 21.5 GFLOP per signal for the
+# whole path, of which the joint stage a5 + a6 (the lambda contraction, modulus and phi_T
+# pooling that k_kd_tc executes) is 20.6 GFLOP: per alpha the cheaper of the direct
+# lambda-contraction and the FFT-along-lambda form, taps at +-5 sigma.
+C3_PATH_FLOP = 21.5e9
+C3_KD_FLOP = 20.6e9
+
+
 def _kd_traffic():
-    """dram__bytes_read + dram__bytes_write of one alpha-0 KD launch (64 signals) from the
-    committed ncu --set full capture (profiles/kd_traffic.json); None if absent."""
+    """ncu DRAM bytes of one alpha-0 k_kd_tc launch (64 signals) from the committed
+    `ncu --set full` capture (profiles/kd_traffic.json), next to the Y2 bytes SURVEY §8(d)
+    counts for that launch (the Y2_alpha0 exchange: read once); None if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "kd_traffic.json")) as f:
             k = json.load(f)
         return {"bytes_per_launch": k["dram_bytes_read"] + k["dram_bytes_write"],
-                "algorithmic_bytes_per_launch": k["algorithmic_bytes_read"] + k["algorithmic_bytes_write"],
+                "read": k["dram_bytes_read"], "write": k["dram_bytes_write"],
+                "survey_y2_bytes_per_launch": k.get("survey_y2_bytes"),
                 "launch": k["kernel"], "source": k["source"]}
     except Exception:
         return None
 
 
-def _path_roofline(signals_per_s_per_gpu, clocks):
-    mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    peak = 148 * 128 * 2 * mhz * 1e6 / 1e12  # FP32 FMA lanes x 2 flop x clock (TFLOP/s)
-    ach = 21.5e9 * signals_per_s_per_gpu / 1e12
-    return {"basis": "SURVEY 8(d) canonical 21.5 GFLOP per c3 signal", "achieved_tflops": round(ach, 2),
-            "fp32_simt_peak_tflops": round(peak, 2), "clock_mhz": mhz, "frac": round(ach / peak, 4),
+def _path_roofline(signals_per_s_per_gpu, peak_tflops, clocks, how):
+    ach = C3_PATH_FLOP * signals_per_s_per_gpu / 1e12
+    return {"basis": "SURVEY 8(d) canonical 21.5 GFLOP per c3 signal (whole path)",
+            "achieved_tflops": round(ach, 2), "fp32_simt_peak_tflops": round(peak_tflops, 2),
+            "peak_source": how, "clock_mhz": (clocks or {}).get("sm_mhz"), "frac": round(ach / peak_tflops, 4),
             "note": "the contraction runs on the tensor cores, so the path can exceed the SIMT roofline"}
 
 
@@ -129,23 +141,39 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(sample_signals: int = 1):
-    """The fp64 oracle as it stands, on the host cores, on c3 notes."""
+def cpu_baseline_and_parity(plan, X, out_gpu):
+    """The fp64 oracle as it stands on the host cores, threaded over signals (one
+    single-threaded worker process per core, tests/oracle_pool.py), on the first n signals
+    of the bench's own batch; its records also give the parity of the GPU records of the
+    same signals (SURVEY §8(c) metric, tests/parity.py)."""
     import numpy as np
-    from oracle import jtfs_oracle as O
-    from paper_2204_08269_b200 import signals
+    from tests import oracle_pool
+    from tests.parity import path_blocks, path_errors, unfloored_errors, TOL
     cores = os.cpu_count() or 1
-    O.set_workers(cores)
-    prm = O.Params(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], T=CFG["T"], F=CFG["F"])
-    s = O.schedule(prm)
-    X = signals.notes(sample_signals, seed0=1000)
+    n = int(min(32, max(8, cores), X.shape[0]))
+    okw = {k: CFG[k] for k in ("N", "J", "Q", "J_fr", "T", "F")}
+    pool = oracle_pool.pool()
+    list(pool.map(int, range(cores)))  # start the workers before the clock
     t0 = time.perf_counter()
-    for b in range(sample_signals):
-        O.jtfs_forward(X[b].astype(np.float64), prm, s=s)
+    futs = [oracle_pool.submit(okw, X[i]) for i in range(n)]
+    res = [f.result() for f in futs]
     dt = time.perf_counter() - t0
-    return {"value": sample_signals / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{sample_signals} c3 note signal(s), full forward JTFS in fp64, scipy.fft workers={cores}",
-            "seconds": dt}
+    errs, unf = [], []
+    for i, (S0, S1, S2) in enumerate(res):
+        g = path_blocks(*plan.unpack(out_gpu[i].astype(np.float64)))
+        o = path_blocks(S0, S1, S2)
+        errs.append(path_errors(g, o))
+        unf.append(unfloored_errors(g, o))
+    e = np.concatenate(errs)
+    cpu = {"value": n / dt, "unit": UNIT, "cores": min(cores, n), "kind": "oracle",
+           "sample": f"the first {n} c3 notes of this run's batch, full forward JTFS in fp64, "
+                     f"{min(cores, n)} single-threaded worker processes (threads over signals)",
+           "seconds": round(dt, 2), "host_cpus": cores}
+    parity = {"max": float(e.max()), "median": float(np.median(e)), "max_unfloored": float(np.concatenate(unf).max()),
+              "n_paths": int(len(errs[0])), "n_signals": n, "tol": TOL, "pass": bool(e.max() <= TOL),
+              "metric": "per-path floored relative L2 vs the fp64 oracle (SURVEY 8(c)); paths = S0, each S1 row, "
+                        "each S2 map"}
+    return cpu, parity
 
 
 def run_reference(args, rank, world):
@@ -355,6 +383,202 @@ def run_c2(args, rank, world, local, dev):
     return 0
 
 
+def _timed_steps(fn, steps, flush, stream):
+    """Per-step CUDA-event times (ms) of fn(), the L2 flushed (256 MiB write, untimed) before
+    every step."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        fn()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def _max_over_ranks(v, dev, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_c3(args, rank, world, local, dev):
+    """The headline: BASELINE configs[2] (c3), signals/s, batch-sharded over the ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2204_08269_b200 import jtfs, shard, signals
+
+    B = args.batch
+    plan = jtfs.Plan(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], Q_fr=CFG["Q_fr"], T=CFG["T"],
+                     F=CFG["F"], device=local)
+    fps = plan.floats_per_signal
+    X = signals.notes(B, seed0=1000 + rank * B)
+    x = torch.from_numpy(X).to(dev)
+    out = torch.empty(B, fps, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.forward(x, out)
+    torch.cuda.synchronize()
+    # FP32 SIMT peak probe (SURVEY 8(d)), measured here, before the timed region
+    ffma, ffma2 = jtfs.measure_fp32_peak(local)
+    for _ in range(2):
+        plan.forward(x, out)            # back to the steady state after the probe
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- headline: device-resident inputs, profiling OFF, L2 flushed between steps ----
+    plan.profile_read(reset=True)       # launch counters
+    clk = ClockSampler(local)
+    clk.start()
+    step_ms = _timed_steps(lambda: plan.forward(x, out), args.steps, flush, stream)
+    clocks = clk.stop()
+    launches = int(sum(v[1] for v in plan.profile_read(reset=True).values()))
+    total_ms = _max_over_ranks(sum(step_ms), dev, world)
+    value = B * world * args.steps / (total_ms / 1e3)
+
+    # ---- with C1 (SURVEY 8(e)): forward + all-gather of every rank's records ----
+    with_c1 = None
+    if world > 1:
+        xg = torch.from_numpy(np.concatenate([signals.notes(B, seed0=1000 + r * B) for r in range(world)])).to(dev)
+        shard.forward_batch_sharded(plan, xg, gather=True)
+        dist.barrier()
+        g_ms = _timed_steps(lambda: shard.forward_batch_sharded(plan, xg, gather=True), args.steps, flush, stream)
+        g_tot = _max_over_ranks(sum(g_ms), dev, world)
+        with_c1 = {"value": B * world * args.steps / (g_tot / 1e3), "ms_per_step": g_tot / args.steps,
+                   "collective": "NCCL all_gather_into_tensor of the fp32 records (shard.gather_outputs)"}
+        del xg
+
+    # ---- profiled pass (separate from the headline): per-stage and per-kernel events ----
+    n_prof = max(1, min(args.steps, 3))
+    plan.profile_read(reset=True)
+    plan.profile_read_kd(reset=True)
+    plan.profile_enable(True)
+    prof_ms = _timed_steps(lambda: plan.forward(x, out), n_prof, flush, stream)
+    plan.profile_enable(False)
+    prof = plan.profile_read(reset=True)
+    kd_alpha_ms = plan.profile_read_kd(reset=True)
+    kd_kernel_ms = sum(kd_alpha_ms) / n_prof           # k_kd_tc launches only (not k_ky), per step
+    stage_ms = {k: v[0] / n_prof for k, v in prof.items()}
+
+    # ---- end to end through the C ABI with pinned host buffers: same steps, same flush ----
+    xh = torch.from_numpy(X).pin_memory()
+    oh = torch.empty(B, fps, dtype=torch.float32).pin_memory()
+    xd = torch.empty_like(x)
+    plan.forward_host(xh, oh, xd, out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = _timed_steps(lambda: plan.forward_host(xh, oh, xd, out), args.steps, flush, stream)
+    e2e_tot = _max_over_ranks(sum(e2e_ms), dev, world)
+    e2e_value = B * world * args.steps / (e2e_tot / 1e3)
+
+    # ---- roofline of the dominant kernel: k_kd_tc on the tensor pipe (kind::f16) ----
+    cost = plan.cost()
+    peaks, src = _peaks()
+    f16_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+    kd_s = kd_kernel_ms / 1e3
+    kd_alg = C3_KD_FLOP * B / kd_s / 1e12
+    kd_recount = cost["KD_joint"][0] * B / kd_s / 1e12
+    kd_exec = cost["KD_tensor_executed"][0] * B / kd_s / 1e12
+    fp32_peak = max(ffma, ffma2)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "dtype_detail": "fp32 FFTs, modulus and pooling; KA DFT in fp64; KD contraction as a two-term "
+                            "fp16 split on the tensor cores (3 products, fp32 accumulation, ~2^-21 relative)",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
+                       "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                       "l2": "flushed before every timed step (256 MiB write)", **CFG},
+            "roofline": {"bound": "tensor",
+                         "kernel": "k_kd_tc (tcgen05 kind::f16 lambda contraction + |.| + phi_T pooling)",
+                         "achieved": kd_alg, "peak": f16_peak, "unit": "TFLOP/s", "frac": kd_alg / f16_peak,
+                         "traffic": _kd_traffic(),
+                         "algorithmic_flops_per_signal": C3_KD_FLOP,
+                         "algorithmic_basis": "SURVEY 8(d): a5 + a6 canonical per-alpha form, 20.6 GFLOP per c3 "
+                                              "signal, x signals / summed k_kd_tc launch time (CUDA events around "
+                                              "each launch on its stream; the alpha >= 5 launches share SMs with "
+                                              "the others, which only lengthens the denominator)",
+                         "kernel_ms_per_step": kd_kernel_ms,
+                         "peak_source": f"dense fp16 = {src} bf16_tflops_sustained (same nominal rate as bf16)",
+                         "secondary_recount": {"flops_per_signal": cost["KD_joint"][0], "achieved": kd_recount,
+                                               "frac": kd_recount / f16_peak,
+                                               "basis": "this build's recount of the exact operator in FFT-along-"
+                                                        "lambda form with untruncated taps (DESIGN.md 5)"},
+                         "executed_tensor_tflops": kd_exec, "executed_tensor_frac": kd_exec / f16_peak,
+                         "executed_flops_per_signal": cost["KD_tensor_executed"][0]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
+                    "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_tot / args.steps,
+                    "how": "jtfs_forward_host (pinned host in/out; H2D / D2H pipelined per 64-signal "
+                           "micro-batch on two copy streams), same steps and L2 flush as the headline"},
+            "path_roofline": _path_roofline(value / max(world, 1), fp32_peak, clocks,
+                                            f"measured in this run: FFMA {ffma:.1f}, FFMA2 {ffma2:.1f} TFLOP/s "
+                                            "(jtfs_measure_fp32_peak)"),
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "with_c1": with_c1,
+            "profiled_pass": {"steps": n_prof, "ms_per_step": sum(prof_ms) / n_prof,
+                              "stages_ms": {k: round(v, 3) for k, v in stage_ms.items()},
+                              "kd_ms_per_alpha": [round(v / n_prof, 3) for v in kd_alpha_ms],
+                              "note": "separate pass with per-stage / per-kernel events; alphas >= 5 run on a "
+                                      "second stream concurrently with the fast alphas"},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(plan, X, out.cpu().numpy())
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_c5(args, rank, world, local, dev):
+    """BASELINE configs[4]: throughput sweep of the c3 plan over batch sizes (white noise)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2204_08269_b200 import jtfs, signals
+    plan = jtfs.Plan(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], Q_fr=CFG["Q_fr"], T=CFG["T"],
+                     F=CFG["F"], device=local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for B in [int(v) for v in args.c5_batches.split(",")]:
+        x = torch.from_numpy(signals.white(B, CFG["N"], seed=rank)).to(dev)
+        out = torch.empty(B, plan.floats_per_signal, dtype=torch.float32, device=dev)
+        for _ in range(args.warmup):
+            plan.forward(x, out)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = ClockSampler(local)
+        clk.start()
+        ms = _timed_steps(lambda: plan.forward(x, out), args.steps, flush, stream)
+        clocks = clk.stop()
+        tot = _max_over_ranks(sum(ms), dev, world)
+        if rank == 0:
+            print(json.dumps({
+                "metric": "JTFS signals/s c5 sweep (N=2^16,J=12,Q=16)", "value": B * world * args.steps / (tot / 1e3),
+                "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "c5 throughput sweep (BASELINE configs[4]), white N(0,1) noise",
+                           "batch_per_gpu": B, "global_batch": B * world,
+                           "l2": "flushed before every timed step (256 MiB write)", **CFG},
+                "clocks": clocks}), flush=True)
+        del x, out
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -363,7 +587,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="signals per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4", "scat1d", "resynth"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c5", "c2", "c4", "scat1d", "resynth"])
+    ap.add_argument("--c5-batches", default="64,128,256,512,1024,2048,4096")
     args = ap.parse_args()
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -390,125 +615,9 @@ def main():
         return run_scat1d(args, rank, world, local, dev)
     if args.workload == "resynth":
         return run_resynth(args, rank, world, local, dev)
-    from paper_2204_08269_b200 import jtfs, signals
-
-    B = args.batch
-    plan = jtfs.Plan(N=CFG["N"], J=CFG["J"], Q=CFG["Q"], J_fr=CFG["J_fr"], Q_fr=CFG["Q_fr"], T=CFG["T"],
-                     F=CFG["F"], device=local)
-    fps = plan.floats_per_signal
-    X = signals.notes(B, seed0=1000 + rank * B)
-    x = torch.from_numpy(X).to(dev)
-    out = torch.empty(B, fps, dtype=torch.float32, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        plan.forward(x, out)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = ClockSampler(local)
-    clk.start()
-    plan.profile_read(reset=True)
-    plan.profile_enable(True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    for k in range(args.steps):
-        flush.fill_(k & 0xFF)                      # L2 flush between timed steps (not timed)
-        ev[k][0].record(stream)
-        plan.forward(x, out)
-        ev[k][1].record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = clk.stop()
-    plan.profile_enable(False)
-    prof = plan.profile_read(reset=True)
-    kd_alpha_ms = plan.profile_read_kd(reset=True)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms = float(tot.item())
-    value = B * world * args.steps / (total_ms / 1e3)
-    launches = int(sum(v[1] for v in prof.values()))
-
-    # ---- end to end through the C ABI with host buffers (pinned), copies timed ----
-    xh = torch.from_numpy(X).pin_memory()
-    oh = torch.empty(B, fps, dtype=torch.float32).pin_memory()
-    plan.forward_host(xh, oh, x, out)
-    k_e2e = max(1, min(args.steps, 3))
-    t_e2e = torch.zeros(1, dtype=torch.float64, device=dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0.record(stream)
-    for _ in range(k_e2e):
-        plan.forward_host(xh, oh, x, out)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    t_e2e[0] = e0.elapsed_time(e1)
-    if world > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = B * world * k_e2e / (float(t_e2e.item()) / 1e3)
-
-    # ---- roofline of the dominant kernel: KD on the tensor pipe (kind::f16, fp16 split) ----
-    # KD runs inside a long step, so the sustained dense bf16 figure is the peak
-    # (fp16 has the same nominal dense rate as bf16 on B200).
-    cost = plan.cost()
-    peaks, src = _peaks()
-    f16_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
-    kd_ms = prof["KD_joint"][0]
-    kd_s = kd_ms / 1e3
-    kd_alg = cost["KD_joint"][0] * B * args.steps / kd_s / 1e12 if kd_ms > 0 else None
-    kd_exec = cost["KD_tensor_executed"][0] * B * args.steps / kd_s / 1e12 if kd_ms > 0 else None
-    stage_share = {k: round(v[0] / max(sum(u[0] for u in prof.values()), 1e-9), 4) for k, v in prof.items()}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "dtype_detail": "fp32 FFTs, modulus and pooling; KA DFT in fp64; KD contraction as a two-term "
-                            "fp16 split on the tensor cores (3 products, fp32 accumulation, ~2^-21 relative)",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": B * world,
-                       "parallelism": f"batch-sharded x{world} (no data-path collective)",
-                       "l2": "flushed before every timed step (256 MiB write)", **CFG},
-            "roofline": {"bound": "tensor",
-                         "kernel": "KD stage (k_ky fp16 split + k_kd_tc: tcgen05 kind::f16 lambda contraction "
-                                   "+ |.| + phi_T pooling)",
-                         "achieved": kd_alg, "peak": f16_peak, "unit": "TFLOP/s",
-                         "frac": (kd_alg / f16_peak) if kd_alg else None, "traffic": _kd_traffic(),
-                         "peak_source": f"dense fp16 = {src} bf16_tflops_sustained (same nominal rate as bf16)",
-                         "algorithmic_flops_per_signal": cost["KD_joint"][0],
-                         "algorithmic_basis": "canonical FFT-along-lambda count of the exact operator (DESIGN.md 5)",
-                         "executed_tensor_tflops": kd_exec,
-                         "executed_tensor_frac": (kd_exec / f16_peak) if kd_exec else None,
-                         "executed_flops_per_signal": cost["KD_tensor_executed"][0],
-                         "executed_basis": "3 fp16 products (hi.hi, hi.lo, lo.hi) x re/im x 2 Mpad K16 L per alpha"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
-                    "d2h_bytes_per_step": int(oh.numel() * 4)},
-            # SURVEY §8(d) report item 2: the whole path against the FP32 SIMT roofline with
-            # the survey's canonical count (21.5 GFLOP per c3 signal: per-alpha cheaper of the
-            # direct / FFT-along-lambda forms + first order), at the measured median SM clock
-            "path_roofline": _path_roofline(value / max(world, 1), clocks),
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "stages_ms": {k: round(v[0], 3) for k, v in prof.items()},
-            "stage_share": stage_share,
-            "kd_ms_per_alpha": [round(v, 3) for v in kd_alpha_ms],
-            "kd_ms_per_alpha_note": "summed over the timed steps; alphas >= 5 run on a second stream "
-                                    "concurrently with the fast alphas, so their times include waiting for SMs",
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(1)
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+    if args.workload == "c5":
+        return run_c5(args, rank, world, local, dev)
+    return run_c3(args, rank, world, local, dev)
 
 
 if __name__ == "__main__":

@@ -159,7 +159,9 @@ JTFS_API jtfs_status jtfs_forward(jtfs_plan_t plan, const float* x, int64_t B, f
  * device, runs jtfs_forward, copies the result to out_host (fp32
  * [B][floats_per_signal]) and synchronises `stream`.  x_dev / out_dev are
  * caller-owned device staging buffers of the same shapes.  Host buffers should
- * be pinned for full copy bandwidth. */
+ * be pinned for full copy bandwidth.  The copies are pipelined per micro-batch on two
+ * internal copy streams (H2D of micro-batch i+1 and D2H of i-1 overlap the compute of
+ * i on `stream`); the result bytes equal jtfs_forward's. */
 JTFS_API jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B,
                               float* out_host, float* x_dev, float* out_dev,
                               void* ws, size_t ws_bytes, void* stream);
@@ -382,6 +384,12 @@ JTFS_API jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir
  * out: L doubles. */
 JTFS_API jtfs_status jtfs_debug_filter(jtfs_plan_t plan, int32_t bank, int32_t idx, int32_t L,
                               int32_t n_grid, double* out);
+
+/* FP32 SIMT peak probe (the ALU roofline must be measured with an FFMA
+ * loop): runs FFMA and packed FFMA2 (fma.rn.f32x2) loops on every SM of `device` for a few
+ * ms each and returns the achieved TFLOP/s (FMA = 2 flops) of the better of 3 timed runs.
+ * Synchronous (blocks until done); at the clock the GPU runs at during the call. */
+JTFS_API jtfs_status jtfs_measure_fp32_peak(int32_t device, double* tflops_ffma, double* tflops_ffma2);
 
 /* Algorithmic cost of one signal per stage (same stage numbering as profiling),
  * for roofline reporting; cost model of DESIGN.md §5 (SURVEY App. B conventions:

@@ -8,6 +8,9 @@
 #include <cstdlib>
 #include <new>
 #include <string>
+#include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "jtfs_internal.h"
 #include "kernels.h"
@@ -197,6 +200,9 @@ struct StageScope {
   cudaStream_t st;
   cudaEvent_t e1 = nullptr;
   StageScope(jtfs::Plan& P_, int s, cudaStream_t st_) : P(P_), stage(s), st(st_) {
+    static const char* const names[6] = {"KA pad+DFT", "KB first order", "KS phi_T averaging",
+                                         "KC second order", "KD joint contraction", "KE phi_F pooling+pack"};
+    nvtxRangePushA(names[stage]);  // host-side NVTX range around the stage's launches
     if (P.prof) {
       cudaEvent_t e0;
       cudaEventCreate(&e0);
@@ -208,6 +214,7 @@ struct StageScope {
   void done(int nlaunch) {
     P.launches[stage] += nlaunch;
     if (P.prof) cudaEventRecord(e1, st);
+    nvtxRangePop();
   }
 };
 
@@ -539,20 +546,72 @@ jtfs_status jtfs_forward_host(jtfs_plan_t plan, const float* x_host, int64_t B, 
   jtfs_status s = check_forward_args(plan, x_dev, B, out_dev, ws, ws_bytes);
   if (s != JTFS_OK || B == 0) return s;
   if (!x_host || !out_host) return fail(JTFS_ERR_INVALID_ARG, "NULL host buffer");
-  const jtfs::Plan& P = plan->P;
+  jtfs::Plan& P = plan->P;
   DeviceGuard guard(P.device);
   cudaStream_t st = (cudaStream_t)stream;
   jtfs_layout_t lay;
   layout_of(P, &lay);
-  cudaError_t e = cudaMemcpyAsync(x_dev, x_host, (size_t)B * P.N * 4, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-  s = jtfs_forward(plan, x_dev, B, out_dev, ws, ws_bytes, stream);
-  if (s != JTFS_OK) return s;
-  e = cudaMemcpyAsync(out_host, out_dev, (size_t)B * lay.floats_per_signal * 4, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
-  e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_fail(e, "stream sync");
-  return JTFS_OK;
+  const size_t fps = (size_t)lay.floats_per_signal;
+  cudaError_t e;
+  if (P.prm.flags & JTFS_CHECK_FINITE) {  // the finite check needs the whole batch first
+    e = cudaMemcpyAsync(x_dev, x_host, (size_t)B * P.N * 4, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    s = jtfs_forward(plan, x_dev, B, out_dev, ws, ws_bytes, stream);
+    if (s != JTFS_OK) return s;
+    e = cudaMemcpyAsync(out_host, out_dev, (size_t)B * fps * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e != cudaSuccess ? cuda_fail(e, "forward_host copies") : JTFS_OK;
+  }
+  // Copies overlapped with compute per micro-batch: H2D of micro-batch i + 1 on an input
+  // copy stream while micro-batch i computes on the caller's stream, D2H of micro-batch i
+  // on an output copy stream while i + 1 computes.  x_dev / out_dev hold the whole batch,
+  // so no buffer is reused across micro-batches; the workspace is used in stream order.
+  const int64_t mb = std::min<int64_t>(B, P.mb);
+  const int64_t nmb = (B + mb - 1) / mb;
+  cudaStream_t cin = nullptr, cout = nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto event = [&]() {
+    cudaEvent_t ev = nullptr;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    evs.push_back(ev);
+    return ev;
+  };
+  e = cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking);
+  std::string err;
+  if (e == cudaSuccess) {
+    cudaEvent_t start = event();
+    cudaEventRecord(start, st);  // the copies follow the caller's earlier work on x_dev / out_dev
+    cudaStreamWaitEvent(cin, start, 0);
+    cudaStreamWaitEvent(cout, start, 0);
+    WsPtrs w = carve(P, ws, mb);
+    for (int64_t i = 0; i < nmb && e == cudaSuccess && err.empty(); ++i) {
+      const int64_t b0 = i * mb, nb = std::min<int64_t>(mb, B - b0);
+      e = cudaMemcpyAsync(x_dev + b0 * P.N, x_host + b0 * P.N, (size_t)nb * P.N * 4, cudaMemcpyHostToDevice, cin);
+      cudaEvent_t in_done = event();
+      cudaEventRecord(in_done, cin);
+      cudaStreamWaitEvent(st, in_done, 0);
+      err = run_microbatch(P, x_dev + b0 * P.N, (int)nb, out_dev + b0 * fps, w, false, 99, st);
+      cudaEvent_t comp_done = event();
+      cudaEventRecord(comp_done, st);
+      cudaStreamWaitEvent(cout, comp_done, 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out_host + b0 * fps, out_dev + b0 * fps, (size_t)nb * fps * 4, cudaMemcpyDeviceToHost,
+                            cout);
+    }
+    cudaEvent_t all_out = event();
+    cudaEventRecord(all_out, cout);
+    cudaStreamWaitEvent(st, all_out, 0);
+    const cudaError_t e2 = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = e2;
+  }
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+  if (cin) cudaStreamDestroy(cin);
+  if (cout) cudaStreamDestroy(cout);
+  if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
+  if (e != cudaSuccess) return cuda_fail(e, "forward_host");
+  e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
 }
 
 // ---- backward / VJP (jtfs.h: jtfs_backward_workspace_size / jtfs_backward) ----
@@ -973,6 +1032,13 @@ jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir, int32_t
   jtfs::launch_debug_fft(P, log2L, dir, fp64 != 0, in, out, (int)rows, tmp, (cudaStream_t)stream);
   cudaError_t e = cudaGetLastError();
   return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
+}
+
+jtfs_status jtfs_measure_fp32_peak(int32_t device, double* tflops_ffma, double* tflops_ffma2) {
+  if (!tflops_ffma || !tflops_ffma2 || device < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  DeviceGuard guard(device);
+  cudaError_t e = jtfs::measure_fp32_peak(tflops_ffma, tflops_ffma2);
+  return e != cudaSuccess ? cuda_fail(e, "fp32 peak probe") : JTFS_OK;
 }
 
 jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap) {

@@ -1009,6 +1009,87 @@ void dispatch_log2(int lg, F&& f) {
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------------
+// FP32 SIMT peak probe (jtfs_measure_fp32_peak; "the bench must measure
+// it with an FFMA loop"): 8 independent FMA chains per thread, scalar FFMA or packed
+// FFMA2 (fma.rn.f32x2), enough warps per SM to hide the 4-cycle latency.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_ffma_peak(float* out, int iters, float b, float c) {
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = (float)(threadIdx.x + j) * 1e-3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = fmaf(a[j], b, c);
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t += a[j];
+  if (t == 1234.5f) out[threadIdx.x] = t;  // keeps the chains live
+}
+
+__global__ void __launch_bounds__(512) k_ffma2_peak(float* out, int iters, float b, float c) {
+  unsigned long long a[8];
+  const float2 bb = make_float2(b, b), cc = make_float2(c, c);
+  const unsigned long long ub = *reinterpret_cast<const unsigned long long*>(&bb);
+  const unsigned long long uc = *reinterpret_cast<const unsigned long long*>(&cc);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 v = make_float2((float)(threadIdx.x + j) * 1e-3f, (float)j * 1e-3f);
+    a[j] = *reinterpret_cast<const unsigned long long*>(&v);
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(ub), "l"(uc));
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 v = *reinterpret_cast<const float2*>(&a[j]);
+    t += v.x + v.y;
+  }
+  if (t == 1234.5f) out[threadIdx.x] = t;
+}
+
+cudaError_t measure_fp32_peak(double* tflops_ffma, double* tflops_ffma2) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  cudaError_t e = cudaMalloc(&out, 512 * sizeof(float));
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 2, threads = 512, iters = 4096;
+  const double fl = (double)blocks * threads * iters * 16 * 8 * 2;  // FMA = 2 flops
+  for (int v = 0; v < 2; ++v) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {  // rep 0 warms the clocks up
+      cudaEventRecord(e0);
+      if (v == 0) k_ffma_peak<<<blocks, threads>>>(out, iters, 0.999999f, 1e-7f);
+      else k_ffma2_peak<<<blocks, threads>>>(out, iters, 0.999999f, 1e-7f);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0) best = std::min(best, ms);
+    }
+    const double t = fl * (v == 0 ? 1.0 : 2.0) / (best * 1e-3) / 1e12;
+    if (v == 0) *tflops_ffma = t;
+    else *tflops_ffma2 = t;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  e = cudaGetLastError();
+  cudaFree(out);
+  return e;
+}
+
 // jtfs_debug_fft: the FFT engine on plain rows (fp32: both directions, lengths 2^1..2^18;
 // fp64: forward, 2^1..2^18), with the plan's twiddle tables (L <= N_pad)
 int launch_debug_fft(const Plan& P, int log2L, int dir, bool fp64, const void* in, void* out, int nrows, void* tmp,

@@ -33,7 +33,8 @@ PATH_SPIN, PATH_PSI_T_PHI_F, PATH_PHI_T_PSI_F, PATH_PHI_T_PHI_F = 0, 1, 2, 3
 EXPORTS = [
     "jtfs_plan", "jtfs_plan_create", "jtfs_plan_destroy", "jtfs_layout", "jtfs_paths",
     "jtfs_lambda_xi", "jtfs_workspace_size", "jtfs_forward", "jtfs_forward_host",
-    "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_debug_joint", "jtfs_debug_fft", "jtfs_cost", "jtfs_profile_enable",
+    "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_debug_joint", "jtfs_debug_fft",
+    "jtfs_measure_fp32_peak", "jtfs_cost", "jtfs_profile_enable",
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
@@ -86,6 +87,7 @@ _lib.jtfs_debug_tap.argtypes = [_P, C.c_int32, _P, C.c_int64, _P, C.c_int64, _P,
 _lib.jtfs_debug_tap_size.argtypes = [_P, C.c_int32, C.c_int64, C.POINTER(C.c_int64)]
 _lib.jtfs_debug_joint.argtypes = [_P, _P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_debug_fft.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_int64, _P, C.c_size_t, _P]
+_lib.jtfs_measure_fp32_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 _lib.jtfs_debug_filter.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
 _lib.jtfs_cost.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32]
 _lib.jtfs_profile_enable.argtypes = [_P, C.c_int32]
@@ -364,7 +366,7 @@ class Plan:
                 out[..., lay.off_s1:lay.off_s2].reshape(*out.shape[:-1], lay.n1, fr),
                 out[..., lay.off_s2:].reshape(*out.shape[:-1], lay.n2, fr))
 
-    def debug_tap(self, tap: int, x):
+    def debug_tap(self, tap: int, x, stream=None):
         import torch
         B = x.shape[0]
         n = C.c_int64()
@@ -372,7 +374,7 @@ class Plan:
         out = torch.empty(int(n.value), dtype=torch.float32, device=x.device)
         ws = self.workspace(B, stream)
         _check(_lib.jtfs_debug_tap(self._h, tap, _ptr(x), B, _ptr(out), out.numel(), _ptr(ws), ws.numel(),
-                                   _stream_handle(None)), "jtfs_debug_tap")
+                                   _stream_handle(stream)), "jtfs_debug_tap")
         return out
 
     def debug_joint(self, y2, yphi, out=None, stream=None):
@@ -498,6 +500,13 @@ def isomap(F, K: int = 40, n_components: int = 3, stream=None):
     _check(_lib.jtfs_isomap(_ptr(F), n, d, F.stride(0), K, n_components, _ptr(emb), _ptr(ev), _ptr(ws), ws.numel(),
                             _stream_handle(stream)), "jtfs_isomap")
     return emb, ev
+
+
+def measure_fp32_peak(device: int = 0):
+    """(FFMA, FFMA2) TFLOP/s measured on `device` (jtfs_measure_fp32_peak; synchronous)."""
+    a, b = C.c_double(), C.c_double()
+    _check(_lib.jtfs_measure_fp32_peak(device, C.byref(a), C.byref(b)), "jtfs_measure_fp32_peak")
+    return a.value, b.value
 
 
 def jtfs_plan(N, J, Q, J_fr, Q_fr, T, F, flags=0) -> Plan:
