@@ -1218,14 +1218,18 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2,
 // KT: second-order time scattering (Scattering1D):
 // S2_t[alpha][lambda][m] = sum_t g_alpha[(frame0 + m) D - t mod L] |Y2_alpha[lambda](t)|
 // -- the phi_T pooling of |Y2| at the retained frames, no lambda convolution.
-// One CTA per (signal, lambda row); fixed-order reduction (bit-stable).
+// The pooling weights come from KD's per-alpha table (plan.cpp): exact taps [L][NF]
+// (one float4 row per column, no index arithmetic), or, where the plan verified it to fp32
+// accuracy, the cubic-moment form [L/32][4][NF] (per 32-column block S_k = sum_j |Y| u_j^k,
+// then sum_k G_k,m S_k).  One CTA per (signal, lambda row), 8 warps; fixed-order
+// reductions (bit-stable).
 // ---------------------------------------------------------------------------------
 struct KTParams {
-  const float* y2;   // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
-  const float* g;    // phi_T taps g_alpha[L]
-  float* out;        // out record of signal 0 at row0's first frame; signal stride fps
+  const float* y2;    // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
+  const float* wtab;  // alpha's phi_T pooling table (taps or moment coefficients)
+  float* out;         // out record of signal 0 at row0's first frame; signal stride fps
   int64_t y2_stride, fps;
-  int L, D, frame0, nframes, K;
+  int L, nframes, K, pool_mode;
 };
 
 template <int NF>
@@ -1234,28 +1238,53 @@ __global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
   const int b = blockIdx.x / p.K, l = blockIdx.x % p.K;
   const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * l) * p.L;
   const float* im = re + p.L;
-  float acc[NF];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (p.pool_mode == 1) {
+    // warp w takes the 32-column blocks w, w + 8, ...; lane j = column j of the block
+    const float u = ((float)lane - 15.5f) * 0.0625f;
+    float accm = 0.f;  // lane m < NF: frame m
+    for (int blk = warp; blk < p.L / 32; blk += 8) {
+      const int t = blk * 32 + lane;
+      const float a = __ldg(re + t), c = __ldg(im + t);
+      const float mag = sqrtf(fmaf(a, a, c * c));
+      float S[4] = {mag, mag * u, mag * u * u, mag * u * u * u};
 #pragma unroll
-  for (int m = 0; m < NF; ++m) acc[m] = 0.f;
-  for (int t = threadIdx.x; t < p.L; t += 256) {
-    const float a = __ldg(re + t), c = __ldg(im + t);
-    const float mag = sqrtf(fmaf(a, a, c * c));
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int m = 0; m < NF; ++m) {
-      if (m < p.nframes) {
-        int i = ((p.frame0 + m) * p.D - t) % p.L;
-        if (i < 0) i += p.L;
-        acc[m] = fmaf(__ldg(p.g + i), mag, acc[m]);
+        for (int o = 16; o > 0; o >>= 1) S[k] += __shfl_xor_sync(0xffffffffu, S[k], o);
+      if (lane < NF) {
+        const float* G = p.wtab + (int64_t)blk * 4 * NF + lane;
+        accm = fmaf(__ldg(G), S[0], accm);
+        accm = fmaf(__ldg(G + NF), S[1], accm);
+        accm = fmaf(__ldg(G + 2 * NF), S[2], accm);
+        accm = fmaf(__ldg(G + 3 * NF), S[3], accm);
       }
     }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane < NF) red[warp][lane] = accm;
+  } else {
+    float acc[NF];
 #pragma unroll
-  for (int m = 0; m < NF; ++m) {
-    float v = acc[m];
+    for (int m = 0; m < NF; ++m) acc[m] = 0.f;
+    for (int t = threadIdx.x; t < p.L; t += 256) {
+      const float a = __ldg(re + t), c = __ldg(im + t);
+      const float mag = sqrtf(fmaf(a, a, c * c));
+      const float4* w4 = reinterpret_cast<const float4*>(p.wtab + (int64_t)t * NF);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][m] = v;
+      for (int m4 = 0; m4 < NF / 4; ++m4) {
+        const float4 w = __ldg(w4 + m4);
+        acc[4 * m4 + 0] = fmaf(w.x, mag, acc[4 * m4 + 0]);
+        acc[4 * m4 + 1] = fmaf(w.y, mag, acc[4 * m4 + 1]);
+        acc[4 * m4 + 2] = fmaf(w.z, mag, acc[4 * m4 + 2]);
+        acc[4 * m4 + 3] = fmaf(w.w, mag, acc[4 * m4 + 3]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < NF; ++m) {
+      float v = acc[m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][m] = v;
+    }
   }
   __syncthreads();
   if (threadIdx.x < NF && threadIdx.x < p.nframes) {
@@ -1272,20 +1301,19 @@ int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64
   for (const auto& d : P.kd) {
     KTParams k{};
     k.y2 = y2 + 2 * d.y2_off;
-    k.g = P.d_g + d.g_off;
+    k.wtab = P.d_wtab + d.wtab_off;
     k.out = out + off_s2 + (int64_t)row0 * P.n_frames;
     k.y2_stride = 2 * P.y2_total;
     k.fps = fps;
     k.L = d.L;
-    k.D = d.D;
-    k.frame0 = P.frame0;
     k.nframes = P.n_frames;
     k.K = d.K;
+    k.pool_mode = (d.pool_mode == 1 && d.L % 32 == 0) ? 1 : 0;
     const int grid = nsig * d.K;
+    // the table's frame stride NF = 8 / 16 / 32 (plan.cpp, n_frames <= 32)
     if (P.n_frames <= 8) k_time_scat<8><<<grid, 256, 0, st>>>(k);
     else if (P.n_frames <= 16) k_time_scat<16><<<grid, 256, 0, st>>>(k);
-    else if (P.n_frames <= 32) k_time_scat<32><<<grid, 256, 0, st>>>(k);
-    else k_time_scat<64><<<grid, 256, 0, st>>>(k);
+    else k_time_scat<32><<<grid, 256, 0, st>>>(k);
     row0 += d.K;
     ++n;
   }

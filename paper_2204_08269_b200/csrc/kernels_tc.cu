@@ -831,7 +831,9 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
   int launches = 0;
   *err = 0;
   cudaStream_t main_st = st;
-  cudaStream_t side = (cudaStream_t)P.kd_side_stream;
+  // profiling (jtfs_profile_enable) serialises every alpha on the caller's stream, so each
+  // launch's event pair measures that launch alone (not the wait for SMs it shares)
+  cudaStream_t side = P.prof ? nullptr : (cudaStream_t)P.kd_side_stream;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (side) {
     // per-call events: concurrent forwards on one plan stay correctly paired
