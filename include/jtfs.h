@@ -398,8 +398,9 @@ JTFS_API jtfs_status jtfs_measure_fp32_peak(int32_t device, double* tflops_ffma,
  * stage's arithmetic (for KD the FFT-along-lambda form); bytes[s]: the stage's
  * unavoidable HBM traffic (input + output of the whole path are charged to
  * KA / KS / KE).  With cap >= 7, flops[6] is the tensor-core work KD actually
- * executes per signal (fp16 two-term split contraction: 3 products x (re, im)
- * x 2 Mpad K16 L summed over alpha) and bytes[6] the A''/Y'' bytes KD stages
+ * executes per signal (spin-pair contraction, fp16 two-term split packed along K:
+ * 8 Mpp K16 L flops summed over alpha, Mpp = pair rows, K16 = 3K rounded up to 16)
+ * and bytes[6] the A''/Y'' bytes KD stages
  * into shared memory per signal.  Host query. */
 JTFS_API jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t cap);
 

@@ -791,10 +791,10 @@ void unit_table(const jtfs::Plan& P, std::vector<jtfs_unit_t>& u) {
   u.clear();
   for (size_t a = 0; a < P.kd.size(); ++a) {
     const auto& d = P.kd[a];
-    // modelled cost: tensor work (3 products x re/im x K16 per complex output) +
-    // epilogue (modulus + pooling per complex output), per column of Mpad rows
-    const double k16 = (double)((2 * d.K + 15) / 16 * 16);
-    const double per_col = (double)P.Mpad * (6.0 * k16 / 8.0 + 24.0);
+    // modelled cost per time column: tensor work (2 products x 2 columns x K16 per pair
+    // row) + epilogue (2 moduli + pooling per pair row)
+    const double k16 = (double)((3 * d.K + 15) / 16 * 16);
+    const double per_col = (double)P.Mpp * (4.0 * k16 / 8.0 + 48.0);
     for (int c = 0; c < d.nchunks; ++c) {
       jtfs_unit_t x{};
       x.alpha = (int32_t)a;
@@ -1051,10 +1051,12 @@ jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t ca
   f[6] = 0;
   b[6] = 0;
   for (const auto& d : P.kd) {
-    const double K16 = d.tc_K16, L = d.L, M = P.Mpad;
-    f[6] += 3.0 * 2.0 * 2.0 * M * K16 * L;
+    // per (M-block of 128 pair rows, Nt-column tile): 2 MMAs (Re / Im A'') per 16-wide chunk
+    // of the packed K' = 3K, each 128 x 2 Nt x 16 MACs
+    const double K16 = d.tc_K16, L = d.L, M = P.Mpp;
+    f[6] += 8.0 * M * K16 * L;
     const double tiles = L / std::max(d.tc_Nt, 1);
-    b[6] += tiles * P.tc_n_mpart * (P.tc_n_mblk * (double)d.tc_nkc * 16384.0 + 4.0 * d.tc_K16 * d.tc_Nt);
+    b[6] += tiles * P.tc_n_mpart * (P.tc_n_mblk * (double)d.tc_nkc * 8192.0 + 4.0 * d.tc_K16 * d.tc_Nt);
   }
   for (int i = 0; i < std::min(cap, 7); ++i) {
     if (flops) flops[i] = f[i];

@@ -60,7 +60,7 @@ struct AlphaKD {
   int nchunks;      // L / chunk
   int64_t part_off; // float offset of partials [nchunks][Mpad][n_frames] in one signal
   // tensor-core (tcgen05 kind::f16, fp16 two-term split) tiling, see kernels_tc.cu
-  int tc_K2 = 0;        // K' = 2K real contraction length (planar Y rows)
+  int tc_K2 = 0;        // K' = 3K packed contraction length ([hi | hi | lo] x [Y_hi; Y_lo; Y_hi])
   int tc_K16 = 0;       // K' rounded up to the MMA K-step (16)
   int tc_nkc = 0;       // 16-wide K chunks (A records per M-block)
   int tc_nbr = 1, tc_BRk = 0;  // TMA row boxes / rows per box of the fp16 B tile
@@ -70,7 +70,7 @@ struct AlphaKD {
   int tc_rps = 1;       // K-records per A ring stage
   int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16
   int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
-  int64_t y16_off = 0;  // fp16 offset of Y16_alpha [hi|lo][K16][L] in one signal's Y16 buffer (KY output)
+  int64_t y16_off = 0;  // fp16 offset of Y16_alpha [K16][2L] in one signal's Y16 buffer (KY output)
   int64_t ys_off = 0;   // float offset of the per-tile inverse Y scales (L / 32 slots) in one signal's ys
   int64_t wtab_off = 0; // float offset of the phi_T pooling table in wtab
   int pool_mode = 0;    // 0: taps [L][NF]; 1: cubic-moment coefficients [L/32][4][NF] (kernels_tc.cu)
@@ -105,7 +105,9 @@ struct Plan {
   int64_t u1_total = 0;          // sum of L1
   std::vector<AlphaKD> kd;       // active alphas in bank order
   int64_t y2_total = 0;          // complex elements of Y2 per signal
-  int M = 0, Mpad = 0;           // joint-stage rows per alpha
+  int M = 0;                     // joint-stage output rows per alpha (all filters)
+  int Mpp_rows = 0, Mpp = 0;     // spin-pair rows (KD) and their padding to whole M-blocks
+  int Mpad = 0;                  // rows of the full (spin-major) layout: 2 Mpp
   int tc_n_mpart = 1, tc_n_mblk = 1;  // M-parts per KD work unit, 128-row M-blocks per part
   int kd_impl = 1;               // 1: tcgen05 (default), 0: SIMT (plan flag JTFS_KD_SIMT, validation)
   std::vector<FrFilter> fr;      // frequential filters: theta=-1 (beta), theta=+1 (beta), phi_F

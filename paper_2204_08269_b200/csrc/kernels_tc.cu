@@ -112,6 +112,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // ---- bulk copy (non-tensor TMA): contiguous global -> smem, completes on an mbarrier ----
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -160,7 +169,7 @@ __device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
 //  elements), lbo = stride between 64-element MN groups, sbo = 1024 between 8-row
 //  K groups.  (Both verified bit-exact with tools/tc_unit16.cu.)
 constexpr uint32_t kLayoutSW128 = 2, kLayoutSW32 = 6;
-constexpr int kRec = 8192;     // one A'' K-record: 128 rows x 16 fp16 x {hi, lo}
+constexpr int kRec = 8192;     // one A'' K-record: 128 pair rows x 16 fp16 x {Re, Im}
 constexpr int kImg = 4096;     // one 128 x 16 fp16 image inside a record
 constexpr int kMaxRps = 4;     // K-records per A ring stage: 1, 2 or 4 (TcParams::rps)
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -210,41 +219,42 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 
-// interleaved (re, im) accumulator columns: 16 time columns per 32 TMEM columns
-template <int NF>
-__device__ __forceinline__ void epi_chunk_i(const uint32_t (&v)[32], const float* wt, float2 (&part)[NF / 2]) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float re = __uint_as_float(v[2 * j]), im = __uint_as_float(v[2 * j + 1]);
-    const float mag = sqrt_fast(fmaf(re, re, im * im));
-    const float4* w4 = reinterpret_cast<const float4*>(wt + j * NF);
-#pragma unroll
-    for (int m4 = 0; m4 < NF / 4; ++m4) {
-      const float4 w = w4[m4];
-      part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mag, part[2 * m4 + 0]);
-      part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mag, part[2 * m4 + 1]);
-    }
-  }
+// tcgen05.ld 32x32b.x16: 16 consecutive accumulator columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
 }
-template <int J0>
-__device__ __forceinline__ void mom_chunk_i(const uint32_t (&v)[32], float (&S)[4]) {
+__device__ __forceinline__ void reg_fence16(uint32_t (&v)[16]) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float re = __uint_as_float(v[2 * j]), im = __uint_as_float(v[2 * j + 1]);
-    const float mag = sqrt_fast(fmaf(re, re, im * im));
-    const float u = ((float)(J0 + j) - 15.5f) * 0.0625f;
-    S[0] += mag;
-    S[1] = fmaf(mag, u, S[1]);
-    S[2] = fmaf(mag, u * u, S[2]);
-    S[3] = fmaf(mag, u * u * u, S[3]);
+  for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(v[i]));
+}
+
+// Both spins of a pair row from its four real products at 8 time columns:
+// v1 = acc1 (Re A . [Yr, Yi]), v2 = acc2 (Im A . [Yr, Yi]), interleaved (Yr, Yi) per column:
+//   Z_-1 = A Y      = (P1 - P2) + i (P3 + P4),   Z_+1 = conj(A) Y = (P1 + P2) + i (P3 - P4)
+// with P1 = Re A Yr, P2 = Im A Yi, P3 = Re A Yi, P4 = Im A Yr (h_{+1} = conj h_{-1}, R10).
+__device__ __forceinline__ void spin_mags(const uint32_t (&v1)[16], const uint32_t (&v2)[16], float (&mm)[8],
+                                          float (&mp)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float p1 = __uint_as_float(v1[2 * j]), p3 = __uint_as_float(v1[2 * j + 1]);
+    const float p4 = __uint_as_float(v2[2 * j]), p2 = __uint_as_float(v2[2 * j + 1]);
+    const float rm = p1 - p2, im_ = p3 + p4, rp = p1 + p2, ip = p3 - p4;
+    mm[j] = sqrt_fast(fmaf(rm, rm, im_ * im_));
+    mp[j] = sqrt_fast(fmaf(rp, rp, ip * ip));
   }
 }
 
 // ---------------------------------------------------------------------------------
-// KY: one CTA per (signal, tile): max |Y''| over the K' x Nt tile -> s_Y (power of
-// two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y - hi) into the
-// planes [hi | lo][K16][L] (rows >= K' not written: TMA zero-fills them), 1 / s_Y
-// into ys[tile].
+// KY: one CTA per (signal, tile of Nt columns): max |Re|, |Im| of Y2_alpha over the K x Nt
+// tile -> s_Y (power of two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y -
+// hi), written as the packed rows [Y_hi (K); Y_lo (K); Y_hi (K)] of [K16][2L] fp16 with
+// (re, im) interleaved per time column (rows >= 3K are never written: the KD tensor map
+// declares 3K rows and TMA zero-fills the rest of each box); 1 / s_Y into ys[tile].
 // ---------------------------------------------------------------------------------
 struct KYParams {
   const float* y2;     // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
@@ -253,7 +263,7 @@ struct KYParams {
   int64_t y16_stride;
   float* ys;           // per-tile inverse scales of signal 0 at alpha's offset; stride ys_stride
   int64_t ys_stride;
-  int K2, K16, L, Nt, ntiles;
+  int K, L, Nt, ntiles;
 };
 
 __global__ void __launch_bounds__(256) k_ky(KYParams p) {
@@ -263,7 +273,7 @@ __global__ void __launch_bounds__(256) k_ky(KYParams p) {
   const float* Y = p.y2 + (int64_t)b * p.y2_stride + t0;
   const int nq = p.Nt / 4;
   float mx = 0.f;
-  for (int i = threadIdx.x; i < p.K2 * nq; i += 256) {
+  for (int i = threadIdx.x; i < 2 * p.K * nq; i += 256) {
     const int k = i / nq, c = 4 * (i % nq);
     const float4 v = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)k * p.L + c));
     mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
@@ -278,49 +288,39 @@ __global__ void __launch_bounds__(256) k_ky(KYParams p) {
   E = max(E, -100);
   const float s = __uint_as_float((uint32_t)(13 - E + 127) << 23);
   if (threadIdx.x == 0) p.ys[(int64_t)b * p.ys_stride + tile] = __uint_as_float((uint32_t)(E - 13 + 127) << 23);
-  // planes [hi | lo][K16][2L]: row 2l = (Yr, Yi) per time column, row 2l+1 = (-Yi, Yr)
-  // (the 2x2 real block of Y2[l] along N: D[m][2t] = Re Z, D[m][2t+1] = Im Z)
-  __half* hi = p.y16 + (int64_t)b * p.y16_stride + 2 * t0;
-  __half* lo = hi + (int64_t)p.K16 * 2 * p.L;
-  const int64_t rs = 2 * (int64_t)p.L;  // plane row stride
-  // rows [K', K16) are never written: the KD tensor map declares K' rows and TMA
-  // zero-fills the out-of-bounds rows of each B box
-  for (int i = threadIdx.x; i < (p.K2 / 2) * p.Nt; i += 256) {
+  __half* row0 = p.y16 + (int64_t)b * p.y16_stride + 2 * t0;
+  const int64_t rs = 2 * (int64_t)p.L;  // row stride (halves)
+  for (int i = threadIdx.x; i < p.K * p.Nt; i += 256) {
     const int l = i / p.Nt, c = i % p.Nt;
     const float yr = __ldg(Y + (int64_t)(2 * l) * p.L + c) * s;
     const float yi = __ldg(Y + (int64_t)(2 * l + 1) * p.L + c) * s;
-    const __half2 h0 = __floats2half2_rn(yr, yi);   // row 2l
-    const float2 f0 = __half22float2(h0);
-    const __half2 l0 = __floats2half2_rn(yr - f0.x, yi - f0.y);
-    const __half2 h1 = __floats2half2_rn(-yi, yr);  // row 2l+1 (negation is exact)
-    const float2 f1 = __half22float2(h1);
-    const __half2 l1 = __floats2half2_rn(-yi - f1.x, yr - f1.y);
-    *reinterpret_cast<__half2*>(hi + (2 * l) * rs + 2 * c) = h0;
-    *reinterpret_cast<__half2*>(lo + (2 * l) * rs + 2 * c) = l0;
-    *reinterpret_cast<__half2*>(hi + (2 * l + 1) * rs + 2 * c) = h1;
-    *reinterpret_cast<__half2*>(lo + (2 * l + 1) * rs + 2 * c) = l1;
+    const __half2 h = __floats2half2_rn(yr, yi);
+    const float2 f = __half22float2(h);
+    const __half2 lo = __floats2half2_rn(yr - f.x, yi - f.y);
+    *reinterpret_cast<__half2*>(row0 + (int64_t)l * rs + 2 * c) = h;
+    *reinterpret_cast<__half2*>(row0 + (int64_t)(p.K + l) * rs + 2 * c) = lo;
+    *reinterpret_cast<__half2*>(row0 + (int64_t)(2 * p.K + l) * rs + 2 * c) = h;
   }
 }
 
 struct TcParams {
-  int K16;         // B tile rows (K' rounded up to 16)
+  int K16;         // B tile rows (3K rounded up to 16)
   int nkc;         // 16-wide K chunks
-  int Nt;          // time columns per tile (64 or 128)
-  int BRk, nbr;    // B TMA box rows, row boxes per plane
+  int Nt;          // time columns per tile (64 or 32)
+  int BRk, nbr;    // B TMA box rows, row boxes
   int NBB;         // fp16 B tile buffers (1 or 2)
-  int nbuf;        // TMEM accumulator buffers (512 / (2 Nt))
   int S;           // A ring stages
   int rps;         // K-records (8 KiB) per A ring stage
   int tpu;         // tiles per work unit
   int nchunks;     // time chunks per signal (L / (Nt * tpu))
   const int32_t* chunk_sel;  // selected chunks (path sharding) or nullptr = all
   int nsel;        // number of selected chunks
-  int n_mpart, n_mblk;  // M-parts and 128-row M-blocks per part
-  int L, nframes, Mpad;
+  int n_mpart, n_mblk;  // M-parts and 128-pair-row M-blocks per part
+  int L, nframes, Mpp;
   int nsig;
   unsigned long long* prof;  // measurement only (JTFS_KD_PROF flag): per-role wait-cycle counters or nullptr
-  const uint16_t* A;   // A''_alpha records [Mpad / 128][nkc] x 16 KiB
-  const float* ainv;   // 1 / s_m per row [Mpad]
+  const uint16_t* A;   // A''_alpha records [Mpp / 128][nkc] x 8 KiB ([Re | Im] images)
+  const float* ainv;   // 1 / s_p per pair row [Mpp]
   const float* wtab;   // phi_T pooling table: taps [L][NF] (pool_mode 0) or cubic moments [L/32][4][NF] (1)
   int pool_mode;
   const float* ys;     // 1 / s_Y per (signal, tile): ys[b * ys_stride + tile]
@@ -332,25 +332,23 @@ struct TcParams {
 constexpr int kThreads = 352;
 // warp roles: 0..7 epilogue, 8 A producer, 9 MMA issuer, 10 B producer
 constexpr int kProdWarp = 8, kMmaWarp = 9, kBWarp = 10;
+constexpr int kNbuf = 2;  // TMEM accumulator buffers, each [acc1 | acc2] of 2 x 2 Nt columns
 
 // shared-memory carve-up (host and device agree through this function)
 struct SmemLayout {
-  uint32_t bhi[2], blo[2], ast, wt, bars, total;
+  uint32_t b[2], ast, wt, bars, total;
 };
 __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int rps, int NF, int pool_mode) {
   SmemLayout l{};
   auto up = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
   uint32_t o = 0;
-  const uint32_t bsz = (uint32_t)(K16 * 2 * Nt * 2);  // one fp16 K16 x 2Nt image (complex along N)
+  const uint32_t bsz = (uint32_t)(K16 * 2 * Nt * 2);  // one fp16 K16 x 2Nt image ((re, im) along N)
   for (int i = 0; i < 2; ++i) {
     if (i < NBB) {
-      l.bhi[i] = o;
-      o = up(o + bsz, 1024);
-      l.blo[i] = o;
+      l.b[i] = o;
       o = up(o + bsz, 1024);
     } else {
-      l.bhi[i] = l.bhi[0];
-      l.blo[i] = l.blo[0];
+      l.b[i] = l.b[0];
     }
   }
   l.ast = o;
@@ -358,13 +356,62 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int 
   l.wt = o;  // [2][Nt][NF] taps, or [2][Nt / 32][4][NF] moment coefficients
   o += (uint32_t)(2 * Nt * (pool_mode ? NF / 8 : NF) * 4);
   l.bars = up(o, 8);
-  o = l.bars + 8 * (4 + 4 + 8 + 2 * S) + 16;
+  o = l.bars + 8 * (4 + 4 + 2 * kNbuf + 2 * S) + 16;
   l.total = o + 1024;  // + alignment slack of the dynamic smem base
   return l;
 }
 
-// NTC: the tile width Nt as a compile-time constant (32 / 64 / 128: the epilogue's column
-// loops unroll completely), or 0 = p.Nt at run time (the instrumented variant)
+// one 8-column group of an epilogue set: both spins' |Z| -> phi_T pooling
+template <int NF, int G>
+__device__ __forceinline__ void epi_group_taps(uint32_t tb1, uint32_t tb2, const float* wt, float2 (&pm)[NF / 2],
+                                               float2 (&pp)[NF / 2]) {
+  uint32_t v1[16], v2[16];
+  tmem_ld16(tb1 + 16 * G, v1);
+  tmem_ld16(tb2 + 16 * G, v2);
+  tmem_wait_ld();
+  reg_fence16(v1);
+  reg_fence16(v2);
+  float mm[8], mp[8];
+  spin_mags(v1, v2, mm, mp);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4* w4 = reinterpret_cast<const float4*>(wt + (8 * G + j) * NF);
+#pragma unroll
+    for (int m4 = 0; m4 < NF / 4; ++m4) {
+      const float4 w = w4[m4];
+      pm[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mm[j], pm[2 * m4 + 0]);
+      pm[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mm[j], pm[2 * m4 + 1]);
+      pp[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mp[j], pp[2 * m4 + 0]);
+      pp[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mp[j], pp[2 * m4 + 1]);
+    }
+  }
+}
+template <int G>
+__device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float (&Sm)[4], float (&Sp)[4]) {
+  uint32_t v1[16], v2[16];
+  tmem_ld16(tb1 + 16 * G, v1);
+  tmem_ld16(tb2 + 16 * G, v2);
+  tmem_wait_ld();
+  reg_fence16(v1);
+  reg_fence16(v2);
+  float mm[8], mp[8];
+  spin_mags(v1, v2, mm, mp);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float u = ((float)(8 * G + j) - 15.5f) * 0.0625f;  // compile-time
+    Sm[0] += mm[j];
+    Sm[1] = fmaf(mm[j], u, Sm[1]);
+    Sm[2] = fmaf(mm[j], u * u, Sm[2]);
+    Sm[3] = fmaf(mm[j], u * u * u, Sm[3]);
+    Sp[0] += mp[j];
+    Sp[1] = fmaf(mp[j], u, Sp[1]);
+    Sp[2] = fmaf(mp[j], u * u, Sp[2]);
+    Sp[3] = fmaf(mp[j], u * u * u, Sp[3]);
+  }
+}
+
+// NTC: the tile width Nt as a compile-time constant (64 / 32: the epilogue's column loops
+// unroll completely).  PROF: the instrumented variant (JTFS_KD_PROF plan flag).
 template <int NF, int MAXSLOT, bool PROF, int NTC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_kd_tc(const __grid_constant__ CUtensorMap tmB, TcParams p) {
@@ -372,20 +419,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  const SmemLayout lay = smem_layout(p.K16, p.Nt, p.NBB, p.S, p.rps, NF, p.pool_mode);
-  const int wfl = p.Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
+  constexpr int Nt = NTC;
+  const SmemLayout lay = smem_layout(p.K16, Nt, p.NBB, p.S, p.rps, NF, p.pool_mode);
+  const int wfl = Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
   uint8_t* Ast = base + lay.ast;
-  float* Wt = reinterpret_cast<float*>(base + lay.wt);  // [2][Nt][NF]
+  float* Wt = reinterpret_cast<float*>(base + lay.wt);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + lay.bars);
   uint64_t* b_full = bars + 0;      // [2] B tile landed
   uint64_t* b_empty = bars + 2;     // [2] MMA done with the B tile
   uint64_t* w_full = bars + 4;      // [2] taps landed
   uint64_t* w_empty = bars + 6;     // [2] epilogue done with the taps
-  uint64_t* acc_full = bars + 8;    // [4]
-  uint64_t* acc_empty = bars + 12;  // [4]
-  uint64_t* a_full = bars + 16;     // [S]
-  uint64_t* a_empty = bars + 16 + p.S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * p.S);
+  uint64_t* acc_full = bars + 8;    // [kNbuf]
+  uint64_t* acc_empty = bars + 8 + kNbuf;
+  uint64_t* a_full = bars + 8 + 2 * kNbuf;  // [S]
+  uint64_t* a_empty = a_full + p.S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + p.S);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -395,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(w_full + i, 1);
       mbar_init(w_empty + i, 8);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kNbuf; ++i) {
       mbar_init(acc_full + i, 1);
       mbar_init(acc_empty + i, 8);
     }
@@ -423,19 +471,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int my_tiles = my_units * p.tpu;
 
   if (warp == kBWarp) {
-    // ===================== B producer: fp16 hi / lo tile + taps =====================
+    // ===================== B producer: the packed fp16 tile + pooling table =====================
     // one copy per lane (copies issued by one thread complete one after another):
-    // lane 0 the taps, lanes 1.. the TMA boxes (planes x 64-column groups x row boxes)
-    const int ncg = 2 * p.Nt / 64, nboxes = 2 * ncg * p.nbr;  // 2Nt columns: complex block along N
-    const uint32_t btx = (uint32_t)(2 * p.K16 * 2 * p.Nt * 2);
+    // lane 0 the table, lanes 1.. the TMA boxes (64-column groups x row boxes)
+    constexpr int ncg = 2 * Nt / 64;
+    const int nboxes = ncg * p.nbr;
+    const uint32_t btx = (uint32_t)(p.K16 * 2 * Nt * 2);
     const int wcol = p.pool_mode ? NF / 8 : NF;  // table floats per time column
-    const uint32_t wbytes = (uint32_t)(p.Nt * wcol * 4);
+    const uint32_t wbytes = (uint32_t)(Nt * wcol * 4);
     for (int gt = 0; gt < my_tiles; ++gt) {
       const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
       int chunk = (u / p.n_mpart) % p.nsel;
       if (p.chunk_sel) chunk = p.chunk_sel[chunk];
       const int b = u / (p.n_mpart * p.nsel);
-      const int t0 = (chunk * p.tpu + gt % p.tpu) * p.Nt;
+      const int t0 = (chunk * p.tpu + gt % p.tpu) * Nt;
       const int wi = gt & 1, bi = gt % p.NBB;
       if (lane == 0) {
         mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
@@ -446,10 +495,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
       for (int i = lane - 1; i >= 0 && i < nboxes; i += 31) {
-        const int h = i / (ncg * p.nbr), cg = (i / p.nbr) % ncg, rb = i % p.nbr;
-        uint8_t* dst = base + (h ? lay.blo[bi] : lay.bhi[bi]);
-        tma_load_4d(dst + cg * (p.K16 * 128) + rb * (p.BRk * 128), &tmB, b_full + bi, 2 * t0 + cg * 64, rb * p.BRk,
-                    h, b);
+        const int cg = i / p.nbr, rb = i % p.nbr;
+        uint8_t* dst = base + lay.b[bi] + cg * (p.K16 * 128) + rb * (p.BRk * 128);
+        tma_load_3d(dst, &tmB, b_full + bi, 2 * t0 + cg * 64, rb * p.BRk, b);
       }
     }
   } else if (warp == kProdWarp) {
@@ -459,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // issue in parallel; a slot is always served by the same lane, which keeps its
     // parity waits unambiguous).
     if (lane < p.S) {
-      uint32_t j = 0, s = 0, ph = 0;
+      uint32_t s = 0, ph = 0;
       for (int gt = 0; gt < my_tiles; ++gt) {
         const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
         const int mpart = u % p.n_mpart;
@@ -472,7 +520,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_expect_tx(a_full + s, bytes);
               bulk_load(Ast + s * stage_bytes, arec + (size_t)(p.rps * st) * (kRec / 2), bytes, a_full + s);
             }
-            ++j;
             if (++s == (uint32_t)p.S) {
               s = 0;
               ph ^= 1;
@@ -483,23 +530,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (warp-wide loop, one elected lane issues) =====================
+    // per M-block and 16-wide K chunk: acc1 += Re A'' . B, acc2 += Im A'' . B (N = 2 Nt)
     uint32_t s = 0, ph = 0, cnt = 0;
     long long w_b = 0, w_acc = 0, w_a = 0;
     const long long t_start = clk<PROF>();
-    const uint32_t idesc = idesc_f16(2 * p.Nt);  // N = 2 Nt: (re, im) interleaved per time column
+    const uint32_t idesc = idesc_f16(2 * Nt);
     const uint32_t colstride = (uint32_t)(p.K16 * 128);
     const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 256, kLayoutSW32);
     for (int gt = 0; gt < my_tiles; ++gt) {
       const int bi = gt % p.NBB;
       mbar_wait_t<PROF>(b_full + bi, (uint32_t)(gt / p.NBB) & 1u, w_b);
       tc_fence_after();
-      const uint64_t dBh = sdesc(smem_u32(base + lay.bhi[bi]), colstride, 1024, kLayoutSW128);
-      const uint64_t dBl = sdesc(smem_u32(base + lay.blo[bi]), colstride, 1024, kLayoutSW128);
+      const uint64_t dB = sdesc(smem_u32(base + lay.b[bi]), colstride, 1024, kLayoutSW128);
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
-        const uint32_t ab = cnt % (uint32_t)p.nbuf, use = cnt / (uint32_t)p.nbuf;
+        const uint32_t ab = cnt % (uint32_t)kNbuf, use = cnt / (uint32_t)kNbuf;
         mbar_wait_t<PROF>(acc_empty + ab, (use + 1) & 1, w_acc);
         tc_fence_after();
-        const uint32_t dd = tmem_base + ab * 2u * (uint32_t)p.Nt;
+        const uint32_t d1 = tmem_base + ab * 4u * (uint32_t)Nt, d2 = d1 + 2u * (uint32_t)Nt;
         for (int st = 0; st < nst; ++st) {
           mbar_wait_t<PROF>(a_full + s, ph, w_a);
           tc_fence_after();
@@ -512,9 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
                 const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
                 const uint32_t acc0 = kc > 0 ? 1u : 0u;
-                mma_f16(dd, a, dBh + yo, idesc, acc0);                        // A_hi B_hi
-                mma_f16(dd, a, dBl + yo, idesc, 1u);                          // A_hi B_lo
-                mma_f16(dd, a + (uint64_t)(kImg >> 4), dBh + yo, idesc, 1u);  // A_lo B_hi
+                mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
+                mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
               }
             }
             mma_commit(a_empty + s);
@@ -541,11 +587,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== epilogue (warps 0..7) =====================
     const int eset = warp >> 2;  // column half
     const int q = warp & 3;      // TMEM lane quarter (warp_id % 4)
-    const int cbeg = eset * (p.Nt / 2);
+    constexpr int half = Nt / 2;
+    const int cbeg = eset * half;
     long long e_w = 0, e_acc = 0, e_math = 0;
     const long long e_start = clk<PROF>();
     uint32_t cnt = 0;
-    float2 accr[MAXSLOT][NF / 2];  // pooled partials of my rows (one per M-block of the part)
+    float2 accm[MAXSLOT][NF / 2], accp[MAXSLOT][NF / 2];  // pooled partials of both spins of my pair rows
     for (int gt = 0; gt < my_tiles; ++gt) {
       const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
       const int mpart = u % p.n_mpart;
@@ -557,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k)
 #pragma unroll
-          for (int m = 0; m < NF / 2; ++m) accr[k][m] = make_float2(0.f, 0.f);
+          for (int m = 0; m < NF / 2; ++m) accm[k][m] = accp[k][m] = make_float2(0.f, 0.f);
       }
       const int wi = gt & 1;
       mbar_wait_t<PROF>(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
@@ -565,67 +612,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* wt = Wt + wi * wfl + cbeg * NF;
 #pragma unroll 1
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
-        const uint32_t ab = cnt % (uint32_t)p.nbuf;
-        mbar_wait_t<PROF>(acc_full + ab, (cnt / (uint32_t)p.nbuf) & 1u, e_acc);
+        const uint32_t ab = cnt % (uint32_t)kNbuf;
+        mbar_wait_t<PROF>(acc_full + ab, (cnt / (uint32_t)kNbuf) & 1u, e_acc);
         const long long tm0 = clk<PROF>();
         tc_fence_after();
-        // accumulator columns 2t / 2t+1 = Re / Im of time column t; this set's time
-        // columns [cbeg, cbeg + Nt/2) start at TMEM column 2 cbeg
-        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ab * 2u * (uint32_t)p.Nt + 2u * (uint32_t)cbeg;
-        float2 part[NF / 2];
+        // accumulator columns 2t / 2t+1 = (Yr, Yi) products of time column t; this set's
+        // columns [cbeg, cbeg + Nt/2) start at TMEM column 2 cbeg of acc1 / acc2
+        const uint32_t tb1 = tmem_base + ((uint32_t)(q * 32) << 16) + ab * 4u * (uint32_t)Nt + 2u * (uint32_t)cbeg;
+        const uint32_t tb2 = tb1 + 2u * (uint32_t)Nt;
+        float2 pm[NF / 2], pp[NF / 2];
 #pragma unroll
-        for (int m = 0; m < NF / 2; ++m) part[m] = make_float2(0.f, 0.f);
-        const int half = (NTC ? NTC : p.Nt) / 2;
+        for (int m = 0; m < NF / 2; ++m) pm[m] = pp[m] = make_float2(0.f, 0.f);
         if (p.pool_mode == 1) {
-          // moment form: per 32-column block S_k = sum_j |Z_j| u_j^k (k <= 3, u_j
-          // compile-time), then part += G_k S_k with the block's 4 x NF coefficients
-          const float* gco = Wt + wi * wfl + (cbeg / 32) * 4 * NF;
-#pragma unroll
-          for (int c0 = 0; c0 < half; c0 += 32) {
-            float S[4] = {0.f, 0.f, 0.f, 0.f};
-            {
-              uint32_t v[32];
-              tmem_ld32(tb + 2 * c0, v);
-              tmem_wait_ld();
-              reg_fence(v);
-              mom_chunk_i<0>(v, S);
-            }
-            {
-              uint32_t v[32];
-              tmem_ld32(tb + 2 * c0 + 32, v);
-              tmem_wait_ld();
-              reg_fence(v);
-              if (c0 + 32 >= half) {  // last read of this buffer: hand it back to the MMA
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(acc_empty + ab);
-              }
-              mom_chunk_i<16>(v, S);
-            }
-            const float4* g4 = reinterpret_cast<const float4*>(gco + (c0 / 32) * 4 * NF);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-              for (int m4 = 0; m4 < NF / 4; ++m4) {
-                const float4 w = g4[k * (NF / 4) + m4];
-                part[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), S[k], part[2 * m4 + 0]);
-                part[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), S[k], part[2 * m4 + 1]);
-              }
+          // moment form (Nt = 64: this set's 32 columns are one 32-column block):
+          // S_k = sum_j |Z_j| u_j^k (k <= 3, u_j compile-time), then part += G_k S_k
+          float Sm[4] = {0.f, 0.f, 0.f, 0.f}, Sp[4] = {0.f, 0.f, 0.f, 0.f};
+          if constexpr (half == 32) {
+            epi_group_mom<0>(tb1, tb2, Sm, Sp);
+            epi_group_mom<1>(tb1, tb2, Sm, Sp);
+            epi_group_mom<2>(tb1, tb2, Sm, Sp);
+            epi_group_mom<3>(tb1, tb2, Sm, Sp);
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty + ab);  // accumulator buffer read: back to the MMA
+          const float4* g4 = reinterpret_cast<const float4*>(Wt + wi * wfl + (cbeg / 32) * 4 * NF);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int m4 = 0; m4 < NF / 4; ++m4) {
+              const float4 w = g4[k * (NF / 4) + m4];
+              pm[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), Sm[k], pm[2 * m4 + 0]);
+              pm[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), Sm[k], pm[2 * m4 + 1]);
+              pp[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), Sp[k], pp[2 * m4 + 0]);
+              pp[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), Sp[k], pp[2 * m4 + 1]);
+            }
         } else {
-#pragma unroll
-          for (int c0 = 0; c0 < half; c0 += 16) {
-            uint32_t v[32];
-            tmem_ld32(tb + 2 * c0, v);
-            tmem_wait_ld();
-            reg_fence(v);
-            if (c0 + 16 >= half) {  // last read of this buffer: hand it back to the MMA
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(acc_empty + ab);
-            }
-            epi_chunk_i<NF>(v, wt + c0 * NF, part);
+          epi_group_taps<NF, 0>(tb1, tb2, wt, pm, pp);
+          epi_group_taps<NF, 1>(tb1, tb2, wt, pm, pp);
+          if constexpr (half == 32) {
+            epi_group_taps<NF, 2>(tb1, tb2, wt, pm, pp);
+            epi_group_taps<NF, 3>(tb1, tb2, wt, pm, pp);
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty + ab);
         }
         e_math += clk<PROF>() - tm0;
         // warp-uniform branch to the M-block's slot (a predicated loop over all
@@ -634,11 +665,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define JTFS_ACC_SLOT(K)                                                                         \
   case K:                                                                                        \
     if constexpr (K < MAXSLOT) {                                                                 \
-      _Pragma("unroll") for (int m = 0; m < NF / 2; ++m) accr[K][m] = ffma2(part[m], inv, accr[K][m]); \
+      _Pragma("unroll") for (int m = 0; m < NF / 2; ++m) {                                       \
+        accm[K][m] = ffma2(pm[m], inv, accm[K][m]);                                              \
+        accp[K][m] = ffma2(pp[m], inv, accp[K][m]);                                              \
+      }                                                                                          \
     }                                                                                            \
     break;
           JTFS_ACC_SLOT(0) JTFS_ACC_SLOT(1) JTFS_ACC_SLOT(2) JTFS_ACC_SLOT(3) JTFS_ACC_SLOT(4)
-          JTFS_ACC_SLOT(5) JTFS_ACC_SLOT(6) JTFS_ACC_SLOT(7) JTFS_ACC_SLOT(8)
 #undef JTFS_ACC_SLOT
           default: break;
         }
@@ -646,19 +679,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(w_empty + wi);  // this warp is done with the tile's taps
       if (tile == p.tpu - 1) {
-        // unit done: my rows' pooled partials of this (time chunk, column half) slice
+        // unit done: my pair rows' pooled partials of this (time chunk, column half) slice,
+        // theta = -1 (and phi_F) at row p, theta = +1 at row Mpp + p
         float* dst = p.part + (int64_t)b * p.part_stride + p.part_off +
-                     (int64_t)(2 * chunk + eset) * p.Mpad * p.nframes;
+                     (int64_t)(2 * chunk + eset) * (2 * p.Mpp) * p.nframes;
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k) {
           if (k < p.n_mblk) {
             const int row = (mpart * p.n_mblk + k) * 128 + q * 32 + lane;
             const float ia = __ldg(p.ainv + row);
-            float* d = dst + (int64_t)row * p.nframes;
+            float* d0 = dst + (int64_t)row * p.nframes;
+            float* d1 = dst + (int64_t)(p.Mpp + row) * p.nframes;
 #pragma unroll
             for (int m = 0; m < NF / 2; ++m) {
-              if (2 * m < p.nframes) d[2 * m] = accr[k][m].x * ia;
-              if (2 * m + 1 < p.nframes) d[2 * m + 1] = accr[k][m].y * ia;
+              if (2 * m < p.nframes) {
+                d0[2 * m] = accm[k][m].x * ia;
+                d1[2 * m] = accp[k][m].x * ia;
+              }
+              if (2 * m + 1 < p.nframes) {
+                d0[2 * m + 1] = accm[k][m].y * ia;
+                d1[2 * m + 1] = accp[k][m].y * ia;
+              }
             }
           }
         }
@@ -726,15 +767,15 @@ size_t tc_smem(const AlphaKD& d, int nf) {
 std::string plan_tc(Plan& P) {
   const int NF = nf_of(P.n_frames);
   const size_t budget = 227 * 1024;
-  P.tc_n_mblk = P.Mpad / 128 / P.tc_n_mpart;
+  P.tc_n_mblk = P.Mpp / 128 / P.tc_n_mpart;
   // A ring stages of rps 8 KiB K-records, as equal as possible with <= 4 records per
-  // stage (nkc = 5 -> 3 + 2, not 4 + 1: a 1-record stage is consumed in 3 MMAs, too fast
+  // stage (nkc = 5 -> 3 + 2, not 4 + 1: a 1-record stage is consumed in 2 MMAs, too fast
   // for the next 4-record copy into its slot).  Measured on c3 (round 1): uniform
   // rps = 1 / 2 / 4 -> 2156 / 2459 / 2542 signals/s (per-copy overhead), so stages stay
   // at <= 32 KiB.  The ring holds at most 24 records (192 KiB).
   constexpr int rec_max = 24;
   for (auto& d : P.kd) {
-    d.tc_K2 = 2 * d.K;
+    d.tc_K2 = 3 * d.K;
     d.tc_K16 = (d.tc_K2 + 15) / 16 * 16;
     d.tc_nkc = d.tc_K16 / 16;
     d.tc_nbr = (d.tc_K16 + 255) / 256;
@@ -743,11 +784,12 @@ std::string plan_tc(Plan& P) {
       const int nst = (d.tc_nkc + 3) / 4;
       d.tc_rps = (d.tc_nkc + nst - 1) / nst;
     }
-    // Nt = 128 (MMA N = 256, the efficient shape) first; two B buffers when they fit
-    // with >= 2 stages of A records.  The moment-form epilogue needs Nt >= 64 (32-column
-    // blocks of each set's Nt / 2 columns): a narrower tile falls back to the exact taps.
+    // Nt = 64 time columns (two accumulators of N = 2 Nt = 128 columns per M-block, two
+    // TMEM buffers); two B buffers when they fit next to >= 2 stages of A records.  The
+    // moment-form epilogue needs Nt = 64 (its 32-column blocks are one epilogue set's
+    // columns): a narrower tile (L < 64 or no fit) falls back to the exact taps.
     auto choose = [&]() {
-      const int cand[7][3] = {{128, 2, 3}, {128, 2, 2}, {128, 1, 3}, {128, 1, 2}, {64, 2, 2}, {64, 1, 2}, {32, 1, 2}};
+      const int cand[4][3] = {{64, 2, 3}, {64, 2, 2}, {64, 1, 2}, {32, 1, 2}};
       for (const auto& c : cand) {
         if (c[0] > d.L) continue;
         d.tc_Nt = c[0];
@@ -761,7 +803,7 @@ std::string plan_tc(Plan& P) {
       return false;
     };
     bool ok = choose();
-    if (ok && d.pool_mode && d.tc_Nt < 64) {
+    if (ok && d.pool_mode && d.tc_Nt != 64) {
       d.pool_mode = 0;
       ok = choose();
     }
@@ -779,9 +821,9 @@ std::string plan_tc(Plan& P) {
     d.tc_tpu = d.chunk / d.tc_Nt;
     // the KY / KD per-tile scale slots (plan.cpp sizes L / 32 per alpha and signal)
     if (d.L / d.tc_Nt > std::max(1, d.L / 32)) return "internal: tensor-core KD tile scales exceed their slots";
-    if (d.L < 64) return "tensor-core KD: alpha " + std::to_string(d.alpha) + " has fewer than 64 time columns";
+    if (d.L < 32) return "tensor-core KD: alpha " + std::to_string(d.alpha) + " has fewer than 32 time columns";
     if (d.chunk % d.tc_Nt || d.nchunks * d.chunk != d.L) return "internal: tensor-core KD chunking";
-    if (d.tc_nbr * d.tc_BRk < d.tc_K16) return "internal: tensor-core KD B boxes";
+    if (d.tc_nbr * d.tc_BRk != d.tc_K16) return "internal: tensor-core KD B boxes";
   }
   return "";
 }
@@ -810,11 +852,11 @@ cudaError_t tc_setup_device(Plan& P) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
   };
 #define JTFS_SET_KD(NF_, MS_)                                                                      \
-  set(tc::k_kd_tc<NF_, MS_, false, 128>); set(tc::k_kd_tc<NF_, MS_, false, 64>);                  \
-  set(tc::k_kd_tc<NF_, MS_, false, 32>); set(tc::k_kd_tc<NF_, MS_, true, 0>);
-  if (NF == 8) { JTFS_SET_KD(8, 9) }
-  else if (NF == 16) { JTFS_SET_KD(16, 4) }
-  else { JTFS_SET_KD(32, 2) }
+  set(tc::k_kd_tc<NF_, MS_, false, 64>); set(tc::k_kd_tc<NF_, MS_, false, 32>);                    \
+  set(tc::k_kd_tc<NF_, MS_, true, 64>); set(tc::k_kd_tc<NF_, MS_, true, 32>);
+  if (NF == 8) { JTFS_SET_KD(8, 5) }
+  else if (NF == 16) { JTFS_SET_KD(16, 2) }
+  else { JTFS_SET_KD(32, 1) }
 #undef JTFS_SET_KD
   return e;
 }
@@ -856,8 +898,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
       q.y16_stride = P.y16_total;
       q.ys = ys + d.ys_off;
       q.ys_stride = P.ys_total;
-      q.K2 = d.tc_K2;
-      q.K16 = d.tc_K16;
+      q.K = d.K;
       q.L = d.L;
       q.Nt = d.tc_Nt;
       q.ntiles = d.L / d.tc_Nt;
@@ -865,12 +906,12 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
       ++launches;
     }
     CUtensorMap tmB;
-    // K' = 2K rows per plane (the planes are allocated with K16 rows): the box rows
-    // beyond K' are out of bounds and arrive zero-filled (the MMA's K padding)
-    cuuint64_t dims[4] = {(cuuint64_t)(2 * d.L), (cuuint64_t)d.tc_K2, 2, (cuuint64_t)nsig};
-    cuuint64_t strides[3] = {(cuuint64_t)d.L * 4, (cuuint64_t)d.tc_K16 * d.L * 4, (cuuint64_t)P.y16_total * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)d.tc_BRk, 1, 1};
-    if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 4, dims, strides, box,
+    // K' = 3K packed rows (the buffer is allocated with K16 rows): the box rows beyond K'
+    // are out of bounds and arrive zero-filled (the MMA's K padding)
+    cuuint64_t dims[3] = {(cuuint64_t)(2 * d.L), (cuuint64_t)d.tc_K2, (cuuint64_t)nsig};
+    cuuint64_t strides[2] = {(cuuint64_t)d.L * 4, (cuuint64_t)P.y16_total * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)d.tc_BRk, 1};
+    if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 3, dims, strides, box,
                 CU_TENSOR_MAP_SWIZZLE_128B)) {
       *err = 1;
       break;  // the join below still orders the side stream before the caller's
@@ -882,7 +923,6 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.BRk = d.tc_BRk;
     p.nbr = d.tc_nbr;
     p.NBB = d.tc_NBB;
-    p.nbuf = std::min(4, 512 / (2 * d.tc_Nt));  // accumulator buffers of 2 Nt columns (4 barrier pairs)
     p.S = d.tc_S;
     p.rps = d.tc_rps;
     p.tpu = d.tc_tpu;
@@ -893,7 +933,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.n_mblk = P.tc_n_mblk;
     p.L = d.L;
     p.nframes = P.n_frames;
-    p.Mpad = P.Mpad;
+    p.Mpp = P.Mpp;
     p.nsig = nsig;
     p.A = P.d_A16 + d.tc_a16_off;
     p.ainv = P.d_Ainv + d.tc_ainv_off;
@@ -922,13 +962,11 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     }
     auto go = [&](auto kern) { kern<<<grid, tc::kThreads, sm, st>>>(tmB, p); };
 #define JTFS_GO_KD(NF_, MS_)                                                                        \
-  if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 0>);                                                 \
-  else if (d.tc_Nt == 128) go(tc::k_kd_tc<NF_, MS_, false, 128>);                                  \
-  else if (d.tc_Nt == 64) go(tc::k_kd_tc<NF_, MS_, false, 64>);                                    \
-  else go(tc::k_kd_tc<NF_, MS_, false, 32>);
-    if (NF == 8) { JTFS_GO_KD(8, 9) }
-    else if (NF == 16) { JTFS_GO_KD(16, 4) }
-    else { JTFS_GO_KD(32, 2) }
+  if (d.tc_Nt == 64) { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 64>); else go(tc::k_kd_tc<NF_, MS_, false, 64>); } \
+  else { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 32>); else go(tc::k_kd_tc<NF_, MS_, false, 32>); }
+    if (NF == 8) { JTFS_GO_KD(8, 5) }
+    else if (NF == 16) { JTFS_GO_KD(16, 2) }
+    else { JTFS_GO_KD(32, 1) }
 #undef JTFS_GO_KD
     ++launches;
     if (P.prof) cudaEventRecord(e1, st);

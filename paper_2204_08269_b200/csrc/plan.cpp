@@ -391,19 +391,44 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
         P.Wrange.push_back(hi + 1);
       }
     }
-    f.row0 = P.M;
     P.M += f.nrows;
   }
   {
-    // M-blocks of 128 complex rows (one TMEM lane each), split into M-parts so that
-    // one part's pooled row accumulators stay in the tcgen05 epilogue's registers:
-    // <= MAXSLOT M-blocks per part (kernels_tc.cu: NF 8: 9, 16: 4, 32: 2)
+    // Spin pairs (kernels_tc.cu, KD): the theta = -1 and theta = +1 wavelets of one beta
+    // share their decimation k, hence their retained rows, and h_{beta,+1} = conj h_{beta,-1}
+    // (psi_hat real, R10).  Pair row p holds one retained row r' of beta (and, after the
+    // wavelets, the phi_F rows, whose taps are real); KD computes both spins of a pair from
+    // the same four real products.  Pair rows are laid out beta-major: [beta 0 rows, ...,
+    // beta nb-1 rows, phi_F rows], padded to whole 128-row M-blocks; the "full" rows of the
+    // partials / KE / SIMT layout are spin-major: theta = -1 (and phi_F) rows at p,
+    // theta = +1 rows at Mpp + p.
+    int prow = 0;
+    std::vector<int> prow0(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) {
+      const FrFilter& fm = P.fr[b];
+      const FrFilter& fp = P.fr[nb + b];
+      if (fm.k != fp.k || fm.rprime != fp.rprime) return "internal: spin-pair rows differ";
+      prow0[b] = prow;
+      prow += fm.nrows;
+    }
+    prow0[nb] = prow;
+    prow += P.fr[2 * nb].nrows;
+    P.Mpp_rows = prow;
+    // M-blocks of 128 pair rows (one TMEM lane each), split into M-parts so that one part's
+    // pooled accumulators (2 spins x NF frames per block) stay in the epilogue's registers:
+    // <= MAXSLOT M-blocks per part (kernels_tc.cu: NF 8: 5, 16: 2, 32: 1)
     const int n_frames_pad = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
-    int max_mblk = n_frames_pad == 8 ? 9 : n_frames_pad == 16 ? 4 : 2;
-    const int mblocks = (P.M + 127) / 128;
+    const int max_mblk = n_frames_pad == 8 ? 5 : n_frames_pad == 16 ? 2 : 1;
+    const int mblocks = (prow + 127) / 128;
     P.tc_n_mpart = (mblocks + max_mblk - 1) / max_mblk;
     P.tc_n_mblk = (mblocks + P.tc_n_mpart - 1) / P.tc_n_mpart;
-    P.Mpad = P.tc_n_mblk * P.tc_n_mpart * 128;
+    P.Mpp = P.tc_n_mblk * P.tc_n_mpart * 128;
+    P.Mpad = 2 * P.Mpp;
+    for (int b = 0; b < nb; ++b) {
+      P.fr[b].row0 = prow0[b];
+      P.fr[nb + b].row0 = P.Mpp + prow0[b];
+    }
+    P.fr[2 * nb].row0 = prow0[nb];
     P.kd_impl = (p.flags & JTFS_KD_SIMT) ? 0 : 1;  // SIMT KD only on explicit request (validation)
   }
   // frequential taps h_f = IDFT_{N_fr}(f_hat) (fp64)
@@ -441,31 +466,35 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       }
     }
   }
-  // A''_alpha for the tensor cores (kernels_tc.cu, complex along N): for complex row m
-  // and K' index k' = 2l + c,  A''[m][2l] = Re A[m][l],  A''[m][2l+1] = Im A[m][l];
-  // with B'' the 2x2 real block of Y2[l] along N (KY), D[m][2t] = Re Z, D[m][2t+1] = Im Z.
-  // Each row is scaled by a power of two s_m (max |entry| * s_m in [2^13, 2^14)) and
-  // split into fp16 hi = rn(a s_m), lo = rn(a s_m - hi); Ainv holds 1 / s_m.
-  // Stored pre-tiled for cp.async.bulk: per (128-row M-block, 16-wide K chunk) one
-  // 8 KiB record [hi | lo], each a 4 KiB UMMA K-major SWIZZLE_32B image (8-row x 32 B
-  // atoms, 16 B chunk index ^= row bit 2).
+  // A''_alpha for the tensor cores (kernels_tc.cu): per pair row p (filter theta = -1 of
+  // its beta, or phi_F) the real and imaginary parts of A_alpha[p][lambda], scaled by a
+  // power of two s_p (max(|Re|, |Im|) s_p in [2^13, 2^14)) and split into fp16
+  // hi = rn(a s_p), lo = rn(a s_p - hi), packed along K as [hi | hi | lo] (3K columns,
+  // padded to 16) against KY's B rows [Y_hi; Y_lo; Y_hi]: one MMA chain then sums
+  // A_hi Y_hi + A_hi Y_lo + A_lo Y_hi.  Stored pre-tiled for cp.async.bulk: per (128-row
+  // M-block, 16-wide K chunk) one 8 KiB record [Re | Im], each a 4 KiB UMMA K-major
+  // SWIZZLE_32B image (8-row x 32 B atoms, 16 B chunk index ^= row bit 2).  Ainv = 1 / s_p.
   P.A16.clear();
   P.Ainv.clear();
   for (auto& d : P.kd) {
-    const int K2 = 2 * d.K;
-    const int nkc = (K2 + 15) / 16;
-    const int nblk = P.Mpad / 128;
+    const int K3 = 3 * d.K;
+    const int nkc = (K3 + 15) / 16;
+    const int nblk = P.Mpp / 128;
     d.tc_a16_off = (int64_t)P.A16.size();
     d.tc_ainv_off = (int64_t)P.Ainv.size();
     const size_t base = P.A16.size();
     P.A16.resize(base + (size_t)nblk * nkc * 4096, 0);
-    P.Ainv.resize(P.Ainv.size() + P.Mpad, 1.f);
-    std::vector<int> row_f(P.Mpad, -1), row_i(P.Mpad, 0);
-    for (size_t fi = 0; fi < P.fr.size(); ++fi)
+    P.Ainv.resize(P.Ainv.size() + P.Mpp, 1.f);
+    std::vector<int> row_f(P.Mpp, -1), row_i(P.Mpp, 0);
+    for (int fi = 0; fi < nb; ++fi)
       for (int i = 0; i < P.fr[fi].nrows; ++i) {
-        row_f[P.fr[fi].row0 + i] = (int)fi;
+        row_f[P.fr[fi].row0 + i] = fi;
         row_i[P.fr[fi].row0 + i] = i;
       }
+    for (int i = 0; i < P.fr[2 * nb].nrows; ++i) {
+      row_f[P.fr[2 * nb].row0 + i] = 2 * nb;
+      row_i[P.fr[2 * nb].row0 + i] = i;
+    }
     auto put = [&](int m, int img, int col, uint16_t h) {
       const int mb = m / 128, r = m % 128, kc = col / 16, kk = col % 16;
       const uint32_t o = (uint32_t)((r / 8) * 256 + (r % 8) * 32 + kk * 2);
@@ -473,27 +502,30 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       P.A16[base + ((size_t)mb * nkc + kc) * 4096 + (size_t)img * 2048 + sw / 2] = h;
     };
     std::vector<std::complex<double>> arow(d.K);
-    for (int m = 0; m < P.Mpad; ++m) {
+    for (int m = 0; m < P.Mpp; ++m) {
       if (row_f[m] < 0) continue;
-      const auto& f = P.fr[row_f[m]];
+      const int fi = row_f[m];
+      const auto& f = P.fr[fi];
       const int rp = f.rprime[row_i[m]];
+      const bool real_taps = f.kind == 1;  // phi_F: real, even spectrum -> real taps
       double amax = 0;
       for (int lam = 0; lam < d.K; ++lam) {
         const int idx = (((rp << f.k) - lam) % P.N_fr + P.N_fr) % P.N_fr;
-        arow[lam] = htap[row_f[m]][idx];
+        arow[lam] = real_taps ? std::complex<double>(htap[fi][idx].real(), 0.0) : htap[fi][idx];
         amax = std::max(amax, std::max(std::abs(arow[lam].real()), std::abs(arow[lam].imag())));
       }
       if (amax == 0) continue;
       const int E = std::ilogb(amax);            // amax in [2^E, 2^(E+1))
-      const double s = std::ldexp(1.0, 13 - E);  // amax * s in [2^13, 2^14)
+      const double sc = std::ldexp(1.0, 13 - E);  // amax * sc in [2^13, 2^14)
       P.Ainv[d.tc_ainv_off + m] = (float)std::ldexp(1.0, E - 13);
       for (int lam = 0; lam < d.K; ++lam) {
-        const double v[2] = {arow[lam].real() * s, arow[lam].imag() * s};
-        for (int c = 0; c < 2; ++c) {
+        const double v[2] = {arow[lam].real() * sc, arow[lam].imag() * sc};
+        for (int c = 0; c < 2; ++c) {  // image 0: Re A, image 1: Im A
           const uint16_t h = half_rn(v[c]);
           const uint16_t l = half_rn(v[c] - half_to_double(h));
-          put(m, 0, 2 * lam + c, h);
-          put(m, 1, 2 * lam + c, l);
+          put(m, c, lam, h);
+          put(m, c, d.K + lam, h);
+          put(m, c, 2 * d.K + lam, l);
         }
       }
     }
@@ -526,9 +558,9 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     mom_tabs.assign(P.kd.size(), {});
     for (size_t ai = 0; ai < P.kd.size(); ++ai) {
       auto& d = P.kd[ai];
-      const int K16 = (2 * d.K + 15) / 16 * 16;
+      const int K48 = (3 * d.K + 15) / 16 * 16;
       d.y16_off = P.y16_total;
-      P.y16_total += (int64_t)2 * K16 * 2 * d.L;  // [hi | lo][K16][2L]: complex block along N
+      P.y16_total += (int64_t)K48 * 2 * d.L;  // [Y_hi; Y_lo; Y_hi][2L] rows, (re, im) interleaved (KY)
       d.ys_off = P.ys_total;
       P.ys_total += std::max(1, d.L / 32);  // one slot per tile; tiles have >= 32 columns (plan_tc checks)
       const float* g = P.g.data() + d.g_off;
