@@ -198,10 +198,32 @@ JTFS_API jtfs_status jtfs_partials_size(jtfs_plan_t plan, int64_t* floats_per_si
  * out: device fp32 [B][floats_per_signal] -- receives S0 and S1 only.  ws must
  * be kept untouched until jtfs_reduce_pack (it holds the phi_T-averaged first
  * order Y_phi).  B must not exceed the plan's micro-batch (JTFS_ERR_INVALID_ARG
- * otherwise; c4 uses B = 1).  Asynchronous on `stream`. */
+ * otherwise; c4 uses B = 1).  Synchronises `stream` once (it uploads the unit list
+ * per call); jtfs_forward_unitset is the asynchronous, capturable form. */
 JTFS_API jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B,
                                         const int32_t* unit_ids, int32_t n_units, float* partials,
                                         float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* A unit set bound once to device tables (host list -> device, synchronous at creation),
+ * so the sharded forward below never synchronises and can be captured in a CUDA graph.
+ * The set belongs to `plan` (destroy it before the plan); NULL-safe destroy. */
+typedef struct jtfs_unitset_s* jtfs_unitset_t;
+JTFS_API jtfs_status jtfs_unitset_create(jtfs_plan_t plan, const int32_t* unit_ids, int32_t n_units,
+                                         jtfs_unitset_t* out);
+JTFS_API jtfs_status jtfs_unitset_destroy(jtfs_unitset_t set);
+
+/* jtfs_forward_units with a bound unit set: same arguments and results, asynchronous on
+ * `stream` with no host synchronisation (graph-capturable).  (jtfs_forward_units binds a
+ * temporary set per call and synchronises `stream` before releasing it.) */
+JTFS_API jtfs_status jtfs_forward_unitset(jtfs_plan_t plan, const float* x, int64_t B, jtfs_unitset_t set,
+                                          float* partials, float* out, void* ws, size_t ws_bytes,
+                                          void* stream);
+
+/* Float range [begin, end) of one signal's partials buffer that unit `unit` writes (its
+ * chunk's slices; every other unit's range is disjoint).  Unit ids are ordered like the
+ * buffer: a contiguous id range owns one contiguous float range, which is what a sharded
+ * forward exchanges.  Host query. */
+JTFS_API jtfs_status jtfs_unit_partials_range(jtfs_plan_t plan, int32_t unit, int64_t* begin, int64_t* end);
 
 /* Eq. (3)/(4) completion from summed partials (device fp32 [B][partials_size])
  * and the Y_phi left in ws by jtfs_forward_units on the same plan: phi_F pooling,

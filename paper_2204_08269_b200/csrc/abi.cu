@@ -823,14 +823,18 @@ jtfs_status jtfs_partials_size(jtfs_plan_t plan, int64_t* floats_per_signal) {
   return JTFS_OK;
 }
 
-jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B, const int32_t* unit_ids,
-                               int32_t n_units, float* partials, float* out, void* ws, size_t ws_bytes,
-                               void* stream) {
-  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
-  if (s != JTFS_OK) return s;
+}  // extern "C"
+
+struct jtfs_unitset_s {
+  jtfs_plan_t plan = nullptr;
+  int device = -1;
+  int32_t* d_sel = nullptr;  // per-alpha ascending chunk ids, concatenated (device)
+  std::vector<int> off, cnt;
+};
+
+namespace {
+jtfs_status build_unitset(jtfs_plan_t plan, const int32_t* unit_ids, int32_t n_units, jtfs_unitset_s& set) {
   jtfs::Plan& P = plan->P;
-  if (B > P.mb) return fail(JTFS_ERR_INVALID_ARG, "forward_units: B exceeds the plan's micro-batch");
-  if (!partials || ((uintptr_t)partials & 15)) return fail(JTFS_ERR_INVALID_ARG, "partials NULL or misaligned");
   if (n_units < 0 || (n_units > 0 && !unit_ids)) return fail(JTFS_ERR_INVALID_ARG, "bad unit list");
   std::vector<jtfs_unit_t> table;
   unit_table(P, table);
@@ -844,24 +848,47 @@ jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B, cons
     seen[id] = 1;
     per[table[id].alpha].push_back(table[id].chunk);
   }
-  jtfs::UnitSel sel;
   std::vector<int32_t> flat;
+  set.off.clear();
+  set.cnt.clear();
   for (auto& v : per) {
     std::sort(v.begin(), v.end());
-    sel.off.push_back((int)flat.size());
-    sel.cnt.push_back((int)v.size());
+    set.off.push_back((int)flat.size());
+    set.cnt.push_back((int)v.size());
     flat.insert(flat.end(), v.begin(), v.end());
   }
+  set.plan = plan;
+  set.device = P.device;
+  DeviceGuard guard(P.device);
+  cudaError_t e = cudaMalloc(&set.d_sel, std::max<size_t>(flat.size(), 1) * 4);
+  if (e == cudaSuccess && !flat.empty())
+    e = cudaMemcpy(set.d_sel, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (set.d_sel) cudaFree(set.d_sel);
+    set.d_sel = nullptr;
+    return cuda_fail(e, "unit set upload");
+  }
+  return JTFS_OK;
+}
+
+jtfs_status run_unitset(jtfs_plan_t plan, const float* x, int64_t B, const jtfs_unitset_s& set, float* partials,
+                        float* out, void* ws, size_t ws_bytes, void* stream) {
+  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK) return s;
+  jtfs::Plan& P = plan->P;
+  if (set.plan != plan) return fail(JTFS_ERR_INVALID_ARG, "unit set bound to another plan");
+  if (B > P.mb) return fail(JTFS_ERR_INVALID_ARG, "forward_units: B exceeds the plan's micro-batch");
+  if (!partials || ((uintptr_t)partials & 15)) return fail(JTFS_ERR_INVALID_ARG, "partials NULL or misaligned");
   if (B == 0) return JTFS_OK;
   DeviceGuard guard(P.device);
   cudaStream_t st = (cudaStream_t)stream;
   WsPtrs w = carve(P, ws, B);
   cudaError_t e = cudaMemsetAsync(partials, 0, (size_t)B * P.part_total * 4, st);
-  if (e == cudaSuccess && !flat.empty())
-    e = cudaMemcpyAsync(w.sel, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host list is a local
   if (e != cudaSuccess) return cuda_fail(e, "forward_units setup");
-  sel.d_sel = w.sel;
+  jtfs::UnitSel sel;
+  sel.d_sel = set.d_sel;
+  sel.off = set.off;
+  sel.cnt = set.cnt;
   RunOpts o;
   o.sel = &sel;
   o.part = partials;
@@ -869,7 +896,72 @@ jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B, cons
   const std::string err = run_microbatch(P, x, (int)B, out, w, false, 99, st, o);
   if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+jtfs_status jtfs_unitset_create(jtfs_plan_t plan, const int32_t* unit_ids, int32_t n_units, jtfs_unitset_t* out) {
+  if (!plan || !out) return fail(JTFS_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (plan->P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");
+  jtfs_unitset_s* set = new (std::nothrow) jtfs_unitset_s();
+  if (!set) return fail(JTFS_ERR_OOM, "host allocation failed");
+  const jtfs_status s = build_unitset(plan, unit_ids, n_units, *set);
+  if (s != JTFS_OK) {
+    delete set;
+    return s;
+  }
+  *out = set;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_unitset_destroy(jtfs_unitset_t set) {
+  if (!set) return JTFS_OK;
+  if (set->d_sel) {
+    DeviceGuard guard(set->device);
+    cudaFree(set->d_sel);
+  }
+  delete set;
+  return JTFS_OK;
+}
+
+jtfs_status jtfs_forward_unitset(jtfs_plan_t plan, const float* x, int64_t B, jtfs_unitset_t set, float* partials,
+                                 float* out, void* ws, size_t ws_bytes, void* stream) {
+  if (!set) return fail(JTFS_ERR_INVALID_ARG, "unit set is NULL");
+  return run_unitset(plan, x, B, *set, partials, out, ws, ws_bytes, stream);
+}
+
+jtfs_status jtfs_forward_units(jtfs_plan_t plan, const float* x, int64_t B, const int32_t* unit_ids,
+                               int32_t n_units, float* partials, float* out, void* ws, size_t ws_bytes,
+                               void* stream) {
+  jtfs_status s = check_forward_args(plan, x, B, out, ws, ws_bytes);
+  if (s != JTFS_OK) return s;
+  jtfs_unitset_s set;
+  s = build_unitset(plan, unit_ids, n_units, set);
+  if (s != JTFS_OK) return s;
+  s = run_unitset(plan, x, B, set, partials, out, ws, ws_bytes, stream);
+  // the temporary device unit list is released after the enqueued work has used it
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  {
+    DeviceGuard guard(set.device);
+    cudaFree(set.d_sel);
+  }
+  if (s == JTFS_OK && e != cudaSuccess) return cuda_fail(e, "forward_units");
+  return s;
+}
+
+jtfs_status jtfs_unit_partials_range(jtfs_plan_t plan, int32_t unit, int64_t* begin, int64_t* end) {
+  if (!plan || !begin || !end) return fail(JTFS_ERR_INVALID_ARG, "NULL argument");
+  const jtfs::Plan& P = plan->P;
+  std::vector<jtfs_unit_t> table;
+  unit_table(P, table);
+  if (unit < 0 || unit >= (int32_t)table.size()) return fail(JTFS_ERR_INVALID_ARG, "unit id out of range");
+  const auto& d = P.kd[table[unit].alpha];
+  const int64_t per = (int64_t)(d.nslices / d.nchunks) * P.Mpad * P.n_frames;  // slices of one chunk
+  *begin = d.part_off + (int64_t)table[unit].chunk * per;
+  *end = *begin + per;
   return JTFS_OK;
 }
 

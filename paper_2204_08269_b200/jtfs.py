@@ -37,6 +37,7 @@ EXPORTS = [
     "jtfs_measure_fp32_peak", "jtfs_cost", "jtfs_profile_enable",
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
+    "jtfs_unitset_create", "jtfs_unitset_destroy", "jtfs_forward_unitset", "jtfs_unit_partials_range",
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
     "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions",
     "jtfs_mulog_mu", "jtfs_mulog_apply", "jtfs_forward_mulog", "jtfs_u2_map_shape", "jtfs_u2_map",
@@ -96,6 +97,10 @@ _lib.jtfs_profile_read_kd.argtypes = [_P, C.POINTER(C.c_double), C.c_int32, C.c_
 _lib.jtfs_units.argtypes = [_P, C.POINTER(jtfs_unit_t), C.c_int32, C.POINTER(C.c_int32)]
 _lib.jtfs_partials_size.argtypes = [_P, C.POINTER(C.c_int64)]
 _lib.jtfs_forward_units.argtypes = [_P, _P, C.c_int64, C.POINTER(C.c_int32), C.c_int32, _P, _P, _P, C.c_size_t, _P]
+_lib.jtfs_unitset_create.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32, C.POINTER(_P)]
+_lib.jtfs_unitset_destroy.argtypes = [_P]
+_lib.jtfs_forward_unitset.argtypes = [_P, _P, C.c_int64, _P, _P, _P, _P, C.c_size_t, _P]
+_lib.jtfs_unit_partials_range.argtypes = [_P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
 _lib.jtfs_reduce_pack.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_scat1d_layout.argtypes = [_P, C.POINTER(jtfs_scat1d_layout_t)]
 _lib.jtfs_scat1d_paths.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32]
@@ -302,6 +307,24 @@ class Plan:
                                        _ptr(ws), ws.numel(), _stream_handle(stream)), "jtfs_forward_units")
         return partials, out
 
+    def unitset(self, unit_ids):
+        """A unit set bound to device tables once (jtfs_unitset_create)."""
+        return UnitSet(self, unit_ids)
+
+    def forward_unitset(self, x, uset, partials, out, stream=None):
+        """forward_units with a bound set: asynchronous, graph-capturable (jtfs_forward_unitset)."""
+        B = x.shape[0]
+        ws = self.workspace(B, stream)
+        _check(_lib.jtfs_forward_unitset(self._h, _ptr(x), B, uset.handle, _ptr(partials), _ptr(out), _ptr(ws),
+                                         ws.numel(), _stream_handle(stream)), "jtfs_forward_unitset")
+        return partials, out
+
+    def unit_partials_range(self, unit: int):
+        """[begin, end) floats of one signal's partials that unit `unit` writes."""
+        a, b = C.c_int64(), C.c_int64()
+        _check(_lib.jtfs_unit_partials_range(self._h, unit, C.byref(a), C.byref(b)), "jtfs_unit_partials_range")
+        return a.value, b.value
+
     def reduce_pack(self, partials, out, stream=None):
         """phi_F pooling + phi paths + packing of S2 from summed partials (same workspace)."""
         B = partials.shape[0]
@@ -500,6 +523,30 @@ def isomap(F, K: int = 40, n_components: int = 3, stream=None):
     _check(_lib.jtfs_isomap(_ptr(F), n, d, F.stride(0), K, n_components, _ptr(emb), _ptr(ev), _ptr(ws), ws.numel(),
                             _stream_handle(stream)), "jtfs_isomap")
     return emb, ev
+
+
+class UnitSet:
+    """jtfs_unitset_create / jtfs_unitset_destroy."""
+
+    def __init__(self, plan: "Plan", unit_ids):
+        self.plan = plan            # keeps the plan alive while the set exists
+        self.ids = [int(i) for i in unit_ids]
+        arr = (C.c_int32 * max(len(self.ids), 1))(*self.ids)
+        h = _P()
+        _check(_lib.jtfs_unitset_create(plan.handle, arr, len(self.ids), C.byref(h)), "jtfs_unitset_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                _lib.jtfs_unitset_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 def measure_fp32_peak(device: int = 0):

@@ -3,19 +3,19 @@
 For a single long signal (config c4) the batch does not shard, but the joint
 stage does: its phi_T-pooled output (Eq. (3)) is a sum over
 time of per-(alpha, time chunk) contributions.  KD's work units are those
-(alpha, chunk) pairs (`Plan.units()`); each rank
+(alpha, chunk) pairs (`Plan.units()`), ordered like the partials buffer they
+write; each rank
 
-  1. runs the replicated first stages (Eqs. (1)-(2): KA..KC, S0/S1) and KD for
-     the units assigned to it (`Plan.forward_units`), whose partial slices are
-     disjoint from every other rank's (the rest of its buffer is zero);
-  2. contributes its partial buffer to a SUM reduction to rank 0 -- every slice
-     is nonzero on exactly one rank, so x + 0 + ... + 0 = x exactly and the
-     result does not depend on the reduction order or on the number of ranks;
-  3. rank 0 finishes Eq. (3) (phi_F pooling, phi paths, packing) with
+  1. owns one contiguous range of unit ids (`contiguous_assign`: the optimal
+     contiguous split of the modelled unit costs), hence one contiguous float range
+     of the partials buffer;
+  2. runs the replicated first stages (Eqs. (1)-(2): KA..KC, S0/S1) and KD for its
+     units (`Plan.forward_unitset`: a unit set bound once, no host sync);
+  3. sends exactly its range to rank 0 (NCCL point-to-point), which receives each
+     rank's range in place -- no arithmetic on the exchange, so the result is
+     byte-identical to `Plan.forward` on one GPU for any rank count;
+  4. rank 0 finishes Eq. (3) (phi_F pooling, phi paths, packing) with
      `Plan.reduce_pack`.
-
-The result is byte-identical to `Plan.forward` on one GPU.  Units are assigned by
-a deterministic longest-processing-time greedy on the plan's modelled unit cost.
 This module is plumbing only: all arithmetic of the path runs in libjtfs.so.
 """
 from __future__ import annotations
@@ -36,13 +36,80 @@ def lpt_assign(costs, world: int):
     return [sorted(p) for p in parts]
 
 
-def exchange_partials(partials, group=None, dst: int = 0):
-    """Sum the ranks' disjoint partial buffers onto `dst` (in place there).
+def contiguous_assign(costs, world: int):
+    """Split unit ids 0..n-1 into `world` contiguous ranges minimising the largest range
+    cost (binary search on the bound + greedy fill; deterministic).  Returns per-rank
+    (first, last + 1) id ranges (possibly empty)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    c = [float(v) for v in costs]
 
-    Exact because each slice is nonzero on exactly one rank."""
+    def fill(bound):
+        parts, start, acc = [], 0, 0.0
+        for i, v in enumerate(c):
+            if acc + v > bound and i > start:
+                parts.append((start, i))
+                start, acc = i, 0.0
+            acc += v
+        parts.append((start, len(c)))
+        return parts
+
+    lo, hi = max(c, default=0.0), sum(c)
+    for _ in range(100):
+        mid = 0.5 * (lo + hi)
+        if len(fill(mid)) <= world:
+            hi = mid
+        else:
+            lo = mid
+    parts = fill(hi)
+    while len(parts) < world:
+        parts.append((len(c), len(c)))
+    return parts
+
+
+def owned_range(plan, first: int, last: int):
+    """[begin, end) floats of one signal's partials written by units first..last-1."""
+    if last <= first:
+        return 0, 0
+    return plan.unit_partials_range(first)[0], plan.unit_partials_range(last - 1)[1]
+
+
+def exchange_partials(partials, ranges, group=None, dst: int = 0):
+    """Every rank sends its own contiguous partials range ranges[rank] = (b, e) (floats
+    per signal) to `dst`, which receives each into place: an exact copy, no reduction
+    (every float is written by exactly one rank's units)."""
     import torch.distributed as dist
-    dist.reduce(partials, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    reqs = []
+    if rank == dst:
+        for r in range(world):
+            b, e = ranges[r]
+            if r != dst and e > b:
+                buf = partials[:, b:e].contiguous() if partials.shape[0] > 1 else partials[0, b:e]
+                reqs.append((dist.irecv(buf, src=dist.get_global_rank(group, r) if group else r, group=group), buf, b, e))
+        for q, buf, b, e in reqs:
+            q.wait()
+            if partials.shape[0] > 1:
+                partials[:, b:e] = buf.view(partials.shape[0], e - b)
+    else:
+        b, e = ranges[rank]
+        if e > b:
+            buf = partials[:, b:e].contiguous() if partials.shape[0] > 1 else partials[0, b:e]
+            dist.send(buf, dst=dist.get_global_rank(group, dst) if group else dst, group=group)
     return partials
+
+
+_SETS = {}
+
+
+def _unitset(plan, first, last):
+    key = (id(plan), first, last)
+    us = _SETS.get(key)
+    if us is None or us.plan is not plan:
+        us = plan.unitset(range(first, last))
+        _SETS[key] = us
+    return us
 
 
 def forward_sharded(plan, x, group=None, stream=None):
@@ -52,17 +119,17 @@ def forward_sharded(plan, x, group=None, stream=None):
     import torch.distributed as dist
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    units = plan.units()
-    mine = lpt_assign([u["cost"] for u in units], world)[rank]
+    parts = contiguous_assign([u["cost"] for u in plan.units()], world)
+    first, last = parts[rank]
     B = x.shape[0]
-    # every step (KD, the NCCL reduce, KE) is ordered on ONE stream: torch's collectives
-    # run on the current stream, so a caller's stream becomes the current one here
+    # every step (KD, the NCCL exchange, KE) is ordered on ONE stream: torch's
+    # point-to-point ops run on the current stream, so a caller's stream becomes it here
     with torch.cuda.stream(stream) if stream is not None else _nullctx():
         partials = torch.empty(B, plan.partials_size, dtype=torch.float32, device=x.device)
         out = torch.empty(B, plan.floats_per_signal, dtype=torch.float32, device=x.device)
-        plan.forward_units(x, mine, partials, out)
+        plan.forward_unitset(x, _unitset(plan, first, last), partials, out)
         if world > 1:
-            exchange_partials(partials, group=group, dst=0)
+            exchange_partials(partials, [owned_range(plan, a, b) for a, b in parts], group=group, dst=0)
         if rank != 0:
             return None
         plan.reduce_pack(partials, out)
@@ -116,10 +183,10 @@ def forward_batch_sharded(plan, x_full, group=None, gather: bool = True, stream=
     float32 [B, N]) with no data-path collective; with `gather` the records are
     all-gathered (one NCCL all_gather_into_tensor).  Outputs are byte-identical to a
     single-GPU forward (the per-signal computation does not depend on B or the split)."""
+    import torch
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    import torch
     b0, b1 = batch_slice(x_full.shape[0], world, rank)
     with torch.cuda.stream(stream) if stream is not None else _nullctx():  # forward and gather on one stream
         out = plan.forward(x_full[b0:b1].contiguous())
