@@ -30,13 +30,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB) -> str:
+    """Compile libjtfs.so (or, for A/B measurements of a compile-time variant, `lib` with
+    extra -D `defines`; select it at run time with JTFS_LIB=<path>)."""
+    if not force and not defines and lib == LIB and not _stale():
         return LIB
     objs, procs = [], []
+    tag = "" if lib == LIB else "." + os.path.basename(lib)
     for src in SOURCES:  # the translation units compile concurrently
-        obj = os.path.join(CSRC, src + ".o")
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(CSRC, src + tag + ".o")
+        cmd = [NVCC, *FLAGS, *("-D" + d for d in defines), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((subprocess.Popen(cmd), cmd))
@@ -45,13 +48,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if pr.wait() != 0:
             raise subprocess.CalledProcessError(pr.returncode, cmd)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-           *objs, "-o", LIB + ".tmp"]
+           *objs, "-o", lib + ".tmp"]
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_2204_08269_b200.build [--force] [-DNAME=VALUE ... --lib PATH]
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = sys.argv[sys.argv.index("--lib") + 1] if "--lib" in sys.argv else LIB
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs, lib=out))

@@ -46,6 +46,10 @@
 #include "jtfs_internal.h"
 #include "kernels.h"
 
+#ifndef JTFS_KD_FMA_SQRT_COLS
+#define JTFS_KD_FMA_SQRT_COLS 0
+#endif
+
 namespace jtfs {
 namespace tc {
 
@@ -233,22 +237,64 @@ __device__ __forceinline__ void reg_fence16(uint32_t (&v)[16]) {
   for (int i = 0; i < 16; ++i) asm volatile("" : "+r"(v[i]));
 }
 
+// ---- packed FP32x2 arithmetic (FFMA2 / FMUL2 / FADD2: two lanes per instruction; a
+// scalar or an immediate operand is broadcast to both halves) ----
+__device__ __forceinline__ unsigned long long f2_u64(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 u64_f2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)), "l"(f2_u64(c)));
+  return u64_f2(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(r);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(r);
+}
+
+// (sqrt q.x, sqrt q.y) on the FMA pipe (to offload MUFU, 16 / clk / SM): the classic
+// magic-constant rsqrt seed (integer ALU), two packed Newton steps y <- y (3/2 - q/2 y^2),
+// s = q y and one Heron correction s <- s - y (s^2 - q) / 2; <= 1.5 ulp (checked against
+// fp64 over 60 decades), exactly 0 for q = 0.  Deterministic, like MUFU.SQRT.
+__device__ __forceinline__ float2 sqrt2_fma(float2 q) {
+  float2 y = make_float2(__uint_as_float(0x5f3759dfu - (__float_as_uint(q.x) >> 1)),
+                         __uint_as_float(0x5f3759dfu - (__float_as_uint(q.y) >> 1)));
+  const float2 h = mul2(q, make_float2(-0.5f, -0.5f));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) y = mul2(y, fma2(mul2(h, y), y, make_float2(1.5f, 1.5f)));
+  const float2 sq = mul2(q, y);
+  const float2 r = fma2(sq, sq, add2(h, h));  // s^2 - q
+  return fma2(mul2(y, r), make_float2(-0.5f, -0.5f), sq);
+}
+
+// columns of each 8-column group whose moduli take the FMA-pipe square root (the rest
+// take MUFU.SQRT): balances the MUFU and FMA pipes of the epilogue
+constexpr int kFmaSqrtCols = JTFS_KD_FMA_SQRT_COLS;
+
 // Both spins of a pair row from its four real products at 8 time columns:
 // v1 = acc1 (Re A . [Yr, Yi]), v2 = acc2 (Im A . [Yr, Yi]), interleaved (Yr, Yi) per column:
 //   Z_-1 = A Y      = (P1 - P2) + i (P3 + P4),   Z_+1 = conj(A) Y = (P1 + P2) + i (P3 - P4)
 // with P1 = Re A Yr, P2 = Im A Yi, P3 = Re A Yi, P4 = Im A Yr (h_{+1} = conj h_{-1}, R10).
-__device__ __forceinline__ void spin_mags(const uint32_t (&v1)[16], const uint32_t (&v2)[16], float (&mm)[8],
-                                          float (&mp)[8]) {
+// Packed per column: X = (Re Z_-, Re Z_+) = (-1, 1) P2 + P1, Y = (Im Z_-, Im Z_+) = (1, -1) P4
+// + P3, Q = X X + Y Y = (|Z_-|^2, |Z_+|^2): four FP32x2 instructions, then two MUFU.SQRT.
+// mz[j] = (|Z_-|, |Z_+|) of column j.
+__device__ __forceinline__ void spin_mags(const uint32_t (&v1)[16], const uint32_t (&v2)[16], float2 (&mz)[8]) {
+  const float2 cm = make_float2(-1.f, 1.f), cp = make_float2(1.f, -1.f);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float p1 = __uint_as_float(v1[2 * j]), p3 = __uint_as_float(v1[2 * j + 1]);
     const float p4 = __uint_as_float(v2[2 * j]), p2 = __uint_as_float(v2[2 * j + 1]);
-    const float rm = p1 - p2, im_ = p3 + p4, rp = p1 + p2, ip = p3 - p4;
-    mm[j] = sqrt_fast(fmaf(rm, rm, im_ * im_));
-    mp[j] = sqrt_fast(fmaf(rp, rp, ip * ip));
+    const float2 X = fma2(cm, make_float2(p2, p2), make_float2(p1, p1));
+    const float2 Y = fma2(cp, make_float2(p4, p4), make_float2(p3, p3));
+    const float2 Q = fma2(X, X, mul2(Y, Y));
+    mz[j] = (j >= 8 - kFmaSqrtCols) ? sqrt2_fma(Q) : make_float2(sqrt_fast(Q.x), sqrt_fast(Q.y));
   }
 }
-
 // ---------------------------------------------------------------------------------
 // KY: one CTA per (signal, tile of Nt columns): max |Re|, |Im| of Y2_alpha over the K x Nt
 // tile -> s_Y (power of two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y -
@@ -371,42 +417,40 @@ __device__ __forceinline__ void epi_group_taps(uint32_t tb1, uint32_t tb2, const
   tmem_wait_ld();
   reg_fence16(v1);
   reg_fence16(v2);
-  float mm[8], mp[8];
-  spin_mags(v1, v2, mm, mp);
+  float2 mz[8];
+  spin_mags(v1, v2, mz);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float4* w4 = reinterpret_cast<const float4*>(wt + (8 * G + j) * NF);
 #pragma unroll
     for (int m4 = 0; m4 < NF / 4; ++m4) {
       const float4 w = w4[m4];
-      pm[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mm[j], pm[2 * m4 + 0]);
-      pm[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mm[j], pm[2 * m4 + 1]);
-      pp[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mp[j], pp[2 * m4 + 0]);
-      pp[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mp[j], pp[2 * m4 + 1]);
+      pm[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mz[j].x, pm[2 * m4 + 0]);
+      pm[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mz[j].x, pm[2 * m4 + 1]);
+      pp[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), mz[j].y, pp[2 * m4 + 0]);
+      pp[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), mz[j].y, pp[2 * m4 + 1]);
     }
   }
 }
+// moments of both spins, packed: S[k] = (sum_j |Z_-,j| u_j^k, sum_j |Z_+,j| u_j^k), u_j
+// compile-time (FFMA2 with an immediate operand)
 template <int G>
-__device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float (&Sm)[4], float (&Sp)[4]) {
+__device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2 (&S)[4]) {
   uint32_t v1[16], v2[16];
   tmem_ld16(tb1 + 16 * G, v1);
   tmem_ld16(tb2 + 16 * G, v2);
   tmem_wait_ld();
   reg_fence16(v1);
   reg_fence16(v2);
-  float mm[8], mp[8];
-  spin_mags(v1, v2, mm, mp);
+  float2 mz[8];
+  spin_mags(v1, v2, mz);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float u = ((float)(8 * G + j) - 15.5f) * 0.0625f;  // compile-time
-    Sm[0] += mm[j];
-    Sm[1] = fmaf(mm[j], u, Sm[1]);
-    Sm[2] = fmaf(mm[j], u * u, Sm[2]);
-    Sm[3] = fmaf(mm[j], u * u * u, Sm[3]);
-    Sp[0] += mp[j];
-    Sp[1] = fmaf(mp[j], u, Sp[1]);
-    Sp[2] = fmaf(mp[j], u * u, Sp[2]);
-    Sp[3] = fmaf(mp[j], u * u * u, Sp[3]);
+    S[0] = add2(S[0], mz[j]);
+    S[1] = fma2(mz[j], make_float2(u, u), S[1]);
+    S[2] = fma2(mz[j], make_float2(u * u, u * u), S[2]);
+    S[3] = fma2(mz[j], make_float2(u * u * u, u * u * u), S[3]);
   }
 }
 
@@ -626,12 +670,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.pool_mode == 1) {
           // moment form (Nt = 64: this set's 32 columns are one 32-column block):
           // S_k = sum_j |Z_j| u_j^k (k <= 3, u_j compile-time), then part += G_k S_k
-          float Sm[4] = {0.f, 0.f, 0.f, 0.f}, Sp[4] = {0.f, 0.f, 0.f, 0.f};
+          float2 S[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           if constexpr (half == 32) {
-            epi_group_mom<0>(tb1, tb2, Sm, Sp);
-            epi_group_mom<1>(tb1, tb2, Sm, Sp);
-            epi_group_mom<2>(tb1, tb2, Sm, Sp);
-            epi_group_mom<3>(tb1, tb2, Sm, Sp);
+            epi_group_mom<0>(tb1, tb2, S);
+            epi_group_mom<1>(tb1, tb2, S);
+            epi_group_mom<2>(tb1, tb2, S);
+            epi_group_mom<3>(tb1, tb2, S);
           }
           tc_fence_before();
           __syncwarp();
@@ -642,10 +686,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int m4 = 0; m4 < NF / 4; ++m4) {
               const float4 w = g4[k * (NF / 4) + m4];
-              pm[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), Sm[k], pm[2 * m4 + 0]);
-              pm[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), Sm[k], pm[2 * m4 + 1]);
-              pp[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), Sp[k], pp[2 * m4 + 0]);
-              pp[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), Sp[k], pp[2 * m4 + 1]);
+              pm[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), S[k].x, pm[2 * m4 + 0]);
+              pm[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), S[k].x, pm[2 * m4 + 1]);
+              pp[2 * m4 + 0] = ffma2(make_float2(w.x, w.y), S[k].y, pp[2 * m4 + 0]);
+              pp[2 * m4 + 1] = ffma2(make_float2(w.z, w.w), S[k].y, pp[2 * m4 + 1]);
             }
         } else {
           epi_group_taps<NF, 0>(tb1, tb2, wt, pm, pp);
