@@ -1148,7 +1148,8 @@ jtfs_status jtfs_cost(jtfs_plan_t plan, double* flops, double* bytes, int32_t ca
     const double K16 = d.tc_K16, L = d.L, M = P.Mpp;
     f[6] += 8.0 * M * K16 * L;
     const double tiles = L / std::max(d.tc_Nt, 1);
-    b[6] += tiles * P.tc_n_mpart * (P.tc_n_mblk * (double)d.tc_nkc * 8192.0 + 4.0 * d.tc_K16 * d.tc_Nt);
+    // A stationary: A loaded once per CTA (negligible per signal); else streamed per tile
+    b[6] += tiles * d.tc_mpart * ((d.tc_stat ? 0.0 : d.tc_mblk * (double)d.tc_nkc * 8192.0) + 4.0 * d.tc_K16 * d.tc_Nt);
   }
   for (int i = 0; i < std::min(cap, 7); ++i) {
     if (flops) flops[i] = f[i];

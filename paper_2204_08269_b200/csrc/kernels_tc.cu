@@ -362,6 +362,7 @@ struct TcParams {
   const int32_t* chunk_sel;  // selected chunks (path sharding) or nullptr = all
   int nsel;        // number of selected chunks
   int n_mpart, n_mblk;  // M-parts and 128-pair-row M-blocks per part
+  int stat;        // 1: A stationary (the CTA's part loaded once; grid % n_mpart == 0), 0: A ring
   int L, nframes, Mpp;
   int nsig;
   unsigned long long* prof;  // measurement only (JTFS_KD_PROF flag): per-role wait-cycle counters or nullptr
@@ -380,11 +381,15 @@ constexpr int kThreads = 352;
 constexpr int kProdWarp = 8, kMmaWarp = 9, kBWarp = 10;
 constexpr int kNbuf = 2;  // TMEM accumulator buffers, each [acc1 | acc2] of 2 x 2 Nt columns
 
-// shared-memory carve-up (host and device agree through this function)
+// shared-memory carve-up (host and device agree through this function): B tile buffers,
+// the A region (a ring of S stages of rps records, or the n_mblk x nkc records of the CTA's
+// M-part when A is stationary), the pooling table buffers, the barriers (nab A barrier
+// pairs: S ring slots or n_mblk stationary blocks)
 struct SmemLayout {
   uint32_t b[2], ast, wt, bars, total;
 };
-__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int S, int rps, int NF, int pool_mode) {
+__host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, uint32_t abytes, int nab, int NF,
+                                                  int pool_mode) {
   SmemLayout l{};
   auto up = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
   uint32_t o = 0;
@@ -398,11 +403,11 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, int 
     }
   }
   l.ast = o;
-  o += (uint32_t)S * rps * kRec;
+  o += abytes;
   l.wt = o;  // [2][Nt][NF] taps, or [2][Nt / 32][4][NF] moment coefficients
   o += (uint32_t)(2 * Nt * (pool_mode ? NF / 8 : NF) * 4);
   l.bars = up(o, 8);
-  o = l.bars + 8 * (4 + 4 + 2 * kNbuf + 2 * S) + 16;
+  o = l.bars + 8 * (4 + 4 + 2 * kNbuf + 2 * nab) + 16;
   l.total = o + 1024;  // + alignment slack of the dynamic smem base
   return l;
 }
@@ -464,7 +469,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   constexpr int Nt = NTC;
-  const SmemLayout lay = smem_layout(p.K16, Nt, p.NBB, p.S, p.rps, NF, p.pool_mode);
+  const int nab = p.stat ? p.n_mblk : p.S;  // A barrier pairs
+  const SmemLayout lay = smem_layout(p.K16, Nt, p.NBB, p.stat ? (uint32_t)(p.n_mblk * p.nkc * kRec)
+                                                              : (uint32_t)(p.S * p.rps * kRec),
+                                     nab, NF, p.pool_mode);
   const int wfl = Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
   uint8_t* Ast = base + lay.ast;
   float* Wt = reinterpret_cast<float*>(base + lay.wt);
@@ -475,9 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* w_empty = bars + 6;     // [2] epilogue done with the taps
   uint64_t* acc_full = bars + 8;    // [kNbuf]
   uint64_t* acc_empty = bars + 8 + kNbuf;
-  uint64_t* a_full = bars + 8 + 2 * kNbuf;  // [S]
-  uint64_t* a_empty = a_full + p.S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + p.S);
+  uint64_t* a_full = bars + 8 + 2 * kNbuf;  // [nab]
+  uint64_t* a_empty = a_full + nab;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + nab);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -491,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(acc_full + i, 1);
       mbar_init(acc_empty + i, 8);
     }
-    for (int i = 0; i < p.S; ++i) {
+    for (int i = 0; i < nab; ++i) {
       mbar_init(a_full + i, 1);
       mbar_init(a_empty + i, 1);
     }
@@ -546,11 +554,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kProdWarp) {
     // ===================== A producer =====================
-    // Bulk copies issued by one thread complete one after another (~600 cycles
-    // each, measured with tools/bulk_bw.cu), so lane s serves ring slot s (S lanes
-    // issue in parallel; a slot is always served by the same lane, which keeps its
-    // parity waits unambiguous).
-    if (lane < p.S) {
+    if (p.stat) {
+      // stationary: the CTA always works on M-part blockIdx % n_mpart (grid % n_mpart == 0);
+      // lane mb copies M-block mb's nkc records once, for the whole launch
+      const int mpart = (int)blockIdx.x % p.n_mpart;
+      if (lane < p.n_mblk) {
+        const uint32_t bytes = (uint32_t)(p.nkc * kRec);
+        mbar_expect_tx(a_full + lane, bytes);
+        bulk_load(Ast + (size_t)lane * bytes, p.A + (size_t)(mpart * p.n_mblk + lane) * p.nkc * (kRec / 2), bytes,
+                  a_full + lane);
+      }
+    } else if (lane < p.S) {
+      // ring: bulk copies issued by one thread complete one after another (~600 cycles
+      // each, measured with tools/bulk_bw.cu), so lane s serves ring slot s (S lanes issue in
+      // parallel; a slot is always served by the same lane: unambiguous parity waits)
       uint32_t s = 0, ph = 0;
       for (int gt = 0; gt < my_tiles; ++gt) {
         const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
@@ -591,28 +608,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_t<PROF>(acc_empty + ab, (use + 1) & 1, w_acc);
         tc_fence_after();
         const uint32_t d1 = tmem_base + ab * 4u * (uint32_t)Nt, d2 = d1 + 2u * (uint32_t)Nt;
-        for (int st = 0; st < nst; ++st) {
-          mbar_wait_t<PROF>(a_full + s, ph, w_a);
+        if (p.stat) {
+          // the M-block's records stay resident: wait once for their copy (phase 0)
+          mbar_wait_t<PROF>(a_full + mb, 0u, w_a);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t dst = dA0 + (uint64_t)((s * stage_bytes) >> 4);
-#pragma unroll
-            for (int r = 0; r < kMaxRps; ++r) {
-              const int kc = p.rps * st + r;
-              if (r < p.rps && kc < p.nkc) {
-                const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
-                const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
-                const uint32_t acc0 = kc > 0 ? 1u : 0u;
-                mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
-                mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
-              }
+            const uint64_t a0 = dA0 + (uint64_t)(((uint32_t)mb * (uint32_t)p.nkc * kRec) >> 4);
+            for (int kc = 0; kc < p.nkc; ++kc) {
+              const uint64_t a = a0 + (uint64_t)((kc * kRec) >> 4);
+              const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
+              const uint32_t acc0 = kc > 0 ? 1u : 0u;
+              mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
+              mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
             }
-            mma_commit(a_empty + s);
           }
           __syncwarp();
-          if (++s == (uint32_t)p.S) {
-            s = 0;
-            ph ^= 1;
+        } else {
+          for (int st = 0; st < nst; ++st) {
+            mbar_wait_t<PROF>(a_full + s, ph, w_a);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t dst = dA0 + (uint64_t)((s * stage_bytes) >> 4);
+#pragma unroll
+              for (int r = 0; r < kMaxRps; ++r) {
+                const int kc = p.rps * st + r;
+                if (r < p.rps && kc < p.nkc) {
+                  const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
+                  const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
+                  const uint32_t acc0 = kc > 0 ? 1u : 0u;
+                  mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
+                  mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
+                }
+              }
+              mma_commit(a_empty + s);
+            }
+            __syncwarp();
+            if (++s == (uint32_t)p.S) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
         if (elect_one()) mma_commit(acc_full + ab);
@@ -798,7 +832,8 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, void* base, int rank, const 
 
 int nf_of(int nframes) { return nframes <= 8 ? 8 : nframes <= 16 ? 16 : 32; }
 size_t tc_smem(const AlphaKD& d, int nf) {
-  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, d.tc_S, d.tc_rps, nf, d.pool_mode).total;
+  const uint32_t abytes = d.tc_stat ? (uint32_t)(d.tc_mblk * d.tc_nkc * tc::kRec) : (uint32_t)(d.tc_S * d.tc_rps * tc::kRec);
+  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, abytes, d.tc_stat ? d.tc_mblk : d.tc_S, nf, d.pool_mode).total;
 }
 }  // namespace
 
@@ -846,17 +881,44 @@ std::string plan_tc(Plan& P) {
       }
       return false;
     };
-    bool ok = choose();
-    if (ok && d.pool_mode && d.tc_Nt != 64) {
-      d.pool_mode = 0;
+    // A stationary (preferred): each CTA keeps its M-part's n_mblk x nkc records resident
+    // for the whole launch, so A never streams from L2 (the bulk-copy A stream bounded the
+    // small-K alphas: 33 % more A bytes per output than B).  The largest part that fits
+    // (fewest CTAs re-reading each B tile), n_mblk <= MAXSLOT (the epilogue's registers).
+    auto choose_stat = [&]() {
+      const int nblocks = P.Mpp / 128, maxslot = NF == 8 ? 5 : NF == 16 ? 2 : 1;
+      if (d.L < 64) return false;
+      for (int np = 1; np <= nblocks; ++np) {
+        if (nblocks % np || nblocks / np > maxslot) continue;
+        for (int nbb = 2; nbb >= 1; --nbb) {
+          d.tc_stat = 1;
+          d.tc_mpart = np;
+          d.tc_mblk = nblocks / np;
+          d.tc_Nt = 64;
+          d.tc_NBB = nbb;
+          d.tc_S = 0;
+          if (tc_smem(d, NF) <= budget) return true;
+        }
+      }
+      d.tc_stat = 0;
+      return false;
+    };
+    bool ok = choose_stat();
+    if (!ok) {
+      d.tc_mpart = P.tc_n_mpart;
+      d.tc_mblk = P.tc_n_mblk;
       ok = choose();
+      if (ok && d.pool_mode && d.tc_Nt != 64) {
+        d.pool_mode = 0;
+        ok = choose();
+      }
     }
     if (!ok) return "tensor-core KD: no tile of alpha " + std::to_string(d.alpha) + " fits shared memory";
     // time chunk per work unit: the largest power of two <= 4096 that still gives
     // about 4 units per SM for a full micro-batch (partials are per chunk; measured on
     // c3, round 1: 4096 / 8192 / 16384-column chunks equal within noise)
     const int64_t sig = (P.prm.flags & JTFS_LATENCY) ? 1 : P.mb;  // signals per KD launch
-    const int64_t target = sig * P.tc_n_mpart * d.L / (4 * 148);
+    const int64_t target = sig * d.tc_mpart * d.L / (4 * 148);
     int ch = 4096;
     while (ch > d.tc_Nt && ch > target) ch /= 2;  // (JTFS_LATENCY: one signal per launch)
     d.chunk = std::min(ch, d.L);
@@ -973,8 +1035,9 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.nchunks = d.nchunks;
     p.chunk_sel = sel ? sel->d_sel + sel->off[i] : nullptr;
     p.nsel = nsel;
-    p.n_mpart = P.tc_n_mpart;
-    p.n_mblk = P.tc_n_mblk;
+    p.n_mpart = d.tc_mpart;
+    p.n_mblk = d.tc_mblk;
+    p.stat = d.tc_stat;
     p.L = d.L;
     p.nframes = P.n_frames;
     p.Mpp = P.Mpp;
@@ -993,8 +1056,10 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.part = part;
     p.part_off = d.part_off;
     p.part_stride = P.part_total;
-    const int units = nsig * nsel * P.tc_n_mpart;
-    const int grid = std::min(units, sms);
+    const int units = nsig * nsel * d.tc_mpart;
+    // stationary A: a multiple of n_mpart CTAs, so CTA b always gets M-part b % n_mpart
+    const int grid = d.tc_stat ? std::max(d.tc_mpart, std::min(units, sms) / d.tc_mpart * d.tc_mpart)
+                               : std::min(units, sms);
     const size_t sm = tc_smem(d, NF);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (P.prof) {
