@@ -82,6 +82,8 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   UP(P.d_twiddle64, P.twiddle64.data(), P.twiddle64.size() * 8);
   for (auto& g : P.u1_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
   for (auto& g : P.y2_groups) UP(g.d_rows, g.rows.data(), g.rows.size() * sizeof(FoldRow));
+  for (auto& g : P.y2_groups) UP(g.d_y16rows, g.y16rows.data(), g.y16rows.size() * sizeof(Y16Row));
+  UP(P.d_ybound, P.ybound.data(), P.ybound.size() * 4);
   {
     // backward tables (kernels.cu launch_backward)
     std::vector<FoldRow> u1flat;
@@ -117,7 +119,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
   UP(P.d_band_L1, P.band_phiT_L1.data(), P.band_phiT_L1.size() * sizeof(Band));
   {
     std::vector<DevAlpha> da;
-    for (const auto& d : P.kd) da.push_back(DevAlpha{d.nslices, 0, d.part_off});
+    for (const auto& d : P.kd) da.push_back(DevAlpha{d.nslices, d.K, d.part_off});
     UP(P.d_alphas, da.data(), da.size() * sizeof(DevAlpha));
   }
   {
@@ -152,6 +154,7 @@ jtfs_status upload_plan(jtfs::Plan& P) {
 struct WsPtrs {
   float2 *xhat, *tmp, *tmp2, *u1hat;
   float *u1, *yphi, *y2, *ys, *part;
+  unsigned int* u1max;
   uint16_t* y16;
   int32_t* sel;
   int* flag;
@@ -170,6 +173,7 @@ WsPtrs carve(const jtfs::Plan& P, void* ws, int64_t mb) {
   w.y2 = (float*)c; c += L.y2;
   w.y16 = (uint16_t*)c; c += L.y16;
   w.ys = (float*)c; c += L.ys;
+  w.u1max = (unsigned int*)c; c += L.u1max;
   w.part = (float*)c; c += L.part;
   w.sel = (int32_t*)c; c += L.sel;
   w.flag = (int*)c;
@@ -237,25 +241,45 @@ std::string run_microbatch(jtfs::Plan& P, const float* x, int nb, float* out, co
   using namespace jtfs;
   jtfs_layout_t lay;
   layout_of(P, &lay);
+  // the tensor-core KD takes Y2 as its packed fp16 operand, written by KC (scale from KB's
+  // per-row max |U1|); debug taps (keep_u1) and the SIMT validation KD take fp32 Y2
+  const bool y16_path = P.kd_impl == 1 && !keep_u1;
   if (!o.joint_only) {
     { StageScope s(P, 0, st); s.done(launch_pad_fft(P, x, nb, w.xhat, w.tmp, st)); }
     if (upto_stage == 0) return "";
-    { StageScope s(P, 1, st); s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st, w.tmp2)); }
+    {
+      StageScope s(P, 1, st);
+      if (y16_path) cudaMemsetAsync(w.u1max, 0, (size_t)nb * P.n1 * 4, st);
+      s.done(launch_first_order(P, w.xhat, nb, w.u1, w.u1hat, w.tmp, keep_u1, st, w.tmp2,
+                                y16_path ? w.u1max : nullptr));
+    }
     {
       StageScope s(P, 2, st);
       s.done(launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, out, lay.floats_per_signal, lay.off_s0, lay.off_s1,
                               P.d_u1_off, P.d_k1, P.d_band_L1, st));
     }
     if (upto_stage == 1) return "";
-    { StageScope s(P, 3, st); s.done(launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
+    {
+      StageScope s(P, 3, st);
+      if (y16_path)
+        s.done(launch_yscale(P, w.u1max, nb, w.ys, st) + launch_second_order16(P, w.u1hat, nb, w.y16, w.ys, w.tmp, st));
+      else
+        s.done(launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st));
+    }
     if (upto_stage == 2) return "";
   }
   {
     StageScope s(P, 4, st);
     int err = 0;
     float* part = o.part ? o.part : w.part;
-    s.done(P.kd_impl == 1 ? launch_kd_tc(P, w.y2, w.y16, w.ys, nb, part, st, &err, o.sel)
-                          : launch_kd(P, w.y2, nb, part, st, o.sel));
+    int n = 0;
+    if (P.kd_impl == 1) {
+      if (o.joint_only) n += launch_y16_from_y2(P, w.y2, nb, w.y16, w.ys, st);  // given fp32 Y2
+      n += launch_kd_tc(P, w.y16, w.ys + (int64_t)nb * P.kd.size(), nb, part, st, &err, o.sel);
+    } else {
+      n += launch_kd(P, w.y2, nb, part, st, o.sel);
+    }
+    s.done(n);
     if (err) return "tcgen05 KD: cuTensorMapEncodeTiled failed for the Y2 tensor map";
   }
   if (o.skip_ke) return "";

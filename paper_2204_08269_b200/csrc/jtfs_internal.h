@@ -38,11 +38,22 @@ struct FoldRow {
   int32_t pad;
 };
 
+// Where KC's fp16 store puts one Y2 row (tensor-core KD layout, kernels_tc.cu): the row's
+// hi / lo / hi segments of alpha's packed [3K][2L] block (KC writes them directly).
+struct Y16Row {
+  int64_t off;   // halves: row lambda of the hi segment inside one signal's Y16 buffer
+  int64_t seg;   // halves between the segments (K rows x 2L)
+  int32_t aslot; // active-alpha index (per-(signal, alpha) scale)
+  int32_t pad;
+};
+
 // A launch group: all rows (per signal) that share one FFT length.
 struct FoldGroup {
   int log2L;
   std::vector<FoldRow> rows;
   FoldRow* d_rows = nullptr;
+  std::vector<Y16Row> y16rows;  // y2 groups: the fp16 destinations of the same rows
+  Y16Row* d_y16rows = nullptr;
 };
 
 // One active second-order temporal wavelet psi_alpha and its KD problem.
@@ -73,7 +84,7 @@ struct AlphaKD {
   int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16
   int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
   int64_t y16_off = 0;  // fp16 offset of Y16_alpha [K16][2L] in one signal's Y16 buffer (KY output)
-  int64_t ys_off = 0;   // float offset of the per-tile inverse Y scales (L / 32 slots) in one signal's ys
+  int64_t ys_off = 0;   // slot of the per-(signal, alpha) Y scale in one signal's ys (= active-alpha index)
   int64_t wtab_off = 0; // float offset of the phi_T pooling table in wtab
   int pool_mode = 0;    // 0: taps [L][NF]; 1: cubic-moment coefficients [L/32][4][NF] (kernels_tc.cu)
   int nslices = 0;      // KD partial slices per signal and alpha (time chunks x epilogue sets)
@@ -128,7 +139,9 @@ struct Plan {
   std::vector<uint16_t> A16;             // A''_alpha re/im, row-scaled fp16 hi/lo, pre-tiled/swizzled (tcgen05 KD)
   std::vector<float> Ainv;               // per alpha and row: 1 / (power-of-two row scale of A16)
   std::vector<float> wtab;               // per alpha: phi_T pooling table (taps or moment coefficients)
-  int64_t y16_total = 0, ys_total = 0;   // per signal: fp16 elements of Y16, per-tile scale slots
+  int64_t y16_total = 0, ys_total = 0;   // per signal: fp16 elements of Y16, scale slots (one per alpha)
+  std::vector<float> ybound;             // [n_alpha][n1]: sqrt(sum psi_hat_alpha^2) of the band row lambda
+                                         // uses (Cauchy-Schwarz: |Y2| <= ybound * max|U1_lambda|)
   std::vector<float> g;                  // time pooling taps per alpha
   std::vector<float> W;                  // lambda pooling matrices per filter
   std::vector<int32_t> Wrange;           // per filter and output row q: first, last + 1 row of |W| >= 1e-9 max
@@ -145,6 +158,7 @@ struct Plan {
   uint16_t* d_A16 = nullptr;
   float* d_Ainv = nullptr;
   float* d_wtab = nullptr;
+  float* d_ybound = nullptr;
   float* d_g = nullptr;
   float* d_W = nullptr;
   int32_t* d_Wrange = nullptr;
@@ -184,7 +198,7 @@ int ilog2_exact(int64_t v);  // -1 if not a power of two
 
 // workspace layout (per micro-batch of mb signals), in bytes
 struct WsLayout {
-  size_t xhat, tmp, tmp2, u1, u1hat, yphi, y2, y16, ys, part, sel, flag, total;
+  size_t xhat, tmp, tmp2, u1, u1hat, yphi, y2, y16, ys, u1max, part, sel, flag, total;
 };
 WsLayout ws_layout(const Plan& p, int64_t mb);
 

@@ -12,6 +12,8 @@
 // Every spectral decimation is done by folding (aliasing-sum) the band-limited
 // product spectrum to the decimated length before a shorter inverse FFT, which is
 // the exact identity IDFT_L(X)[n d] = (1/d) IDFT_{L/d}(fold X)[n].
+#include <cuda_fp16.h>
+
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -85,6 +87,8 @@ struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
   float* dst_real;    // modulus output (U1) or nullptr
   float* dst_planar;  // planar complex output (Y2: re row at dst_off, im row at dst_off + L) or nullptr
   int64_t dst_stride;
+  unsigned int* u1max = nullptr;  // first order: per (signal, lambda = rows[r].pad) max |U1| (float bits)
+  int n1 = 0;
   __device__ float2 load(int rho, int i) const {
     const int b = rho / nrows, r = rho % nrows;
     return fold_value(src + (int64_t)b * src_stride, rows[r], bandvals, i, L);
@@ -93,12 +97,50 @@ struct ProbFold {  // rows rho = b * nrows + r: band-multiply + fold gather
     const int b = rho / nrows, r = rho % nrows;
     const FoldRow& d = rows[r];
     if (dst_real) {
-      dst_real[(int64_t)b * dst_stride + d.dst_off + o] = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * d.scale;
+      const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * d.scale;
+      dst_real[(int64_t)b * dst_stride + d.dst_off + o] = u;
+      if (u1max) atomicMax(u1max + (int64_t)b * n1 + d.pad, __float_as_uint(u));
     } else {
       float* row = dst_planar + (int64_t)b * dst_stride + d.dst_off;
       row[o] = v.x * d.scale;
       row[L + o] = v.y * d.scale;
     }
+  }
+};
+
+// KC for the tensor-core KD: the Y2 row goes straight into KD's packed fp16 B layout,
+// x s = hi + lo (hi = rn16(x s), lo = rn16(x s - hi)) with the per-(signal, alpha) power-of-
+// two scale s of k_yscale, written as rows [hi; lo; hi] (segments y.seg halves apart) with
+// (re, im) interleaved per time column (kernels_tc.cu)
+struct ProbFold16 {
+  using CT = float2;
+  const float2* src;
+  int64_t src_stride;
+  const FoldRow* rows;
+  int nrows;
+  const float* bandvals;
+  int L;
+  const Y16Row* y16rows;
+  __half* y16;
+  int64_t y16_stride;
+  const float* ysc;  // [signal][n_alpha] scales
+  int nalpha;
+  __device__ float2 load(int rho, int i) const {
+    const int b = rho / nrows, r = rho % nrows;
+    return fold_value(src + (int64_t)b * src_stride, rows[r], bandvals, i, L);
+  }
+  __device__ void store(int rho, int o, float2 v) const {
+    const int b = rho / nrows, r = rho % nrows;
+    const Y16Row y = y16rows[r];
+    const float s = rows[r].scale * __ldg(ysc + (int64_t)b * nalpha + y.aslot);
+    const float xr = v.x * s, xi = v.y * s;
+    const __half2 hi = __floats2half2_rn(xr, xi);
+    const float2 f = __half22float2(hi);
+    const __half2 lo = __floats2half2_rn(xr - f.x, xi - f.y);
+    __half* dst = y16 + (int64_t)b * y16_stride + y.off + 2 * o;
+    *reinterpret_cast<__half2*>(dst) = hi;
+    *reinterpret_cast<__half2*>(dst + y.seg) = lo;
+    *reinterpret_cast<__half2*>(dst + 2 * y.seg) = hi;
   }
 };
 
@@ -195,6 +237,16 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
       if (u1dbg && rho0 + g < nrows) {
         const int b = (rho0 + g) / prob.nrows, r = (rho0 + g) % prob.nrows;
         u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = u;
+      }
+      if (prob.u1max) {  // per-row max |U1|: a warp's 32 elements share one row when L >= 32
+        const int b = rho / prob.nrows, r = rho % prob.nrows;
+        unsigned int* slot = prob.u1max + (int64_t)b * prob.n1 + prob.rows[r].pad;
+        if constexpr (L >= 32) {
+          const unsigned int m = __reduce_max_sync(0xffffffffu, rho0 + g < nrows ? __float_as_uint(u) : 0u);
+          if ((threadIdx.x & 31) == 0 && rho0 + g < nrows) atomicMax(slot, m);
+        } else if (rho0 + g < nrows) {
+          atomicMax(slot, __float_as_uint(u));
+        }
       }
     }
     __syncthreads();
@@ -390,9 +442,18 @@ __global__ void __launch_bounds__(NT) k_fft4_mid2(ProbFold prob, const float2* _
     const int rho = b * nr + 2 * j + h;
     const float2* in = tmp_in + (int64_t)rho * L;
     const float sc = prob.rows[2 * j + h].scale;
+    float umax = 0.f;  // this thread's max |U1| of row 2j + h (KB's per-row max for KC's fp16 scale)
     auto ld1 = [&](int g, int e) -> float2 { return in[(ka0 + g) * Lb + e]; };
-    auto st1 = [&](int g, int kb, float2 v) { s2f[2 * (g * LS + padx(kb))] = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc; };
+    auto st1 = [&](int g, int kb, float2 v) {
+      const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc;
+      umax = fmaxf(umax, u);
+      s2f[2 * (g * LS + padx(kb))] = u;
+    };
     fft_fused<LOG2B, G, NT, +1, LS, true, true, true, float2, decltype(ld1), decltype(st1), false>(s1, Ws, ld1, st1);
+    if (prob.u1max) {
+      const unsigned int m = __reduce_max_sync(0xffffffffu, __float_as_uint(umax));
+      if ((threadIdx.x & 31) == 0) atomicMax(prob.u1max + (int64_t)b * prob.n1 + prob.rows[2 * j + h].pad, m);
+    }
     __syncthreads();
   }
   __syncthreads();
@@ -1138,7 +1199,7 @@ int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2
 }
 
 int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,
-                       bool keep_u1, cudaStream_t st, float2* tmp2) {
+                       bool keep_u1, cudaStream_t st, float2* tmp2, unsigned int* u1max) {
   const float2* W = (const float2*)P.d_twiddle;
   const int ltw = ilog2_exact(P.N_tw);
   int n = 0;
@@ -1146,7 +1207,7 @@ int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, f
   for (const auto& g : P.u1_groups) {
     n += g.log2L <= 12 ? 1 : (fuse ? 3 : 4);
     const int nr = (int)g.rows.size();
-    ProbFold pf{xhat, P.N_pad, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, u1, nullptr, P.u1_total};
+    ProbFold pf{xhat, P.N_pad, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, u1, nullptr, P.u1_total, u1max, P.n1};
     ProbRealFwd prf{u1, u1hat, P.u1_total, g.d_rows, nr};
     dispatch_log2(g.log2L, [&](auto c) {
       constexpr int LG = decltype(c)::value;
@@ -1192,6 +1253,60 @@ int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int
   const int items = nsig * (P.n1 + 1);
   k_phi_first<<<(items + 3) / 4, 128, 0, st>>>(p);
   return 1;
+}
+
+// ---------------------------------------------------------------------------------
+// per-(signal, alpha) power-of-two scale of KD's fp16 operand (read by KC's fp16 store and
+// KD): s = 2^(13 - E), bound = max_{lambda < K} ybound[alpha][lambda] max|U1_lambda| in
+// [2^E, 2^(E+1)) -- a true upper bound of |Y2_alpha| (plan.cpp), so |Y2| s < 2^14 fits
+// fp16, and every value above 2^-27 of the bound keeps the split's 2^-22 relative error.
+// One warp per (signal, alpha); fixed-order max (exact, order-independent anyway).
+// ---------------------------------------------------------------------------------
+__global__ void k_yscale(const unsigned int* __restrict__ u1max, const float* __restrict__ ybound,
+                         const DevAlpha* __restrict__ alphas, int n1, int nalpha, float* ysc, float* ysi) {
+  const int b = blockIdx.x, a = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a >= nalpha) return;
+  const int K = alphas[a].pad;
+  float m = 0.f;
+  for (int l = lane; l < K; l += 32)
+    m = fmaxf(m, __uint_as_float(__ldg(u1max + (int64_t)b * n1 + l)) * __ldg(ybound + (int64_t)a * n1 + l));
+  const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+  if (lane == 0) {
+    int E = (int)(mb >> 23) - 127;
+    E = max(E, -100);
+    ysc[(int64_t)b * nalpha + a] = __uint_as_float((uint32_t)(13 - E + 127) << 23);
+    ysi[(int64_t)b * nalpha + a] = __uint_as_float((uint32_t)(E - 13 + 127) << 23);
+  }
+}
+
+int launch_yscale(const Plan& P, const unsigned int* u1max, int nsig, float* ys, cudaStream_t st) {
+  const int na = (int)P.kd.size();
+  k_yscale<<<nsig, 32 * na, 0, st>>>(u1max, P.d_ybound, (const DevAlpha*)P.d_alphas, P.n1, na, ys,
+                                     ys + (int64_t)nsig * na);
+  return 1;
+}
+
+// KC in the tensor-core KD's fp16 layout (ProbFold16): no fp32 Y2, no separate conversion
+int launch_second_order16(const Plan& P, const float2* u1hat, int nsig, uint16_t* y16, const float* ysc,
+                          float2* tmp, cudaStream_t st) {
+  const float2* W = (const float2*)P.d_twiddle;
+  const int ltw = ilog2_exact(P.N_tw);
+  int n = 0;
+  for (const auto& g : P.y2_groups) {
+    n += g.log2L <= 12 ? 1 : 2;
+    const int nr = (int)g.rows.size();
+    ProbFold16 pf{u1hat, P.u1_total, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, g.d_y16rows,
+                  reinterpret_cast<__half*>(y16), P.y16_total, ysc, (int)P.kd.size()};
+    dispatch_log2(g.log2L, [&](auto c) {
+      constexpr int LG = decltype(c)::value;
+      if constexpr (LG <= 12) {
+        launch_rows<LG, +1>(pf, nsig * nr, W, ltw, st);
+      } else {
+        launch_fft4<LG, +1>(pf, pf, nsig * nr, tmp, W, ltw, st);
+      }
+    });
+  }
+  return n;
 }
 
 int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st) {

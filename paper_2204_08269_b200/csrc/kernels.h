@@ -36,7 +36,7 @@ struct DevFilter {
   int64_t wr_off;  // [lam_out] int2 {first, last + 1} row of each output's phi_F band
 };
 struct DevAlpha {
-  int32_t nchunks, pad;
+  int32_t nchunks, pad;  // pad: K (admissible lambda rows)
   int64_t part_off;
 };
 
@@ -63,7 +63,14 @@ int launch_pad_fft(const Plan& P, const float* x, int nsig, float2* xhat, float2
 // tmp2 (optional): a second four-step intermediate; with it (and keep_u1 false) the
 // lengths > 4096 run the fused inverse-DFT / modulus / forward-DFT middle stage
 int launch_first_order(const Plan& P, const float2* xhat, int nsig, float* u1, float2* u1hat, float2* tmp,
-                        bool keep_u1, cudaStream_t st, float2* tmp2 = nullptr);
+                        bool keep_u1, cudaStream_t st, float2* tmp2 = nullptr, unsigned int* u1max = nullptr);
+// per-(signal, alpha) fp16 scales ys[nsig][n_alpha] and inverses ys + nsig n_alpha (KC -> KD)
+int launch_yscale(const Plan& P, const unsigned int* u1max, int nsig, float* ys, cudaStream_t st);
+// KC writing KD's packed fp16 operand directly (tensor-core KD forward)
+int launch_second_order16(const Plan& P, const float2* u1hat, int nsig, uint16_t* y16, const float* ysc,
+                          float2* tmp, cudaStream_t st);
+// fp32 Y2 -> KD's fp16 operand with exact per-(signal, alpha) scales (jtfs_debug_joint)
+int launch_y16_from_y2(Plan& P, const float* y2, int nsig, uint16_t* y16, float* ys, cudaStream_t st);
 int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int nsig, float* yphi, float* out,
                       int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
                       const Band* d_band_L1, cudaStream_t st);
@@ -74,7 +81,8 @@ int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
 int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64_t fps, int64_t off_s2,
                      cudaStream_t st);
 cudaError_t ke_set_smem(const Plan& P);
-int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st, int* err,
+// KD on the tensor cores from KD's fp16 operand y16 and the inverse scales ysi [nsig][n_alpha]
+int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float* part, cudaStream_t st, int* err,
                  const UnitSel* sel = nullptr);
 cudaError_t tc_setup_device(Plan& P);
 

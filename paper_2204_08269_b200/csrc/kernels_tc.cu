@@ -296,48 +296,49 @@ __device__ __forceinline__ void spin_mags(const uint32_t (&v1)[16], const uint32
   }
 }
 // ---------------------------------------------------------------------------------
-// KY: one CTA per (signal, tile of Nt columns): max |Re|, |Im| of Y2_alpha over the K x Nt
-// tile -> s_Y (power of two, max * s_Y in [2^13, 2^14)), hi = rn16(y s_Y), lo = rn16(y s_Y -
-// hi), written as the packed rows [Y_hi (K); Y_lo (K); Y_hi (K)] of [K16][2L] fp16 with
-// (re, im) interleaved per time column (rows >= 3K are never written: the KD tensor map
-// declares 3K rows and TMA zero-fills the rest of each box); 1 / s_Y into ys[tile].
+// fp32 Y2 -> KD's fp16 operand (validation entry jtfs_debug_joint only; the forward's KC
+// writes the operand directly, kernels.cu ProbFold16).  k_y2max: exact max |Re|, |Im| of
+// Y2_alpha per (signal, alpha) -> the same power-of-two scale rule as k_yscale; k_ky: the
+// packed rows [Y_hi (K); Y_lo (K); Y_hi (K)] of [K16][2L] fp16, (re, im) interleaved.
 // ---------------------------------------------------------------------------------
 struct KYParams {
   const float* y2;     // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
   int64_t y2_stride;
   __half* y16;         // Y16 of signal 0 at alpha's offset; signal stride y16_stride halves
   int64_t y16_stride;
-  float* ys;           // per-tile inverse scales of signal 0 at alpha's offset; stride ys_stride
+  float* ysc;          // scale of (signal 0, alpha); signal stride ys_stride
+  float* ysi;          // inverse scale
   int64_t ys_stride;
-  int K, L, Nt, ntiles;
+  int K, L;
 };
 
-__global__ void __launch_bounds__(256) k_ky(KYParams p) {
+__global__ void __launch_bounds__(256) k_y2max(KYParams p) {
   __shared__ uint32_t red[8];
-  const int b = blockIdx.x / p.ntiles, tile = blockIdx.x % p.ntiles;
-  const int t0 = tile * p.Nt;
-  const float* Y = p.y2 + (int64_t)b * p.y2_stride + t0;
-  const int nq = p.Nt / 4;
+  const int b = blockIdx.x;
+  const float* Y = p.y2 + (int64_t)b * p.y2_stride;
   float mx = 0.f;
-  for (int i = threadIdx.x; i < 2 * p.K * nq; i += 256) {
-    const int k = i / nq, c = 4 * (i % nq);
-    const float4 v = __ldg(reinterpret_cast<const float4*>(Y + (int64_t)k * p.L + c));
-    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-  }
+  for (int64_t i = threadIdx.x; i < (int64_t)2 * p.K * p.L; i += 256) mx = fmaxf(mx, fabsf(__ldg(Y + i)));
   const uint32_t w = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
   __syncthreads();
-  uint32_t mbits = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) mbits = max(mbits, red[i]);
-  int E = (int)(mbits >> 23) - 127;
-  E = max(E, -100);
-  const float s = __uint_as_float((uint32_t)(13 - E + 127) << 23);
-  if (threadIdx.x == 0) p.ys[(int64_t)b * p.ys_stride + tile] = __uint_as_float((uint32_t)(E - 13 + 127) << 23);
-  __half* row0 = p.y16 + (int64_t)b * p.y16_stride + 2 * t0;
+  if (threadIdx.x == 0) {
+    uint32_t mbits = 0;
+    for (int i = 0; i < 8; ++i) mbits = max(mbits, red[i]);
+    int E = (int)(mbits >> 23) - 127;
+    E = max(E, -100);
+    p.ysc[(int64_t)b * p.ys_stride] = __uint_as_float((uint32_t)(13 - E + 127) << 23);
+    p.ysi[(int64_t)b * p.ys_stride] = __uint_as_float((uint32_t)(E - 13 + 127) << 23);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ky(KYParams p) {
+  const int b = blockIdx.y;
+  const float* Y = p.y2 + (int64_t)b * p.y2_stride;
+  const float s = __ldg(p.ysc + (int64_t)b * p.ys_stride);
+  __half* row0 = p.y16 + (int64_t)b * p.y16_stride;
   const int64_t rs = 2 * (int64_t)p.L;  // row stride (halves)
-  for (int i = threadIdx.x; i < p.K * p.Nt; i += 256) {
-    const int l = i / p.Nt, c = i % p.Nt;
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < (int64_t)p.K * p.L; i += (int64_t)gridDim.x * 256) {
+    const int l = (int)(i / p.L), c = (int)(i % p.L);
     const float yr = __ldg(Y + (int64_t)(2 * l) * p.L + c) * s;
     const float yi = __ldg(Y + (int64_t)(2 * l + 1) * p.L + c) * s;
     const __half2 h = __floats2half2_rn(yr, yi);
@@ -370,7 +371,7 @@ struct TcParams {
   const float* ainv;   // 1 / s_p per pair row [Mpp]
   const float* wtab;   // phi_T pooling table: taps [L][NF] (pool_mode 0) or cubic moments [L/32][4][NF] (1)
   int pool_mode;
-  const float* ys;     // 1 / s_Y per (signal, tile): ys[b * ys_stride + tile]
+  const float* ys;     // 1 / s_Y of (signal, this alpha): ys[b * ys_stride]
   int64_t ys_stride;
   float* part;
   int64_t part_off, part_stride;
@@ -686,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int wi = gt & 1;
       mbar_wait_t<PROF>(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
-      const float inv = __ldg(p.ys + (int64_t)b * p.ys_stride + chunk * p.tpu + tile);
+      const float inv = __ldg(p.ys + (int64_t)b * p.ys_stride);
       const float* wt = Wt + wi * wfl + cbeg * NF;
 #pragma unroll 1
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
@@ -881,16 +882,16 @@ std::string plan_tc(Plan& P) {
       }
       return false;
     };
-    // A stationary (preferred): each CTA keeps its M-part's n_mblk x nkc records resident
-    // for the whole launch, so A never streams from L2 (the bulk-copy A stream bounded the
-    // small-K alphas: 33 % more A bytes per output than B).  The largest part that fits
-    // (fewest CTAs re-reading each B tile), n_mblk <= MAXSLOT (the epilogue's registers).
+    // A stationary: each CTA keeps its M-part's n_mblk x nkc records resident for the whole
+    // launch, so A never streams from L2.  Used only where it fits with two B buffers and at
+    // most two M-parts (measured on c3: alpha 0 22.3 -> 20.9 ms per step; alphas 2-4, which
+    // need one B buffer or 5-10 parts re-reading every B tile, got 15-35 % slower).
     auto choose_stat = [&]() {
       const int nblocks = P.Mpp / 128, maxslot = NF == 8 ? 5 : NF == 16 ? 2 : 1;
       if (d.L < 64) return false;
-      for (int np = 1; np <= nblocks; ++np) {
+      for (int np = 1; np <= std::min(2, nblocks); ++np) {
         if (nblocks % np || nblocks / np > maxslot) continue;
-        for (int nbb = 2; nbb >= 1; --nbb) {
+        for (int nbb = 2; nbb >= 2; --nbb) {
           d.tc_stat = 1;
           d.tc_mpart = np;
           d.tc_mblk = nblocks / np;
@@ -967,7 +968,27 @@ cudaError_t tc_setup_device(Plan& P) {
   return e;
 }
 
-int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, float* part, cudaStream_t st,
+int launch_y16_from_y2(Plan& P, const float* y2, int nsig, uint16_t* y16, float* ys, cudaStream_t st) {
+  const int na = (int)P.kd.size();
+  for (int i = 0; i < na; ++i) {
+    const auto& d = P.kd[i];
+    tc::KYParams q{};
+    q.y2 = y2 + 2 * d.y2_off;
+    q.y2_stride = 2 * P.y2_total;
+    q.y16 = reinterpret_cast<__half*>(y16) + d.y16_off;
+    q.y16_stride = P.y16_total;
+    q.ysc = ys + i;
+    q.ysi = ys + (int64_t)nsig * na + i;
+    q.ys_stride = na;
+    q.K = d.K;
+    q.L = d.L;
+    tc::k_y2max<<<nsig, 256, 0, st>>>(q);
+    tc::k_ky<<<dim3(std::max(1, std::min(64, d.K * d.L / 4096)), nsig), 256, 0, st>>>(q);
+  }
+  return 2 * na;
+}
+
+int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float* part, cudaStream_t st,
                  int* err, const UnitSel* sel) {
   const int NF = nf_of(P.n_frames);
   int sms = 148;
@@ -994,30 +1015,14 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     const auto& d = P.kd[i];
     const int nsel = sel ? sel->cnt[i] : d.nchunks;
     if (nsel == 0) continue;
-    st = (side && (int)i >= P.kd_side_from) ? side : main_st;  // KY + KD of this alpha
-    // ---- KY: fp16 split of the Y'' tiles ----
-    {
-      tc::KYParams q{};
-      q.y2 = y2 + 2 * d.y2_off;
-      q.y2_stride = 2 * P.y2_total;
-      q.y16 = reinterpret_cast<__half*>(y16) + d.y16_off;
-      q.y16_stride = P.y16_total;
-      q.ys = ys + d.ys_off;
-      q.ys_stride = P.ys_total;
-      q.K = d.K;
-      q.L = d.L;
-      q.Nt = d.tc_Nt;
-      q.ntiles = d.L / d.tc_Nt;
-      tc::k_ky<<<nsig * q.ntiles, 256, 0, st>>>(q);
-      ++launches;
-    }
+    st = (side && (int)i >= P.kd_side_from) ? side : main_st;
     CUtensorMap tmB;
     // K' = 3K packed rows (the buffer is allocated with K16 rows): the box rows beyond K'
     // are out of bounds and arrive zero-filled (the MMA's K padding)
     cuuint64_t dims[3] = {(cuuint64_t)(2 * d.L), (cuuint64_t)d.tc_K2, (cuuint64_t)nsig};
     cuuint64_t strides[2] = {(cuuint64_t)d.L * 4, (cuuint64_t)P.y16_total * 2};
     cuuint32_t box[3] = {64, (cuuint32_t)d.tc_BRk, 1};
-    if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, y16 + d.y16_off, 3, dims, strides, box,
+    if (!encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, const_cast<uint16_t*>(y16) + d.y16_off, 3, dims, strides, box,
                 CU_TENSOR_MAP_SWIZZLE_128B)) {
       *err = 1;
       break;  // the join below still orders the side stream before the caller's
@@ -1046,7 +1051,7 @@ int launch_kd_tc(Plan& P, const float* y2, uint16_t* y16, float* ys, int nsig, f
     p.ainv = P.d_Ainv + d.tc_ainv_off;
     p.wtab = P.d_wtab + d.wtab_off;
     p.pool_mode = d.pool_mode;
-    p.ys = ys + d.ys_off;
+    p.ys = ysi + d.ys_off;
     p.ys_stride = P.ys_total;
     static unsigned long long* prof = nullptr;
     const bool do_prof = (P.prm.flags & JTFS_KD_PROF) != 0;  // measurement-only plan flag

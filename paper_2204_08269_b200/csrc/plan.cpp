@@ -266,6 +266,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
     r.band_off = P.band_psi1[l].off;
     r.dst_off = P.u1_off[l];
     r.scale = (float)(1.0 / P.N_pad);
+    r.pad = l;  // lambda (KB's per-row max |U1|)
     P.u1_groups.back().rows.push_back(r);
   }
 
@@ -319,6 +320,38 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       r.scale = (float)(1.0 / P.L1[l]);
       G->rows.push_back(r);
     }
+  }
+
+  // ---- fp16 destinations of the Y2 rows (KC writes the KD's packed B rows directly) and
+  // the Cauchy-Schwarz bound sqrt(sum_m psi_hat_alpha[m]^2) of each (alpha, lambda) band:
+  // |Y2_alpha[lambda](n)| = |sum_t psi(t) U1_lambda(n - t)| <= ||psi||_1 max|U1_lambda|
+  // <= sqrt(L) ||psi||_2 max|U1_lambda| = sqrt(sum_m |psi_hat[m]|^2) max|U1_lambda|
+  // (Parseval; psi = IDFT_L of the band values KC multiplies) ----
+  {
+    std::vector<int64_t> y16_off_of(P.kd.size());
+    int64_t acc = 0;
+    for (size_t a = 0; a < P.kd.size(); ++a) {
+      y16_off_of[a] = acc;
+      const int K48 = (3 * P.kd[a].K + 15) / 16 * 16;
+      acc += (int64_t)K48 * 2 * P.kd[a].L;
+    }
+    for (auto& G : P.y2_groups) G.y16rows.clear();
+    for (size_t a = 0; a < P.kd.size(); ++a) {
+      const auto& d = P.kd[a];
+      FoldGroup* G = nullptr;
+      for (auto& g : P.y2_groups)
+        if (g.log2L == ilog2_exact(d.L)) G = &g;
+      for (int l = 0; l < d.K; ++l)
+        G->y16rows.push_back(Y16Row{y16_off_of[a] + (int64_t)l * 2 * d.L, (int64_t)d.K * 2 * d.L, (int32_t)a, 0});
+    }
+    P.ybound.assign(P.kd.size() * (size_t)P.n1, 0.f);
+    for (size_t a = 0; a < P.kd.size(); ++a)
+      for (int l = 0; l < P.kd[a].K; ++l) {
+        const Band& bd = band2[std::make_pair(P.kd[a].alpha, P.k1[l])];
+        double e = 0;
+        for (int t = 0; t < bd.len; ++t) e += (double)bv[bd.off + t] * (double)bv[bd.off + t];
+        P.ybound[a * P.n1 + l] = (float)(std::sqrt(e) * (1.0 + 1e-6));
+      }
   }
 
   // ---- frequential filters and the joint-stage row set (R9, R10, R11) ----
@@ -562,7 +595,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
       d.y16_off = P.y16_total;
       P.y16_total += (int64_t)K48 * 2 * d.L;  // [Y_hi; Y_lo; Y_hi][2L] rows, (re, im) interleaved (KY)
       d.ys_off = P.ys_total;
-      P.ys_total += std::max(1, d.L / 32);  // one slot per tile; tiles have >= 32 columns (plan_tc checks)
+      P.ys_total += 1;  // one scale per (signal, alpha): KC's fp16 store and KD share it
       const float* g = P.g.data() + d.g_off;
       auto tap = [&](int m, int64_t t) -> double { return pool_tap(P, d, m, t); };
       // phi_T pooling in moment form where it is exact to fp32 (kernels_tc.cu,
@@ -760,7 +793,8 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
   w.yphi = al((size_t)mb * p.n1 * p.NPT * 4);
   w.y2 = al((size_t)mb * p.y2_total * 8);
   w.y16 = al((size_t)mb * p.y16_total * 2);
-  w.ys = al((size_t)mb * p.ys_total * 4);
+  w.ys = al((size_t)mb * p.ys_total * 8);        // [mb][n_alpha] scales, then [mb][n_alpha] inverses
+  w.u1max = al((size_t)mb * p.n1 * 4);         // per (signal, lambda) max |U1| (KB)
   w.part = al((size_t)mb * p.part_total * 4);
   {
     size_t nsel = 0;  // jtfs_forward_units' chunk lists (at most one id per chunk)
@@ -768,7 +802,8 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
     w.sel = al(nsel * 4);
   }
   w.flag = 256;
-  w.total = w.xhat + w.tmp + w.tmp2 + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.part + w.sel + w.flag;
+  w.total = w.xhat + w.tmp + w.tmp2 + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.u1max + w.part + w.sel +
+            w.flag;
   return w;
 }
 
