@@ -283,16 +283,18 @@ constexpr int kFmaSqrtCols = JTFS_KD_FMA_SQRT_COLS;
 // Packed per column: X = (Re Z_-, Re Z_+) = (-1, 1) P2 + P1, Y = (Im Z_-, Im Z_+) = (1, -1) P4
 // + P3, Q = X X + Y Y = (|Z_-|^2, |Z_+|^2): four FP32x2 instructions, then two MUFU.SQRT.
 // mz[j] = (|Z_-|, |Z_+|) of column j.
-__device__ __forceinline__ void spin_mags(const uint32_t (&v1)[16], const uint32_t (&v2)[16], float2 (&mz)[8]) {
+template <int NC>
+__device__ __forceinline__ void spin_mags(const uint32_t (&v1)[2 * NC], const uint32_t (&v2)[2 * NC],
+                                          float2 (&mz)[NC]) {
   const float2 cm = make_float2(-1.f, 1.f), cp = make_float2(1.f, -1.f);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < NC; ++j) {
     const float p1 = __uint_as_float(v1[2 * j]), p3 = __uint_as_float(v1[2 * j + 1]);
     const float p4 = __uint_as_float(v2[2 * j]), p2 = __uint_as_float(v2[2 * j + 1]);
     const float2 X = fma2(cm, make_float2(p2, p2), make_float2(p1, p1));
     const float2 Y = fma2(cp, make_float2(p4, p4), make_float2(p3, p3));
     const float2 Q = fma2(X, X, mul2(Y, Y));
-    mz[j] = (j >= 8 - kFmaSqrtCols) ? sqrt2_fma(Q) : make_float2(sqrt_fast(Q.x), sqrt_fast(Q.y));
+    mz[j] = ((j & 7) >= 8 - kFmaSqrtCols) ? sqrt2_fma(Q) : make_float2(sqrt_fast(Q.x), sqrt_fast(Q.y));
   }
 }
 // ---------------------------------------------------------------------------------
@@ -424,7 +426,7 @@ __device__ __forceinline__ void epi_group_taps(uint32_t tb1, uint32_t tb2, const
   reg_fence16(v1);
   reg_fence16(v2);
   float2 mz[8];
-  spin_mags(v1, v2, mz);
+  spin_mags<8>(v1, v2, mz);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const float4* w4 = reinterpret_cast<const float4*>(wt + (8 * G + j) * NF);
@@ -439,20 +441,21 @@ __device__ __forceinline__ void epi_group_taps(uint32_t tb1, uint32_t tb2, const
   }
 }
 // moments of both spins, packed: S[k] = (sum_j |Z_-,j| u_j^k, sum_j |Z_+,j| u_j^k), u_j
-// compile-time (FFMA2 with an immediate operand)
+// compile-time (FFMA2 with an immediate operand).  One group = 16 time columns: two x32
+// TMEM loads (acc1, acc2) behind one wait, so 16 independent columns are in flight.
 template <int G>
 __device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2 (&S)[4]) {
-  uint32_t v1[16], v2[16];
-  tmem_ld16(tb1 + 16 * G, v1);
-  tmem_ld16(tb2 + 16 * G, v2);
+  uint32_t v1[32], v2[32];
+  tmem_ld32(tb1 + 32 * G, v1);
+  tmem_ld32(tb2 + 32 * G, v2);
   tmem_wait_ld();
-  reg_fence16(v1);
-  reg_fence16(v2);
-  float2 mz[8];
-  spin_mags(v1, v2, mz);
+  reg_fence(v1);
+  reg_fence(v2);
+  float2 mz[16];
+  spin_mags<16>(v1, v2, mz);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float u = ((float)(8 * G + j) - 15.5f) * 0.0625f;  // compile-time
+  for (int j = 0; j < 16; ++j) {
+    const float u = ((float)(16 * G + j) - 15.5f) * 0.0625f;  // compile-time
     S[0] = add2(S[0], mz[j]);
     S[1] = fma2(mz[j], make_float2(u, u), S[1]);
     S[2] = fma2(mz[j], make_float2(u * u, u * u), S[2]);
@@ -709,8 +712,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (half == 32) {
             epi_group_mom<0>(tb1, tb2, S);
             epi_group_mom<1>(tb1, tb2, S);
-            epi_group_mom<2>(tb1, tb2, S);
-            epi_group_mom<3>(tb1, tb2, S);
           }
           tc_fence_before();
           __syncwarp();
