@@ -22,10 +22,10 @@ FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "jtfs.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
@@ -33,8 +33,8 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB) -> str:
     """Compile libjtfs.so (or, for A/B measurements of a compile-time variant, `lib` with
     extra -D `defines`; select it at run time with JTFS_LIB=<path>)."""
-    if not force and not defines and lib == LIB and not _stale():
-        return LIB
+    if not force and not _stale(lib):
+        return lib
     objs, procs = [], []
     tag = "" if lib == LIB else "." + os.path.basename(lib)
     for src in SOURCES:  # the translation units compile concurrently

@@ -474,11 +474,44 @@ static jtfs_status forward_impl(jtfs_plan_t plan, const float* x, int64_t B, flo
   }
   jtfs_layout_t lay;
   layout_of(P, &lay);
+#ifdef JTFS_WS_GUARDS
+  // validation build: the trailing guard band of every workspace region is filled with a
+  // pattern before and checked after the forward (an overflow of any region is an error)
+  std::vector<int64_t> gstart;
+  {
+    const jtfs::WsLayout L = jtfs::ws_layout(P, mb);
+    const size_t sz[13] = {L.xhat, L.tmp, L.tmp2, L.u1, L.u1hat, L.yphi, L.y2, L.y16, L.ys, L.u1max, L.part, L.sel,
+                           L.flag};
+    int64_t o = 0;
+    for (size_t r : sz) {
+      o += (int64_t)r;
+      gstart.push_back(o - (int64_t)jtfs::kWsGuard);
+    }
+    for (int64_t g : gstart) cudaMemsetAsync((char*)ws + g, 0xA5, jtfs::kWsGuard, st);
+  }
+#endif
   for (int64_t b0 = 0; b0 < B; b0 += mb) {
     const int nb = (int)std::min<int64_t>(mb, B - b0);
     const std::string err = run_microbatch(P, x + b0 * P.N, nb, out + b0 * lay.floats_per_signal, w, false, 99, st, opts);
     if (!err.empty()) return fail(JTFS_ERR_CUDA, err);
   }
+#ifdef JTFS_WS_GUARDS
+  {
+    int64_t* d_starts = nullptr;
+    int* d_flag = nullptr;
+    cudaMalloc(&d_starts, gstart.size() * 8);
+    cudaMalloc(&d_flag, 4);
+    cudaMemcpy(d_starts, gstart.data(), gstart.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemsetAsync(d_flag, 0, 4, st);
+    jtfs::launch_guard_check(ws, d_starts, (int)gstart.size(), (int64_t)jtfs::kWsGuard, d_flag, st);
+    int h = 0;
+    cudaMemcpyAsync(&h, d_flag, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(d_starts);
+    cudaFree(d_flag);
+    if (h) return fail(JTFS_ERR_CUDA, "workspace guard overwritten (region mask " + std::to_string(h) + ")");
+  }
+#endif
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return JTFS_OK;

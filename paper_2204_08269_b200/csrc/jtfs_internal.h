@@ -196,6 +196,14 @@ struct Plan {
 std::string build_plan(const jtfs_params& p, Plan& plan);   // returns "" or an error message
 int ilog2_exact(int64_t v);  // -1 if not a power of two
 
+// workspace guard bands (validation builds: -DJTFS_WS_GUARDS, abi.cu checks them after
+// every forward; 0 in production builds)
+#ifdef JTFS_WS_GUARDS
+constexpr size_t kWsGuard = 65536;
+#else
+constexpr size_t kWsGuard = 0;
+#endif
+
 // workspace layout (per micro-batch of mb signals), in bytes
 struct WsLayout {
   size_t xhat, tmp, tmp2, u1, u1hat, yphi, y2, y16, ys, u1max, part, sel, flag, total;

@@ -1151,6 +1151,16 @@ cudaError_t measure_fp32_peak(double* tflops_ffma, double* tflops_ffma2) {
   return e;
 }
 
+// workspace guard check (JTFS_WS_GUARDS builds): any byte != pattern in the bands -> flag
+__global__ void k_guard_check(const unsigned char* ws, const int64_t* starts, int n, int64_t len, int* flag) {
+  const unsigned char* g = ws + starts[blockIdx.y];
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < len; i += (int64_t)gridDim.x * 256)
+    if (g[i] != 0xA5) atomicOr(flag, 1 << min((int)blockIdx.y, 30));
+}
+void launch_guard_check(const void* ws, const int64_t* d_starts, int n, int64_t len, int* flag, cudaStream_t st) {
+  k_guard_check<<<dim3(16, n), 256, 0, st>>>((const unsigned char*)ws, d_starts, n, len, flag);
+}
+
 // jtfs_debug_fft: the FFT engine on plain rows (fp32: both directions, lengths 2^1..2^18;
 // fp64: forward, 2^1..2^18), with the plan's twiddle tables (L <= N_pad)
 int launch_debug_fft(const Plan& P, int log2L, int dir, bool fp64, const void* in, void* out, int nrows, void* tmp,

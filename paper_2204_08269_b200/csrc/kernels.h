@@ -107,6 +107,7 @@ size_t isomap_workspace_bytes(int64_t n, int K);
 cudaError_t launch_isomap(const float* F, int n, int d, int64_t ldf, int K, int c, double* emb, double* evals,
                           void* ws, cudaStream_t st, int* disconnected);
 void launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t st);
+void launch_guard_check(const void* ws, const int64_t* d_starts, int n, int64_t len, int* flag, cudaStream_t st);
 cudaError_t measure_fp32_peak(double* tflops_ffma, double* tflops_ffma2);  // synchronous probe
 int launch_debug_fft(const Plan& P, int log2L, int dir, bool fp64, const void* in, void* out, int nrows, void* tmp,
                      cudaStream_t st);

@@ -771,7 +771,9 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
 }
 
 WsLayout ws_layout(const Plan& p, int64_t mb) {
-  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  // (JTFS_WS_GUARDS validation builds: every region carries a trailing guard band that the
+  // forward fills with a pattern and checks afterwards -- abi.cu)
+  auto al = [](size_t b) { return (b + 255) / 256 * 256 + kWsGuard; };
   WsLayout w{};
   w.xhat = al((size_t)mb * p.N_pad * 8);
   // four-step intermediate: largest group (rows x L) among U1 / Y2 / KA
@@ -801,7 +803,7 @@ WsLayout ws_layout(const Plan& p, int64_t mb) {
     for (const auto& d : p.kd) nsel += (size_t)std::max(1, d.L / 32);  // chunks >= 32 columns
     w.sel = al(nsel * 4);
   }
-  w.flag = 256;
+  w.flag = 256 + kWsGuard;
   w.total = w.xhat + w.tmp + w.tmp2 + w.u1 + w.u1hat + w.yphi + w.y2 + w.y16 + w.ys + w.u1max + w.part + w.sel +
             w.flag;
   return w;
