@@ -79,7 +79,6 @@ struct AlphaKD {
   int tc_NBB = 2;       // fp16 B-operand tile buffers
   int tc_S = 2, tc_tpu = 1;
   int tc_rps = 1;       // K-records per A ring stage
-  int tc_ew = 8;        // KD epilogue warps (8: two column sets, 16: four)
   int tc_stat = 0;      // 1: A stationary per CTA (its M-part's records resident), 0: A ring
   int tc_mpart = 1, tc_mblk = 1;  // M-parts of this alpha's KD and 128-pair-row M-blocks per part
   int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16

@@ -379,8 +379,9 @@ struct TcParams {
   int64_t part_off, part_stride;
 };
 
-// warp roles: 0..EW-1 epilogue, EW A producer, EW+1 MMA issuer, EW+2 B producer
-__host__ __device__ constexpr int threads_of(int ew) { return (ew + 3) * 32; }
+constexpr int kThreads = 352;
+// warp roles: 0..7 epilogue, 8 A producer, 9 MMA issuer, 10 B producer
+constexpr int kProdWarp = 8, kMmaWarp = 9, kBWarp = 10;
 constexpr int kNbuf = 2;  // TMEM accumulator buffers, each [acc1 | acc2] of 2 x 2 Nt columns
 
 // shared-memory carve-up (host and device agree through this function): B tile buffers,
@@ -462,36 +463,11 @@ __device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2
   }
 }
 
-// 8 columns of a set that covers half (OFF = 0 or 16) of a 32-column moment block (the
-// 16-warp epilogue): x16 TMEM loads, u_j of the block's basis, compile-time
-template <int G, int OFF>
-__device__ __forceinline__ void epi_group_mom8(uint32_t tb1, uint32_t tb2, float2 (&S)[4]) {
-  uint32_t v1[16], v2[16];
-  tmem_ld16(tb1 + 16 * G, v1);
-  tmem_ld16(tb2 + 16 * G, v2);
-  tmem_wait_ld();
-  reg_fence16(v1);
-  reg_fence16(v2);
-  float2 mz[8];
-  spin_mags<8>(v1, v2, mz);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float u = ((float)(OFF + 8 * G + j) - 15.5f) * 0.0625f;  // compile-time
-    S[0] = add2(S[0], mz[j]);
-    S[1] = fma2(mz[j], make_float2(u, u), S[1]);
-    S[2] = fma2(mz[j], make_float2(u * u, u * u), S[2]);
-    S[3] = fma2(mz[j], make_float2(u * u * u, u * u * u), S[3]);
-  }
-}
-
 // NTC: the tile width Nt as a compile-time constant (64 / 32: the epilogue's column loops
-// unroll completely).  PROF: the instrumented variant (JTFS_KD_PROF plan flag).  EW:
-// epilogue warps, 8 (two column sets) or 16 (four sets: twice the warps per SMSP to hide
-// the latencies of the epilogue-bound small-K alphas; fewer registers per thread).
-template <int NF, int MAXSLOT, bool PROF, int NTC, int EW>
-__global__ void __launch_bounds__((EW + 3) * 32, 1)
+// unroll completely).  PROF: the instrumented variant (JTFS_KD_PROF plan flag).
+template <int NF, int MAXSLOT, bool PROF, int NTC>
+__global__ void __launch_bounds__(kThreads, 1)
     k_kd_tc(const __grid_constant__ CUtensorMap tmB, TcParams p) {
-  constexpr int kProdWarp = EW, kMmaWarp = EW + 1, kBWarp = EW + 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
@@ -521,11 +497,11 @@ __global__ void __launch_bounds__((EW + 3) * 32, 1)
       mbar_init(b_full + i, 1);
       mbar_init(b_empty + i, 1);
       mbar_init(w_full + i, 1);
-      mbar_init(w_empty + i, EW);
+      mbar_init(w_empty + i, 8);
     }
     for (int i = 0; i < kNbuf; ++i) {
       mbar_init(acc_full + i, 1);
-      mbar_init(acc_empty + i, EW);
+      mbar_init(acc_empty + i, 8);
     }
     for (int i = 0; i < nab; ++i) {
       mbar_init(a_full + i, 1);
@@ -690,11 +666,10 @@ __global__ void __launch_bounds__((EW + 3) * 32, 1)
       atomicAdd(p.prof + 3, (unsigned long long)w_a);
     }
   } else {
-    // ===================== epilogue (warps 0..EW-1) =====================
-    constexpr int nsets = EW / 4;
-    const int eset = warp >> 2;  // column set
+    // ===================== epilogue (warps 0..7) =====================
+    const int eset = warp >> 2;  // column half
     const int q = warp & 3;      // TMEM lane quarter (warp_id % 4)
-    constexpr int half = Nt / nsets;  // columns per set
+    constexpr int half = Nt / 2;
     const int cbeg = eset * half;
     long long e_w = 0, e_acc = 0, e_math = 0;
     const long long e_start = clk<PROF>();
@@ -737,14 +712,6 @@ __global__ void __launch_bounds__((EW + 3) * 32, 1)
           if constexpr (half == 32) {
             epi_group_mom<0>(tb1, tb2, S);
             epi_group_mom<1>(tb1, tb2, S);
-          } else if constexpr (half == 16) {  // this set = one half of a 32-column block
-            if (eset & 1) {
-              epi_group_mom8<0, 16>(tb1, tb2, S);
-              epi_group_mom8<1, 16>(tb1, tb2, S);
-            } else {
-              epi_group_mom8<0, 0>(tb1, tb2, S);
-              epi_group_mom8<1, 0>(tb1, tb2, S);
-            }
           }
           tc_fence_before();
           __syncwarp();
@@ -795,7 +762,7 @@ __global__ void __launch_bounds__((EW + 3) * 32, 1)
         // unit done: my pair rows' pooled partials of this (time chunk, column half) slice,
         // theta = -1 (and phi_F) at row p, theta = +1 at row Mpp + p
         float* dst = p.part + (int64_t)b * p.part_stride + p.part_off +
-                     (int64_t)(nsets * chunk + eset) * (2 * p.Mpp) * p.nframes;
+                     (int64_t)(2 * chunk + eset) * (2 * p.Mpp) * p.nframes;
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k) {
           if (k < p.n_mblk) {
@@ -916,49 +883,33 @@ std::string plan_tc(Plan& P) {
       }
       return false;
     };
-    // Epilogue warps: 16 for the small-K alphas, whose KD is epilogue-bound (MUFU + FMA
-    // latencies with two warps per SMSP), 8 otherwise.  With 16 the pooled
-    // accumulators must fit fewer registers: <= 2 (NF 8) / 1 (NF 16) M-blocks per part.
-    const int nblocks = P.Mpp / 128;
-    d.tc_ew = (NF <= 16 && d.tc_nkc <= 7 && d.L >= 64) ? 16 : 8;
-    const int maxslot = d.tc_ew == 16 ? (NF == 8 ? 2 : 1) : (NF == 8 ? 5 : NF == 16 ? 2 : 1);
-    int mblk_ring = P.tc_n_mblk;
-    if (d.tc_ew == 16) {
-      mblk_ring = 1;
-      for (int k = maxslot; k >= 1; --k)
-        if (nblocks % k == 0) { mblk_ring = k; break; }
-    }
     // A stationary: each CTA keeps its M-part's n_mblk x nkc records resident for the whole
-    // launch, so A never streams from L2.  Used only with two B buffers, and for the 8-warp
-    // epilogue at most two M-parts (measured on c3: alpha 0 22.3 -> 20.9 ms per step; alphas
-    // 2-4, which need one B buffer or 5-10 parts re-reading every B tile, got 15-35 % slower).
+    // launch, so A never streams from L2.  Used only where it fits with two B buffers and at
+    // most two M-parts (measured on c3: alpha 0 22.3 -> 20.9 ms per step; alphas 2-4, which
+    // need one B buffer or 5-10 parts re-reading every B tile, got 15-35 % slower).
     auto choose_stat = [&]() {
+      const int nblocks = P.Mpp / 128, maxslot = NF == 8 ? 5 : NF == 16 ? 2 : 1;
       if (d.L < 64) return false;
-      for (int np = 1; np <= nblocks; ++np) {
+      for (int np = 1; np <= std::min(2, nblocks); ++np) {
         if (nblocks % np || nblocks / np > maxslot) continue;
-        if (d.tc_ew == 8 && np > 2) break;
-        d.tc_stat = 1;
-        d.tc_mpart = np;
-        d.tc_mblk = nblocks / np;
-        d.tc_Nt = 64;
-        d.tc_NBB = 2;
-        d.tc_S = 0;
-        if (tc_smem(d, NF) <= budget) return true;
+        for (int nbb = 2; nbb >= 2; --nbb) {
+          d.tc_stat = 1;
+          d.tc_mpart = np;
+          d.tc_mblk = nblocks / np;
+          d.tc_Nt = 64;
+          d.tc_NBB = nbb;
+          d.tc_S = 0;
+          if (tc_smem(d, NF) <= budget) return true;
+        }
       }
       d.tc_stat = 0;
       return false;
     };
     bool ok = choose_stat();
     if (!ok) {
-      d.tc_mblk = mblk_ring;
-      d.tc_mpart = nblocks / mblk_ring;
+      d.tc_mpart = P.tc_n_mpart;
+      d.tc_mblk = P.tc_n_mblk;
       ok = choose();
-      if (ok && d.tc_ew == 16 && d.tc_Nt != 64) {
-        d.tc_ew = 8;  // the 16-warp epilogue needs 64-column tiles
-        d.tc_mblk = P.tc_n_mblk;
-        d.tc_mpart = P.tc_n_mpart;
-        ok = choose();
-      }
       if (ok && d.pool_mode && d.tc_Nt != 64) {
         d.pool_mode = 0;
         ok = choose();
@@ -1009,13 +960,11 @@ cudaError_t tc_setup_device(Plan& P) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
   };
 #define JTFS_SET_KD(NF_, MS_)                                                                      \
-  set(tc::k_kd_tc<NF_, MS_, false, 64, 8>); set(tc::k_kd_tc<NF_, MS_, false, 32, 8>);              \
-  set(tc::k_kd_tc<NF_, MS_, true, 64, 8>); set(tc::k_kd_tc<NF_, MS_, true, 32, 8>);
-#define JTFS_SET_KD16(NF_, MS_) set(tc::k_kd_tc<NF_, MS_, false, 64, 16>); set(tc::k_kd_tc<NF_, MS_, true, 64, 16>);
-  if (NF == 8) { JTFS_SET_KD(8, 5) JTFS_SET_KD16(8, 2) }
-  else if (NF == 16) { JTFS_SET_KD(16, 2) JTFS_SET_KD16(16, 1) }
+  set(tc::k_kd_tc<NF_, MS_, false, 64>); set(tc::k_kd_tc<NF_, MS_, false, 32>);                    \
+  set(tc::k_kd_tc<NF_, MS_, true, 64>); set(tc::k_kd_tc<NF_, MS_, true, 32>);
+  if (NF == 8) { JTFS_SET_KD(8, 5) }
+  else if (NF == 16) { JTFS_SET_KD(16, 2) }
   else { JTFS_SET_KD(32, 1) }
-#undef JTFS_SET_KD16
 #undef JTFS_SET_KD
   return e;
 }
@@ -1126,19 +1075,13 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       cudaEventRecord(e0, st);
       P.prof_kd[i].push_back({(void*)e0, (void*)e1});
     }
-    auto go = [&](auto kern) { kern<<<grid, tc::threads_of(d.tc_ew), sm, st>>>(tmB, p); };
+    auto go = [&](auto kern) { kern<<<grid, tc::kThreads, sm, st>>>(tmB, p); };
 #define JTFS_GO_KD(NF_, MS_)                                                                        \
-  if (d.tc_Nt == 64) { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 64, 8>); else go(tc::k_kd_tc<NF_, MS_, false, 64, 8>); } \
-  else { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 32, 8>); else go(tc::k_kd_tc<NF_, MS_, false, 32, 8>); }
-#define JTFS_GO_KD16(NF_, MS_)                                                                      \
-  { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 64, 16>); else go(tc::k_kd_tc<NF_, MS_, false, 64, 16>); }
-    if (d.tc_ew == 16) {
-      if (NF == 8) { JTFS_GO_KD16(8, 2) }
-      else { JTFS_GO_KD16(16, 1) }
-    } else if (NF == 8) { JTFS_GO_KD(8, 5) }
+  if (d.tc_Nt == 64) { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 64>); else go(tc::k_kd_tc<NF_, MS_, false, 64>); } \
+  else { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 32>); else go(tc::k_kd_tc<NF_, MS_, false, 32>); }
+    if (NF == 8) { JTFS_GO_KD(8, 5) }
     else if (NF == 16) { JTFS_GO_KD(16, 2) }
     else { JTFS_GO_KD(32, 1) }
-#undef JTFS_GO_KD16
 #undef JTFS_GO_KD
     ++launches;
     if (P.prof) cudaEventRecord(e1, st);
@@ -1146,11 +1089,11 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       unsigned long long h[16];
       cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      const double nm = (double)grid, ne = (double)grid * d.tc_ew;
+      const double nm = (double)grid, ne = (double)grid * 8;
       std::fprintf(stderr,
-                   "KDPROF alpha %zu EW %d Nt %d NBB %d S %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
+                   "KDPROF alpha %zu Nt %d NBB %d S %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
                    "epi: total %.0f wait_w %.0f wait_acc %.0f math %.0f (kcycles/CTA)\n",
-                   i, d.tc_ew, d.tc_Nt, d.tc_NBB, d.tc_S, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
+                   i, d.tc_Nt, d.tc_NBB, d.tc_S, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
                    h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3);
     }
   }

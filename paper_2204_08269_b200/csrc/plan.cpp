@@ -704,7 +704,7 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   }
   P.part_total = 0;
   for (auto& d : P.kd) {
-    d.nslices = d.nchunks * (P.kd_impl == 1 ? d.tc_ew / 4 : 1);  // tcgen05 KD: one slice per epilogue set
+    d.nslices = d.nchunks * (P.kd_impl == 1 ? 2 : 1);  // tcgen05 KD: one slice per epilogue set
     d.part_off = P.part_total;
     P.part_total += (int64_t)d.nslices * P.Mpad * P.n_frames;
   }
