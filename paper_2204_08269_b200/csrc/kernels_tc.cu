@@ -463,6 +463,30 @@ __device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2
   }
 }
 
+// The CTA's tile sequence (unit u = blockIdx.x + i * gridDim.x, tiles 0..tpu-1 of each
+// unit), walked incrementally: the unit's fields (runtime divisions) once per unit.
+struct TileCursor {
+  int tile, u, mpart, chunk, b;
+  __device__ __forceinline__ void unit_fields(const TcParams& p) {
+    mpart = u % p.n_mpart;
+    const int c = (u / p.n_mpart) % p.nsel;
+    chunk = p.chunk_sel ? p.chunk_sel[c] : c;
+    b = u / (p.n_mpart * p.nsel);
+  }
+  __device__ __forceinline__ void start(const TcParams& p) {
+    tile = 0;
+    u = (int)blockIdx.x;
+    unit_fields(p);
+  }
+  __device__ __forceinline__ void next(const TcParams& p) {
+    if (++tile == p.tpu) {
+      tile = 0;
+      u += (int)gridDim.x;
+      unit_fields(p);
+    }
+  }
+};
+
 // NTC: the tile width Nt as a compile-time constant (64 / 32: the epilogue's column loops
 // unroll completely).  PROF: the instrumented variant (JTFS_KD_PROF plan flag).
 template <int NF, int MAXSLOT, bool PROF, int NTC>
@@ -535,12 +559,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t btx = (uint32_t)(p.K16 * 2 * Nt * 2);
     const int wcol = p.pool_mode ? NF / 8 : NF;  // table floats per time column
     const uint32_t wbytes = (uint32_t)(Nt * wcol * 4);
-    for (int gt = 0; gt < my_tiles; ++gt) {
-      const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
-      int chunk = (u / p.n_mpart) % p.nsel;
-      if (p.chunk_sel) chunk = p.chunk_sel[chunk];
-      const int b = u / (p.n_mpart * p.nsel);
-      const int t0 = (chunk * p.tpu + gt % p.tpu) * Nt;
+    TileCursor cur;
+    cur.start(p);
+    for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
+      const int chunk = cur.chunk, b = cur.b;
+      const int t0 = (chunk * p.tpu + cur.tile) * Nt;
       const int wi = gt & 1, bi = gt % p.NBB;
       if (lane == 0) {
         mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
@@ -573,9 +596,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // each, measured with tools/bulk_bw.cu), so lane s serves ring slot s (S lanes issue in
       // parallel; a slot is always served by the same lane: unambiguous parity waits)
       uint32_t s = 0, ph = 0;
-      for (int gt = 0; gt < my_tiles; ++gt) {
-        const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
-        const int mpart = u % p.n_mpart;
+      TileCursor cur;
+      cur.start(p);
+      for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
+        const int mpart = cur.mpart;
         for (int mb = 0; mb < p.n_mblk; ++mb) {
           const uint16_t* arec = p.A + (size_t)(mpart * p.n_mblk + mb) * p.nkc * (kRec / 2);
           for (int st = 0; st < nst; ++st) {
@@ -675,13 +699,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long e_start = clk<PROF>();
     uint32_t cnt = 0;
     float2 accm[MAXSLOT][NF / 2], accp[MAXSLOT][NF / 2];  // pooled partials of both spins of my pair rows
-    for (int gt = 0; gt < my_tiles; ++gt) {
-      const int u = (int)blockIdx.x + (gt / p.tpu) * (int)gridDim.x;
-      const int mpart = u % p.n_mpart;
-      int chunk = (u / p.n_mpart) % p.nsel;
-      if (p.chunk_sel) chunk = p.chunk_sel[chunk];
-      const int b = u / (p.n_mpart * p.nsel);
-      const int tile = gt % p.tpu;
+    TileCursor cur;
+    cur.start(p);
+    for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
+      const int mpart = cur.mpart, chunk = cur.chunk, b = cur.b, tile = cur.tile;
       if (tile == 0) {
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k)
