@@ -453,20 +453,14 @@ __device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2
   reg_fence(v2);
   float2 mz[16];
   spin_mags<16>(v1, v2, mz);
-  // two interleaved partial sums per moment (even / odd columns): 8 dependency chains of
-  // length 8 instead of 4 of length 16 (the FFMA2 latency chains bounded the epilogue)
-  float2 T[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const float u = ((float)(16 * G + j) - 15.5f) * 0.0625f;  // compile-time
-    float2(&A)[4] = (j & 1) ? T : S;
-    A[0] = add2(A[0], mz[j]);
-    A[1] = fma2(mz[j], make_float2(u, u), A[1]);
-    A[2] = fma2(mz[j], make_float2(u * u, u * u), A[2]);
-    A[3] = fma2(mz[j], make_float2(u * u * u, u * u * u), A[3]);
+    S[0] = add2(S[0], mz[j]);
+    S[1] = fma2(mz[j], make_float2(u, u), S[1]);
+    S[2] = fma2(mz[j], make_float2(u * u, u * u), S[2]);
+    S[3] = fma2(mz[j], make_float2(u * u * u, u * u * u), S[3]);
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) S[k] = add2(S[k], T[k]);
 }
 
 // The CTA's tile sequence (unit u = blockIdx.x + i * gridDim.x, tiles 0..tpu-1 of each
