@@ -275,6 +275,13 @@ def run_scat1d(args, rank, world, local, dev):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
+    # separate profiled pass: per-stage events (KA, KB, KS, KC, KT in the KD slot)
+    plan.profile_read(reset=True)
+    plan.profile_enable(True)
+    _timed_steps(lambda: plan.scattering1d(x, out), 2, flush, stream)
+    plan.profile_enable(False)
+    stages = {("KT_time_pooling" if k == "KD_joint" else k): round(v[0] / 2, 3)
+              for k, v in plan.profile_read(reset=True).items() if k != "KE_pool_pack"}
     if rank == 0:
         lay = plan.scat1d_layout
         print(json.dumps({
@@ -284,7 +291,8 @@ def run_scat1d(args, rank, world, local, dev):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "notes, Scattering1D setting of P:309-310", "batch_per_gpu": B,
                        "n1": lay.n1, "n2": lay.n2, "frames": lay.n_frames,
-                       "l2": "flushed before every timed step (256 MiB write)", **CFGS1D}}), flush=True)
+                       "l2": "flushed before every timed step (256 MiB write)", **CFGS1D},
+            "profiled_pass_stages_ms": stages}), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
