@@ -1420,6 +1420,70 @@ __global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
   }
 }
 
+// KT for the alphas with exact taps: the taps of a 128-column tile are staged in shared
+// memory once per CTA ([frame][column], padded rows) and shared by the CTA's 16 rows (2 per
+// warp), lane m accumulating frame m; each 32-column chunk's moduli go through a per-warp
+// shared buffer (broadcast reads).  The taps table ([L][NF], L2-resident) is read once per
+// 16 rows instead of once per row (the per-row form re-read NF x 4 B per column from L2).
+template <int NF>
+__global__ void __launch_bounds__(256) k_time_scat_taps(KTParams p) {
+  constexpr int TC = 128, TS = TC + 4;
+  __shared__ __align__(16) float taps[NF][TS];
+  __shared__ __align__(16) float mags[8][2][32];
+  const int ngrp = (p.K + 15) / 16;
+  const int b = blockIdx.x / ngrp, grp = blockIdx.x % ngrp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = grp * 16 + warp * 2;
+  const float* Yb = p.y2 + (int64_t)b * p.y2_stride;
+  float acc0 = 0.f, acc1 = 0.f;
+  for (int t0 = 0; t0 < p.L; t0 += TC) {
+    __syncthreads();  // the previous tile's taps are consumed
+    for (int idx = threadIdx.x; idx < TC * NF; idx += 256) {
+      const int t = idx / NF, m = idx % NF;
+      taps[m][t] = (t0 + t < p.L) ? __ldg(p.wtab + (int64_t)(t0 + t) * NF + m) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int c = 0; c < TC; c += 32) {
+      const int t = t0 + c + lane;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        float mg = 0.f;
+        if (r0 + r < p.K && t < p.L) {
+          const float* re = Yb + (int64_t)(2 * (r0 + r)) * p.L;
+          const float a = __ldg(re + t), d = __ldg(re + p.L + t);
+          mg = sqrtf(fmaf(a, a, d * d));
+        }
+        mags[warp][r][lane] = mg;
+      }
+      __syncwarp();
+      if (lane < NF) {
+        const float4* w4 = reinterpret_cast<const float4*>(&taps[lane][c]);
+        const float4* m0 = reinterpret_cast<const float4*>(&mags[warp][0][0]);
+        const float4* m1 = reinterpret_cast<const float4*>(&mags[warp][1][0]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 w = w4[q], x = m0[q], y = m1[q];
+          acc0 = fmaf(w.x, x.x, acc0);
+          acc0 = fmaf(w.y, x.y, acc0);
+          acc0 = fmaf(w.z, x.z, acc0);
+          acc0 = fmaf(w.w, x.w, acc0);
+          acc1 = fmaf(w.x, y.x, acc1);
+          acc1 = fmaf(w.y, y.y, acc1);
+          acc1 = fmaf(w.z, y.z, acc1);
+          acc1 = fmaf(w.w, y.w, acc1);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (lane < p.nframes) {
+    float* o = p.out + (int64_t)b * p.fps + (int64_t)r0 * p.nframes + lane;
+    if (r0 < p.K) o[0] = acc0;
+    if (r0 + 1 < p.K) o[p.nframes] = acc1;
+  }
+}
+
 int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64_t fps, int64_t off_s2,
                      cudaStream_t st) {
   int row0 = 0, n = 0;
@@ -1434,11 +1498,18 @@ int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64
     k.nframes = P.n_frames;
     k.K = d.K;
     k.pool_mode = (d.pool_mode == 1 && d.L % 32 == 0) ? 1 : 0;
-    const int grid = nsig * d.K;
     // the table's frame stride NF = 8 / 16 / 32 (plan.cpp, n_frames <= 32)
-    if (P.n_frames <= 8) k_time_scat<8><<<grid, 256, 0, st>>>(k);
-    else if (P.n_frames <= 16) k_time_scat<16><<<grid, 256, 0, st>>>(k);
-    else k_time_scat<32><<<grid, 256, 0, st>>>(k);
+    if (k.pool_mode == 1) {
+      const int grid = nsig * d.K;
+      if (P.n_frames <= 8) k_time_scat<8><<<grid, 256, 0, st>>>(k);
+      else if (P.n_frames <= 16) k_time_scat<16><<<grid, 256, 0, st>>>(k);
+      else k_time_scat<32><<<grid, 256, 0, st>>>(k);
+    } else {
+      const int grid = nsig * ((d.K + 15) / 16);
+      if (P.n_frames <= 8) k_time_scat_taps<8><<<grid, 256, 0, st>>>(k);
+      else if (P.n_frames <= 16) k_time_scat_taps<16><<<grid, 256, 0, st>>>(k);
+      else k_time_scat_taps<32><<<grid, 256, 0, st>>>(k);
+    }
     row0 += d.K;
     ++n;
   }

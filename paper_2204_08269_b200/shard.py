@@ -100,16 +100,20 @@ def exchange_partials(partials, ranges, group=None, dst: int = 0):
     return partials
 
 
-_SETS = {}
+_SHARDS = {}
 
 
-def _unitset(plan, first, last):
-    key = (id(plan), first, last)
-    us = _SETS.get(key)
-    if us is None or us.plan is not plan:
-        us = plan.unitset(range(first, last))
-        _SETS[key] = us
-    return us
+def _shard_of(plan, world: int, rank: int):
+    """(unit set bound for this rank, owned partial ranges of every rank), computed once per
+    (plan, world, rank): the host-side assignment is not on the per-forward path."""
+    key = (id(plan), world, rank)
+    hit = _SHARDS.get(key)
+    if hit is None or hit[0].plan is not plan:
+        parts = contiguous_assign([u["cost"] for u in plan.units()], world)
+        first, last = parts[rank]
+        hit = (plan.unitset(range(first, last)), [owned_range(plan, a, b) for a, b in parts])
+        _SHARDS[key] = hit
+    return hit
 
 
 def forward_sharded(plan, x, group=None, stream=None):
@@ -119,17 +123,16 @@ def forward_sharded(plan, x, group=None, stream=None):
     import torch.distributed as dist
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    parts = contiguous_assign([u["cost"] for u in plan.units()], world)
-    first, last = parts[rank]
+    uset, ranges = _shard_of(plan, world, rank)
     B = x.shape[0]
     # every step (KD, the NCCL exchange, KE) is ordered on ONE stream: torch's
     # point-to-point ops run on the current stream, so a caller's stream becomes it here
     with torch.cuda.stream(stream) if stream is not None else _nullctx():
         partials = torch.empty(B, plan.partials_size, dtype=torch.float32, device=x.device)
         out = torch.empty(B, plan.floats_per_signal, dtype=torch.float32, device=x.device)
-        plan.forward_unitset(x, _unitset(plan, first, last), partials, out)
+        plan.forward_unitset(x, uset, partials, out)
         if world > 1:
-            exchange_partials(partials, [owned_range(plan, a, b) for a, b in parts], group=group, dst=0)
+            exchange_partials(partials, ranges, group=group, dst=0)
         if rank != 0:
             return None
         plan.reduce_pack(partials, out)
