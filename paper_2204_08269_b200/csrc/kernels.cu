@@ -1420,67 +1420,103 @@ __global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
   }
 }
 
-// KT for the alphas with exact taps: the taps of a 128-column tile are staged in shared
-// memory once per CTA ([frame][column], padded rows) and shared by the CTA's 16 rows (2 per
-// warp), lane m accumulating frame m; each 32-column chunk's moduli go through a per-warp
-// shared buffer (broadcast reads).  The taps table ([L][NF], L2-resident) is read once per
-// 16 rows instead of once per row (the per-row form re-read NF x 4 B per column from L2).
+// KT, thread = row: a CTA takes 32 rows (one per lane) of one (signal, alpha); its 8 warps
+// split the columns in 32-column blocks (warp w: blocks w, w + 8, ...).  Each lane reads its
+// row's 32 columns of a block (16 B vector loads), forms |Y2| and pools them in registers:
+// with the cubic-moment form S_k = sum_j |Y2_j| u_j^k (k <= 3) and then pooled += G_k S_k
+// (the block's 4 x NF coefficients, a broadcast shared-memory read), else with the exact taps
+// (NF FMAs per column, taps [32][NF] of the block broadcast from shared memory).  The 8
+// warps' partial sums are combined in fixed order (bit-stable).
 template <int NF>
-__global__ void __launch_bounds__(256) k_time_scat_taps(KTParams p) {
-  constexpr int TC = 128, TS = TC + 4;
-  __shared__ __align__(16) float taps[NF][TS];
-  __shared__ __align__(16) float mags[8][2][32];
-  const int ngrp = (p.K + 15) / 16;
+__global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
+  constexpr int TB = 8;  // 32-column blocks staged per round (one per warp)
+  constexpr int NTAB = TB * 32 * NF, NRED = 8 * 32 * (NF + 1);
+  __shared__ __align__(16) float sbuf[NTAB > NRED ? NTAB : NRED];
+  float(*tab)[32][NF] = reinterpret_cast<float(*)[32][NF]>(sbuf);       // per block: taps [32][NF] or moments [4][NF]
+  float(*red)[32][NF + 1] = reinterpret_cast<float(*)[32][NF + 1]>(sbuf);  // the warps' partial sums (after the loop)
+  const int ngrp = (p.K + 31) / 32;
   const int b = blockIdx.x / ngrp, grp = blockIdx.x % ngrp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r0 = grp * 16 + warp * 2;
-  const float* Yb = p.y2 + (int64_t)b * p.y2_stride;
-  float acc0 = 0.f, acc1 = 0.f;
-  for (int t0 = 0; t0 < p.L; t0 += TC) {
-    __syncthreads();  // the previous tile's taps are consumed
-    for (int idx = threadIdx.x; idx < TC * NF; idx += 256) {
-      const int t = idx / NF, m = idx % NF;
-      taps[m][t] = (t0 + t < p.L) ? __ldg(p.wtab + (int64_t)(t0 + t) * NF + m) : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int c = 0; c < TC; c += 32) {
-      const int t = t0 + c + lane;
+  const int r = grp * 32 + lane;
+  const bool active = r < p.K;
+  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * (active ? r : 0)) * p.L;
+  const float* im = re + p.L;
+  const int nblk = p.L / 32;
+  const int wblk = p.pool_mode ? 4 * NF : 32 * NF;  // table floats per block
+  float acc[NF];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        float mg = 0.f;
-        if (r0 + r < p.K && t < p.L) {
-          const float* re = Yb + (int64_t)(2 * (r0 + r)) * p.L;
-          const float a = __ldg(re + t), d = __ldg(re + p.L + t);
-          mg = sqrtf(fmaf(a, a, d * d));
-        }
-        mags[warp][r][lane] = mg;
-      }
-      __syncwarp();
-      if (lane < NF) {
-        const float4* w4 = reinterpret_cast<const float4*>(&taps[lane][c]);
-        const float4* m0 = reinterpret_cast<const float4*>(&mags[warp][0][0]);
-        const float4* m1 = reinterpret_cast<const float4*>(&mags[warp][1][0]);
+  for (int m = 0; m < NF; ++m) acc[m] = 0.f;
+  for (int blk0 = 0; blk0 < nblk; blk0 += TB) {
+    __syncthreads();
+    const int nb = min(TB, nblk - blk0);
+    for (int idx = threadIdx.x; idx < nb * wblk; idx += 256)
+      (&tab[0][0][0])[(idx / wblk) * 32 * NF + idx % wblk] = __ldg(p.wtab + (int64_t)blk0 * wblk + idx);
+    __syncthreads();
+    if (warp < nb && active) {
+      const int t0 = (blk0 + warp) * 32;
+      const float* tb = &tab[warp][0][0];
+      if (p.pool_mode) {
+        float S0 = 0.f, S1 = 0.f, S2 = 0.f, S3 = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 w = w4[q], x = m0[q], y = m1[q];
-          acc0 = fmaf(w.x, x.x, acc0);
-          acc0 = fmaf(w.y, x.y, acc0);
-          acc0 = fmaf(w.z, x.z, acc0);
-          acc0 = fmaf(w.w, x.w, acc0);
-          acc1 = fmaf(w.x, y.x, acc1);
-          acc1 = fmaf(w.y, y.y, acc1);
-          acc1 = fmaf(w.z, y.z, acc1);
-          acc1 = fmaf(w.w, y.w, acc1);
+          const float4 a = __ldg(reinterpret_cast<const float4*>(re + t0) + q);
+          const float4 c = __ldg(reinterpret_cast<const float4*>(im + t0) + q);
+          const float mg[4] = {sqrtf(fmaf(a.x, a.x, c.x * c.x)), sqrtf(fmaf(a.y, a.y, c.y * c.y)),
+                               sqrtf(fmaf(a.z, a.z, c.z * c.z)), sqrtf(fmaf(a.w, a.w, c.w * c.w))};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float u = ((float)(4 * q + e) - 15.5f) * 0.0625f;  // compile-time
+            S0 += mg[e];
+            S1 = fmaf(mg[e], u, S1);
+            S2 = fmaf(mg[e], u * u, S2);
+            S3 = fmaf(mg[e], u * u * u, S3);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < NF; ++m) {
+          float v = acc[m];
+          v = fmaf(tb[m], S0, v);
+          v = fmaf(tb[NF + m], S1, v);
+          v = fmaf(tb[2 * NF + m], S2, v);
+          v = fmaf(tb[3 * NF + m], S3, v);
+          acc[m] = v;
+        }
+      } else {
+#pragma unroll 2
+        for (int q = 0; q < 8; ++q) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(re + t0) + q);
+          const float4 c = __ldg(reinterpret_cast<const float4*>(im + t0) + q);
+          const float mg[4] = {sqrtf(fmaf(a.x, a.x, c.x * c.x)), sqrtf(fmaf(a.y, a.y, c.y * c.y)),
+                               sqrtf(fmaf(a.z, a.z, c.z * c.z)), sqrtf(fmaf(a.w, a.w, c.w * c.w))};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float4* w4 = reinterpret_cast<const float4*>(tb + (4 * q + e) * NF);
+#pragma unroll
+            for (int m4 = 0; m4 < NF / 4; ++m4) {
+              const float4 w = w4[m4];
+              acc[4 * m4 + 0] = fmaf(w.x, mg[e], acc[4 * m4 + 0]);
+              acc[4 * m4 + 1] = fmaf(w.y, mg[e], acc[4 * m4 + 1]);
+              acc[4 * m4 + 2] = fmaf(w.z, mg[e], acc[4 * m4 + 2]);
+              acc[4 * m4 + 3] = fmaf(w.w, mg[e], acc[4 * m4 + 3]);
+            }
+          }
         }
       }
-      __syncwarp();
     }
   }
-  if (lane < p.nframes) {
-    float* o = p.out + (int64_t)b * p.fps + (int64_t)r0 * p.nframes + lane;
-    if (r0 < p.K) o[0] = acc0;
-    if (r0 + 1 < p.K) o[p.nframes] = acc1;
+  __syncthreads();  // the table buffer becomes the reduction buffer
+#pragma unroll
+  for (int m = 0; m < NF; ++m) red[warp][lane][m] = acc[m];
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < 32 * NF; idx += 256) {
+    const int rl = idx / NF, m = idx % NF;
+    const int row = grp * 32 + rl;
+    if (row < p.K && m < p.nframes) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[w][rl][m];
+      p.out[(int64_t)b * p.fps + (int64_t)row * p.nframes + m] = v;
+    }
   }
 }
 
@@ -1498,17 +1534,18 @@ int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64
     k.nframes = P.n_frames;
     k.K = d.K;
     k.pool_mode = (d.pool_mode == 1 && d.L % 32 == 0) ? 1 : 0;
-    // the table's frame stride NF = 8 / 16 / 32 (plan.cpp, n_frames <= 32)
-    if (k.pool_mode == 1) {
+    // the table's frame stride NF = 8 / 16 / 32 (plan.cpp, n_frames <= 32); blocks of 32
+    // columns (L is a power of two >= 32 for every alpha that reaches KT: L / 32 >= 1)
+    if (d.L % 32 == 0) {
+      const int grid = nsig * ((d.K + 31) / 32);
+      if (P.n_frames <= 8) k_time_scat_rows<8><<<grid, 256, 0, st>>>(k);
+      else if (P.n_frames <= 16) k_time_scat_rows<16><<<grid, 256, 0, st>>>(k);
+      else k_time_scat_rows<32><<<grid, 256, 0, st>>>(k);
+    } else {
       const int grid = nsig * d.K;
       if (P.n_frames <= 8) k_time_scat<8><<<grid, 256, 0, st>>>(k);
       else if (P.n_frames <= 16) k_time_scat<16><<<grid, 256, 0, st>>>(k);
       else k_time_scat<32><<<grid, 256, 0, st>>>(k);
-    } else {
-      const int grid = nsig * ((d.K + 15) / 16);
-      if (P.n_frames <= 8) k_time_scat_taps<8><<<grid, 256, 0, st>>>(k);
-      else if (P.n_frames <= 16) k_time_scat_taps<16><<<grid, 256, 0, st>>>(k);
-      else k_time_scat_taps<32><<<grid, 256, 0, st>>>(k);
     }
     row0 += d.K;
     ++n;
