@@ -834,7 +834,12 @@ jtfs_status jtfs_scattering1d(jtfs_plan_t plan, const float* x, int64_t B, float
                                      lay.off_s1, P.d_u1_off, P.d_k1, P.d_band_L1, st));
     }
     { StageScope sc(P, 3, st); sc.done(jtfs::launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
-    { StageScope sc(P, 4, st); sc.done(jtfs::launch_time_scat(P, w.y2, nb, ob, lay.floats_per_signal, lay.off_s2, st)); }
+    {
+      StageScope sc(P, 4, st);
+      const jtfs::WsLayout L = jtfs::ws_layout(P, mb);
+      sc.done(jtfs::launch_time_scat(P, w.y2, nb, ob, lay.floats_per_signal, lay.off_s2, st, w.part,
+                                     (L.part - jtfs::kWsGuard) / 4));
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");

@@ -1355,6 +1355,8 @@ struct KTParams {
   float* out;         // out record of signal 0 at row0's first frame; signal stride fps
   int64_t y2_stride, fps;
   int L, nframes, K, pool_mode;
+  int nsplit;         // k_time_scat_rows: column splits (partials [signal][split][K][NF] in part)
+  float* part;
 };
 
 template <int NF>
@@ -1435,18 +1437,22 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
   float(*tab)[32][NF] = reinterpret_cast<float(*)[32][NF]>(sbuf);       // per block: taps [32][NF] or moments [4][NF]
   float(*red)[32][NF + 1] = reinterpret_cast<float(*)[32][NF + 1]>(sbuf);  // the warps' partial sums (after the loop)
   const int ngrp = (p.K + 31) / 32;
-  const int b = blockIdx.x / ngrp, grp = blockIdx.x % ngrp;
+  const int split = blockIdx.x % p.nsplit;
+  const int b = blockIdx.x / (p.nsplit * ngrp), grp = (blockIdx.x / p.nsplit) % ngrp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = grp * 32 + lane;
   const bool active = r < p.K;
   const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * (active ? r : 0)) * p.L;
   const float* im = re + p.L;
-  const int nblk = p.L / 32;
+  // this CTA's 32-column blocks: split `split` of nsplit equal ranges
+  const int nblk_all = p.L / 32;
+  const int per = (nblk_all + p.nsplit - 1) / p.nsplit;
+  const int bbeg = split * per, nblk = min(nblk_all, bbeg + per);
   const int wblk = p.pool_mode ? 4 * NF : 32 * NF;  // table floats per block
   float acc[NF];
 #pragma unroll
   for (int m = 0; m < NF; ++m) acc[m] = 0.f;
-  for (int blk0 = 0; blk0 < nblk; blk0 += TB) {
+  for (int blk0 = bbeg; blk0 < nblk; blk0 += TB) {
     __syncthreads();
     const int nb = min(TB, nblk - blk0);
     for (int idx = threadIdx.x; idx < nb * wblk; idx += 256)
@@ -1515,13 +1521,27 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
       float v = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) v += red[w][rl][m];
-      p.out[(int64_t)b * p.fps + (int64_t)row * p.nframes + m] = v;
+      if (p.nsplit == 1) p.out[(int64_t)b * p.fps + (int64_t)row * p.nframes + m] = v;
+      else p.part[(((int64_t)b * p.nsplit + split) * p.K + row) * NF + m] = v;
     }
   }
 }
 
+// sum of k_time_scat_rows' column-split partials in fixed split order
+template <int NF>
+__global__ void k_time_scat_sum(KTParams p, int nsig) {
+  const int64_t i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= (int64_t)nsig * p.K * p.nframes) return;
+  const int m = (int)(i % p.nframes);
+  const int row = (int)((i / p.nframes) % p.K);
+  const int b = (int)(i / ((int64_t)p.nframes * p.K));
+  float v = 0.f;
+  for (int sp = 0; sp < p.nsplit; ++sp) v += p.part[(((int64_t)b * p.nsplit + sp) * p.K + row) * NF + m];
+  p.out[(int64_t)b * p.fps + (int64_t)row * p.nframes + m] = v;
+}
+
 int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64_t fps, int64_t off_s2,
-                     cudaStream_t st) {
+                     cudaStream_t st, float* scratch, size_t scratch_floats) {
   int row0 = 0, n = 0;
   for (const auto& d : P.kd) {
     KTParams k{};
@@ -1537,10 +1557,23 @@ int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64
     // the table's frame stride NF = 8 / 16 / 32 (plan.cpp, n_frames <= 32); blocks of 32
     // columns (L is a power of two >= 32 for every alpha that reaches KT: L / 32 >= 1)
     if (d.L % 32 == 0) {
-      const int grid = nsig * ((d.K + 31) / 32);
+      // enough CTAs for the machine (>= 4 per SM): split the columns, >= 8 blocks each
+      const int ngrp = (d.K + 31) / 32, NF = P.n_frames <= 8 ? 8 : P.n_frames <= 16 ? 16 : 32;
+      int nsplit = std::max(1, std::min(d.L / 32 / 8, (4 * 148 + nsig * ngrp - 1) / (nsig * ngrp)));
+      while (nsplit > 1 && (size_t)nsig * nsplit * d.K * NF > scratch_floats) --nsplit;
+      k.nsplit = nsplit;
+      k.part = scratch;
+      const int grid = nsig * ngrp * nsplit;
       if (P.n_frames <= 8) k_time_scat_rows<8><<<grid, 256, 0, st>>>(k);
       else if (P.n_frames <= 16) k_time_scat_rows<16><<<grid, 256, 0, st>>>(k);
       else k_time_scat_rows<32><<<grid, 256, 0, st>>>(k);
+      if (nsplit > 1) {
+        const int sg = (int)(((int64_t)nsig * d.K * P.n_frames + 255) / 256);
+        if (P.n_frames <= 8) k_time_scat_sum<8><<<sg, 256, 0, st>>>(k, nsig);
+        else if (P.n_frames <= 16) k_time_scat_sum<16><<<sg, 256, 0, st>>>(k, nsig);
+        else k_time_scat_sum<32><<<sg, 256, 0, st>>>(k, nsig);
+        ++n;
+      }
     } else {
       const int grid = nsig * d.K;
       if (P.n_frames <= 8) k_time_scat<8><<<grid, 256, 0, st>>>(k);

@@ -79,7 +79,7 @@ int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_
 size_t ke_smem_bytes(const Plan& P);
 int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
 int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64_t fps, int64_t off_s2,
-                     cudaStream_t st);
+                     cudaStream_t st, float* scratch, size_t scratch_floats);
 cudaError_t ke_set_smem(const Plan& P);
 // KD on the tensor cores from KD's fp16 operand y16 and the inverse scales ysi [nsig][n_alpha]
 int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float* part, cudaStream_t st, int* err,
