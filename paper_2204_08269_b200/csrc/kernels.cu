@@ -1434,7 +1434,6 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
   constexpr int TB = 8;  // 32-column blocks staged per round (one per warp)
   constexpr int NTAB = TB * 32 * NF, NRED = 8 * 32 * (NF + 1);
   __shared__ __align__(16) float sbuf[NTAB > NRED ? NTAB : NRED];
-  extern __shared__ __align__(16) float ytile[];  // [8 warps][re, im][32 rows][36]
   float(*tab)[32][NF] = reinterpret_cast<float(*)[32][NF]>(sbuf);       // per block: taps [32][NF] or moments [4][NF]
   float(*red)[32][NF + 1] = reinterpret_cast<float(*)[32][NF + 1]>(sbuf);  // the warps' partial sums (after the loop)
   const int ngrp = (p.K + 31) / 32;
@@ -1443,6 +1442,8 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = grp * 32 + lane;
   const bool active = r < p.K;
+  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * (active ? r : 0)) * p.L;
+  const float* im = re + p.L;
   // this CTA's 32-column blocks: split `split` of nsplit equal ranges
   const int nblk_all = p.L / 32;
   const int per = (nblk_all + p.nsplit - 1) / p.nsplit;
@@ -1457,34 +1458,15 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
     for (int idx = threadIdx.x; idx < nb * wblk; idx += 256)
       (&tab[0][0][0])[(idx / wblk) * 32 * NF + idx % wblk] = __ldg(p.wtab + (int64_t)blk0 * wblk + idx);
     __syncthreads();
-    if (warp < nb) {
+    if (warp < nb && active) {
       const int t0 = (blk0 + warp) * 32;
       const float* tb = &tab[warp][0][0];
-      // the warp's 32 rows x 32 columns of Re / Im Y2: coalesced row loads (lane = column)
-      // into a per-warp tile, then lane = row reads its 32 columns (padded rows: LDS.128 at
-      // the minimum 4 wavefronts)
-      float* tre = ytile + warp * 2 * 32 * 36;
-      float* tim = tre + 32 * 36;
-      const float* yb = p.y2 + (int64_t)b * p.y2_stride + t0 + lane;
-#pragma unroll 4
-      for (int rr = 0; rr < 32; ++rr) {
-        const int row = grp * 32 + rr;
-        float a = 0.f, c = 0.f;
-        if (row < p.K) {
-          a = __ldg(yb + (int64_t)(2 * row) * p.L);
-          c = __ldg(yb + (int64_t)(2 * row + 1) * p.L);
-        }
-        tre[rr * 36 + lane] = a;
-        tim[rr * 36 + lane] = c;
-      }
-      __syncwarp();
-      const float4* rre = reinterpret_cast<const float4*>(tre + lane * 36);
-      const float4* rim = reinterpret_cast<const float4*>(tim + lane * 36);
-      if (active && p.pool_mode) {
+      if (p.pool_mode) {
         float S0 = 0.f, S1 = 0.f, S2 = 0.f, S3 = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 a = rre[q], c = rim[q];
+          const float4 a = __ldg(reinterpret_cast<const float4*>(re + t0) + q);
+          const float4 c = __ldg(reinterpret_cast<const float4*>(im + t0) + q);
           const float mg[4] = {sqrtf(fmaf(a.x, a.x, c.x * c.x)), sqrtf(fmaf(a.y, a.y, c.y * c.y)),
                                sqrtf(fmaf(a.z, a.z, c.z * c.z)), sqrtf(fmaf(a.w, a.w, c.w * c.w))};
 #pragma unroll
@@ -1505,10 +1487,11 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
           v = fmaf(tb[3 * NF + m], S3, v);
           acc[m] = v;
         }
-      } else if (active) {
+      } else {
 #pragma unroll 2
         for (int q = 0; q < 8; ++q) {
-          const float4 a = rre[q], c = rim[q];
+          const float4 a = __ldg(reinterpret_cast<const float4*>(re + t0) + q);
+          const float4 c = __ldg(reinterpret_cast<const float4*>(im + t0) + q);
           const float mg[4] = {sqrtf(fmaf(a.x, a.x, c.x * c.x)), sqrtf(fmaf(a.y, a.y, c.y * c.y)),
                                sqrtf(fmaf(a.z, a.z, c.z * c.z)), sqrtf(fmaf(a.w, a.w, c.w * c.w))};
 #pragma unroll
@@ -1525,7 +1508,6 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
           }
         }
       }
-      __syncwarp();
     }
   }
   __syncthreads();  // the table buffer becomes the reduction buffer
@@ -1582,17 +1564,9 @@ int launch_time_scat(const Plan& P, const float* y2, int nsig, float* out, int64
       k.nsplit = nsplit;
       k.part = scratch;
       const int grid = nsig * ngrp * nsplit;
-      constexpr size_t ysm = 8 * 2 * 32 * 36 * sizeof(float);  // the per-warp Y2 tiles (73.7 KB)
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_time_scat_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm);
-        cudaFuncSetAttribute(k_time_scat_rows<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm);
-        cudaFuncSetAttribute(k_time_scat_rows<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ysm);
-        attr = true;
-      }
-      if (P.n_frames <= 8) k_time_scat_rows<8><<<grid, 256, ysm, st>>>(k);
-      else if (P.n_frames <= 16) k_time_scat_rows<16><<<grid, 256, ysm, st>>>(k);
-      else k_time_scat_rows<32><<<grid, 256, ysm, st>>>(k);
+      if (P.n_frames <= 8) k_time_scat_rows<8><<<grid, 256, 0, st>>>(k);
+      else if (P.n_frames <= 16) k_time_scat_rows<16><<<grid, 256, 0, st>>>(k);
+      else k_time_scat_rows<32><<<grid, 256, 0, st>>>(k);
       if (nsplit > 1) {
         const int sg = (int)(((int64_t)nsig * d.K * P.n_frames + 255) / 256);
         if (P.n_frames <= 8) k_time_scat_sum<8><<<sg, 256, 0, st>>>(k, nsig);
