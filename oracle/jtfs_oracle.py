@@ -21,7 +21,8 @@ order) follows the readings R1-R20 of DESIGN.md §3 (= SURVEY.md §8(c)).
 Every convolution is written the plain way: DFT on the stated grid, multiply
 by the sampled filter, inverse DFT at full rate, THEN decimate by indexing.
 No folding, no truncation, no blocking.  scipy.fft (pocketfft, fp64) is the
-DFT library primitive; tests pin it against an explicit DFT matrix.
+DFT library primitive; tests pin it against an explicit DFT matrix (L <= 128) and
+against an independent textbook radix-2 FFT at every length 2^1 .. 2^18.
 
 Pinned by tests/test_oracle_*.py (closed forms, the paper's 44 x 32 shape,
 brute-force time-domain convolution at tiny N, exact invariants, Fig. 1 spin

@@ -221,3 +221,49 @@ def test_u2_map_equals_bruteforce(prm):
         got = O.u2_map(x, prm, pi, s)
         assert got.shape == ref.shape == O.u2_map_shape(s, pi)
         assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref)), pi
+
+
+def _textbook_fft(v, sign):
+    """Iterative radix-2 decimation-in-time DFT sum_n v[n] e^{sign 2 pi i k n / L} (fp64),
+    twiddles from exact integer range reduction: written independently of scipy / numpy.fft."""
+    L = len(v)
+    bits = L.bit_length() - 1
+    idx = np.arange(L)
+    rev = np.zeros(L, dtype=np.int64)
+    for b in range(bits):
+        rev |= ((idx >> b) & 1) << (bits - 1 - b)
+    a = np.asarray(v, dtype=np.complex128)[rev].copy()
+    span = 1
+    while span < L:
+        k = np.arange(span)
+        w = np.exp(sign * 2j * np.pi * k / (2 * span))
+        a = a.reshape(-1, 2 * span)
+        top, bot = a[:, :span].copy(), a[:, span:] * w
+        a[:, :span] = top + bot
+        a[:, span:] = top - bot
+        a = a.reshape(-1)
+        span *= 2
+    return a
+
+
+def test_dft_primitive_against_textbook_fft_every_length():
+    # the oracle's DFT primitive (scipy.fft / pocketfft) against an independent textbook
+    # radix-2 FFT at every power-of-two length the path uses (2^1 .. 2^18): pins the library
+    # routine at the sizes where the explicit-matrix check (L <= 128) cannot reach
+    rng = np.random.default_rng(12)
+    for lg in range(1, 19):
+        L = 2 ** lg
+        v = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+        ref_f = _textbook_fft(v, -1)
+        ref_i = _textbook_fft(v, +1) / L
+        sc = np.linalg.norm(ref_f)
+        assert np.linalg.norm(O._fft(v) - ref_f) <= 1e-13 * sc * lg, lg
+        assert np.linalg.norm(O._ifft(v) - ref_i) <= 1e-13 * np.linalg.norm(ref_i) * lg, lg
+
+
+def test_textbook_fft_against_explicit_matrix():
+    # the textbook FFT itself, pinned to the definition on small lengths
+    rng = np.random.default_rng(13)
+    for L in (2, 8, 64, 256):
+        v = rng.standard_normal(L) + 1j * rng.standard_normal(L)
+        np.testing.assert_allclose(_textbook_fft(v, -1), dft_explicit(v), atol=1e-10)
