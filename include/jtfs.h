@@ -272,6 +272,13 @@ JTFS_API jtfs_status jtfs_backward_workspace_size(jtfs_plan_t plan, int64_t B, s
 JTFS_API jtfs_status jtfs_backward(jtfs_plan_t plan, const float* x, int64_t B, const float* dout, float* dx,
                                    void* ws, size_t ws_bytes, void* stream);
 
+/* Texture-resynthesis loss of one record: E = ||Sy - Sx||_2 / ||Sx||_2 and
+ * dE/dSy = (Sy - Sx) / (||Sy - Sx|| ||Sx||) (0 where Sy = Sx), fp64 fixed-order sums.
+ *   Sy, Sx  device fp32 [floats_per_signal];  E  device fp64 scalar;  dout  device fp32
+ *   [floats_per_signal] (the jtfs_backward input).  Asynchronous on `stream`. */
+JTFS_API jtfs_status jtfs_resynth_loss(jtfs_plan_t plan, const float* Sy, const float* Sx, double* E,
+                                       float* dout, void* stream);
+
 /* Debug/test query: byte offsets inside the backward workspace (for B signals)
  * of its regions, in this order: 0 X_hat, 1 tmp, 2 U1, 3 U1hat, 4 Y_phi, 5 Y2,
  * 6 scratch out, 7 dP, 8 dY_phi, 9 dY2, 10 DFT(dY2), 11 dU1hat, 12 dU1, 13 W,

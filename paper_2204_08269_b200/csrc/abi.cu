@@ -532,6 +532,18 @@ jtfs_status jtfs_forward_mulog(jtfs_plan_t plan, const float* x, int64_t B, cons
   return forward_impl(plan, x, B, out, ws, ws_bytes, stream, o);
 }
 
+jtfs_status jtfs_resynth_loss(jtfs_plan_t plan, const float* Sy, const float* Sx, double* E, float* dout,
+                              void* stream) {
+  if (!plan || !Sy || !Sx || !E || !dout) return fail(JTFS_ERR_INVALID_ARG, "NULL argument");
+  if (plan->P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");
+  DeviceGuard guard(plan->P.device);
+  jtfs_layout_t lay;
+  layout_of(plan->P, &lay);
+  jtfs::launch_resynth_loss(Sy, Sx, lay.floats_per_signal, E, dout, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
+}
+
 jtfs_status jtfs_mulog_mu(jtfs_plan_t plan, const float* S, int64_t B, float* mu, void* stream) {
   if (!plan || !S || !mu || B < 1) return fail(JTFS_ERR_INVALID_ARG, "bad argument (B must be >= 1)");
   if (plan->P.device < 0) return fail(JTFS_ERR_UNSUPPORTED, "host-only plan");

@@ -855,6 +855,36 @@ __global__ void __launch_bounds__(256) k_ke(KEParams p) {
 }
 
 // ---------------------------------------------------------------------------------
+// NEXT-1.  Resynthesis loss E = ||S y - S x|| / ||S x|| and its gradient w.r.t.
+// S y, dE/dSy = (S y - S x) / (||S y - S x|| ||S x||) (0 when S y = S x), one record: one
+// block, fp64 sums in a fixed order (fixed shared tree), then the scaled difference.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_resynth_loss(const float* __restrict__ Sy, const float* __restrict__ Sx,
+                                                      int64_t n, double* E, float* dout) {
+  __shared__ double rr[256], xx[256];
+  double a = 0.0, c = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) {
+    const double d = (double)Sy[i] - (double)Sx[i], x = (double)Sx[i];
+    a = fma(d, d, a);
+    c = fma(x, x, c);
+  }
+  rr[threadIdx.x] = a;
+  xx[threadIdx.x] = c;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      rr[threadIdx.x] += rr[threadIdx.x + h];
+      xx[threadIdx.x] += xx[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  const double nr = sqrt(rr[0]), nx = sqrt(xx[0]);
+  if (threadIdx.x == 0) *E = nx > 0.0 ? nr / nx : 0.0;
+  const double sc = (nr > 0.0 && nx > 0.0) ? 1.0 / (nr * nx) : 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) dout[i] = (float)(((double)Sy[i] - (double)Sx[i]) * sc);
+}
+
+// ---------------------------------------------------------------------------------
 // NEXT-4.  mu(lambda_2) = (1/B) sum_b sum_{lambda,t} S2_b[p] (Eq. (adalog:mu)):
 // one block per path, fp64 per-thread sums in a fixed index order, fixed shared tree.
 // ---------------------------------------------------------------------------------
@@ -1635,6 +1665,10 @@ int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st) {
 
 cudaError_t ke_set_smem(const Plan& P) {
   return cudaFuncSetAttribute(k_ke, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ke_smem_bytes(P));
+}
+
+void launch_resynth_loss(const float* Sy, const float* Sx, int64_t n, double* E, float* dout, cudaStream_t st) {
+  dev::k_resynth_loss<<<1, 256, 0, st>>>(Sy, Sx, n, E, dout);
 }
 
 int launch_mulog_mu(const Plan& P, const float* S, int64_t B, float* mu, cudaStream_t st) {

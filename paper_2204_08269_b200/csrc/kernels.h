@@ -93,6 +93,8 @@ struct BwdWs {
 };
 int launch_backward(Plan& P, const float* x, int nb, const float* dout, float* dx, const BwdWs& w,
                     cudaStream_t st);
+// NEXT-1: resynthesis loss and its gradient w.r.t. the record
+void launch_resynth_loss(const float* Sy, const float* Sx, int64_t n, double* E, float* dout, cudaStream_t st);
 // NEXT-4: mu-log (Eqs. (adalog:mu), (adalog)) and the scale-rate map (Fig. 1)
 int launch_mulog_mu(const Plan& P, const float* S, int64_t B, float* mu, cudaStream_t st);
 int launch_mulog_apply(const Plan& P, const float* S, int64_t B, const float* mu, float eps, float* out,

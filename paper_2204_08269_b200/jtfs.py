@@ -39,7 +39,7 @@ EXPORTS = [
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
     "jtfs_unitset_create", "jtfs_unitset_destroy", "jtfs_forward_unitset", "jtfs_unit_partials_range",
     "jtfs_scat1d_layout", "jtfs_scat1d_paths", "jtfs_scattering1d",
-    "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions",
+    "jtfs_backward_workspace_size", "jtfs_backward", "jtfs_backward_regions", "jtfs_resynth_loss",
     "jtfs_mulog_mu", "jtfs_mulog_apply", "jtfs_forward_mulog", "jtfs_u2_map_shape", "jtfs_u2_map",
     "jtfs_knn_workspace_size", "jtfs_knn_regress", "jtfs_isomap_workspace_size", "jtfs_isomap",
 ]
@@ -107,6 +107,7 @@ _lib.jtfs_scat1d_paths.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32]
 _lib.jtfs_scattering1d.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_backward_workspace_size.argtypes = [_P, C.c_int64, C.POINTER(C.c_size_t)]
 _lib.jtfs_backward.argtypes = [_P, _P, C.c_int64, _P, _P, _P, C.c_size_t, _P]
+_lib.jtfs_resynth_loss.argtypes = [_P, _P, _P, _P, _P, _P]
 _lib.jtfs_backward_regions.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), C.c_int32]
 _lib.jtfs_mulog_mu.argtypes = [_P, _P, C.c_int64, _P, _P]
 _lib.jtfs_mulog_apply.argtypes = [_P, _P, C.c_int64, _P, C.c_float, _P, _P]
@@ -348,6 +349,16 @@ class Plan:
         _check(_lib.jtfs_backward(self._h, _ptr(x), B, _ptr(dout), _ptr(dx), _ptr(self._bws), self._bws.numel(),
                                   _stream_handle(stream)), "jtfs_backward")
         return dx
+
+    def resynth_loss(self, Sy, Sx, stream=None):
+        """(E as a device fp64 scalar tensor, dE/dSy) for one record (jtfs_resynth_loss)."""
+        import torch
+        assert Sy.is_contiguous() and Sx.is_contiguous() and Sy.numel() == Sx.numel() == self.floats_per_signal
+        E = torch.empty((), dtype=torch.float64, device=Sy.device)
+        dout = torch.empty_like(Sy)
+        _check(_lib.jtfs_resynth_loss(self._h, _ptr(Sy), _ptr(Sx), _ptr(E), _ptr(dout), _stream_handle(stream)),
+               "jtfs_resynth_loss")
+        return E, dout
 
     def backward_regions(self, B: int):
         """Byte offsets of the backward workspace regions (jtfs_backward_regions)."""

@@ -10,15 +10,12 @@ from __future__ import annotations
 
 
 def loss_and_grad(plan, Sx, y):
-    """E(y) and dE/dy for y (CUDA float32 [1, N]), Sx the target record [1, F]."""
-    import torch
+    """E(y) and dE/dy for y (CUDA float32 [1, N]), Sx the target record [1, F]: forward,
+    the fused loss kernel (jtfs_resynth_loss: E and dE/dSy) and jtfs_backward, all in
+    libjtfs.so; E is read back for the bold driver's accept / reject decision."""
     Sy = plan.forward(y)
-    r = Sy - Sx
-    nr = torch.linalg.vector_norm(r.double())
-    nx = torch.linalg.vector_norm(Sx.double())
-    E = float((nr / nx).item())
-    dout = (r.double() / (nr * nx)).float().contiguous() if nr > 0 else torch.zeros_like(Sy)
-    return E, plan.backward(y, dout)
+    E, dout = plan.resynth_loss(Sy, Sx)
+    return float(E.item()), plan.backward(y, dout)
 
 
 def resynthesize(plan, x, y0, iters: int, mu0: float | None = None, up: float = 1.2, down: float = 0.5):

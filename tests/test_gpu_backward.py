@@ -62,25 +62,58 @@ def test_backward_matches_oracle_vjp(jt, variant):
         assert err <= 1e-4, (variant, b, err)
 
 
-def test_backward_directional_derivative_paper_setting(jt):
-    # fp64 central differences of the oracle's forward along a random direction v
+def test_backward_directional_derivatives_paper_setting(jt):
+    # fp64 central differences of the oracle's forward at the paper's resynthesis setting
+    # along four directions -- two random, a localised Gaussian bump and a
+    # sinusoid inside the band of the filterbank -- each <= 1e-3 relative
     import torch
+    from . import oracle_pool
     plan = jt.Plan(**PAPER)
-    prm = O.Params(**PAPER)
-    s = O.schedule(prm)
+    okw = {k: PAPER[k] for k in ("N", "J", "Q", "J_fr", "T", "F")}
     rng = np.random.default_rng(9)
-    X = signals.bird_texture(2 ** 16, seed=11)
-    x = torch.from_numpy(X[None, :].copy()).cuda()
+    X = signals.bird_texture(2 ** 16, seed=11).astype(np.float64)
+    x = torch.from_numpy(X.astype(np.float32)[None, :].copy()).cuda()
     D = rng.standard_normal(plan.floats_per_signal).astype(np.float32)
     dx = plan.backward(x, torch.from_numpy(D[None, :]).cuda()).cpu().numpy()[0].astype(np.float64)
-    v = rng.standard_normal(2 ** 16)
-    v *= 1e-4 * np.linalg.norm(X) / np.linalg.norm(v)
-    O.set_workers(8)
-    fp = O.pack(O.jtfs_forward(X.astype(np.float64) + v, prm, s=s)) @ D.astype(np.float64)
-    fm = O.pack(O.jtfs_forward(X.astype(np.float64) - v, prm, s=s)) @ D.astype(np.float64)
-    fd = (fp - fm) / 2.0
-    an = dx @ v
-    assert abs(an - fd) <= 1e-3 * abs(fd), (an, fd)
+    n = np.arange(2 ** 16)
+    dirs = [rng.standard_normal(2 ** 16), rng.standard_normal(2 ** 16),
+            np.exp(-0.5 * ((n - 20000) / 300.0) ** 2),
+            np.sin(2 * np.pi * 0.05 * n)]
+    futs = []
+    for v in dirs:
+        v = v * (1e-4 * np.linalg.norm(X) / np.linalg.norm(v))
+        # the oracle runs on the fp32 input promoted to fp64; perturb in fp64 (submit takes
+        # fp32 arrays, so the +-v signals are built in a float64-preserving job below)
+        futs.append((v, oracle_pool.pool().submit(_oracle_pair, okw, X, v)))
+    for v, fu in futs:
+        fp, fm = fu.result()
+        fd = (fp - fm) @ D.astype(np.float64) / 2.0
+        an = dx @ v
+        assert abs(an - fd) <= 1e-3 * abs(fd), (an, fd)
+
+
+def _oracle_pair(okw, X, v):
+    from oracle import jtfs_oracle as O
+    O.set_workers(1)
+    prm = O.Params(**okw)
+    s = O.schedule(prm)
+    return (O.pack(O.jtfs_forward(X + v, prm, s=s)), O.pack(O.jtfs_forward(X - v, prm, s=s)))
+
+
+def test_resynth_loss_kernel(jt):
+    # jtfs_resynth_loss against the definition E = ||Sy - Sx|| / ||Sx||, dE/dSy in fp64
+    import torch
+    plan = jt.Plan(**C1)
+    rng = np.random.default_rng(4)
+    Sx = torch.from_numpy(rng.standard_normal(plan.floats_per_signal).astype(np.float32)).cuda()
+    Sy = Sx + torch.from_numpy(1e-2 * rng.standard_normal(plan.floats_per_signal).astype(np.float32)).cuda()
+    E, g = plan.resynth_loss(Sy, Sx)
+    r = (Sy.double() - Sx.double()).cpu().numpy()
+    nx = np.linalg.norm(Sx.double().cpu().numpy())
+    assert abs(float(E.item()) - np.linalg.norm(r) / nx) <= 1e-12 * np.linalg.norm(r) / nx
+    np.testing.assert_allclose(g.cpu().numpy(), (r / (np.linalg.norm(r) * nx)).astype(np.float32), rtol=1e-6)
+    E0, g0 = plan.resynth_loss(Sx, Sx)
+    assert float(E0.item()) == 0.0 and torch.count_nonzero(g0).item() == 0
 
 
 def test_resynthesis_on_gpu_decreases_error(jt):
