@@ -676,11 +676,17 @@ std::string build_plan(const jtfs_params& p, Plan& P) {
   // micro-batches mean fewer launches and better-balanced KD grids).  The KD
   // partials depend on the chunking plan_tc picks for this micro-batch; they are
   // small next to Y2, so size first without them and shrink if needed.
-  const size_t ws_budget = (size_t)16 << 30;
+#ifndef JTFS_WS_GIB
+#define JTFS_WS_GIB 16
+#endif
+#ifndef JTFS_MB_CAP
+#define JTFS_MB_CAP 64
+#endif
+  const size_t ws_budget = (size_t)JTFS_WS_GIB << 30;
   P.part_total = 0;
   {
     const size_t per = ws_layout(P, 1).total;
-    P.mb = (int)std::max<size_t>(1, std::min<size_t>(64, ws_budget / std::max<size_t>(per, 1)));
+    P.mb = (int)std::max<size_t>(1, std::min<size_t>(JTFS_MB_CAP, ws_budget / std::max<size_t>(per, 1)));
   }
   if (P.kd_impl == 1) {
     const std::string e = plan_tc(P);
