@@ -55,6 +55,7 @@ typedef enum {
 #define JTFS_KD_SIMT 4u        /* KD on the FP32 SIMT validation kernel instead of tcgen05 */
 #define JTFS_POOL_EXACT 8u     /* KD epilogue with the exact phi_T taps (no cubic-moment form) */
 #define JTFS_KD_PROF 16u       /* instrumented KD: per-role wait cycles to stderr (syncs per launch) */
+#define JTFS_KD_NOPAIR 32u     /* tcgen05 KD on single CTAs only (no cta_group::2 CTA pairs) */
 
 /* pad modes (reading R6) */
 #define JTFS_PAD_REFLECT 0     /* numpy 'reflect' to N_pad = 2N, centred */

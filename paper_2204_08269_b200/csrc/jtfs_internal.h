@@ -81,6 +81,8 @@ struct AlphaKD {
   int tc_rps = 1;       // K-records per A ring stage
   int tc_stat = 0;      // 1: A stationary per CTA (its M-part's records resident), 0: A ring
   int tc_mpart = 1, tc_mblk = 1;  // M-parts of this alpha's KD and 128-pair-row M-blocks per part
+                                  // (pair: M-block pairs per part, one block per CTA)
+  int tc_pair = 0;      // 1: CTA pairs (cluster of 2, tcgen05 cta_group::2, M = 256)
   int64_t tc_a16_off = 0;   // uint16 offset of A''_alpha's 16 KiB records in A16
   int64_t tc_ainv_off = 0;  // float offset of the per-row inverse A scales in Ainv
   int64_t y16_off = 0;  // fp16 offset of Y16_alpha [K16][2L] in one signal's Y16 buffer (KY output)

@@ -133,6 +133,45 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
+// ---- CTA pairs (cluster of 2, tcgen05 cta_group::2) ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// arrive on a barrier of another CTA of the cluster.  Default (.release, .cta) semantics:
+// the only ordering needed is that of the preceding tcgen05.ld's (tcgen05.fence::
+// before_thread_sync); a .cluster-scope release costs ~1k cycles per arrive (measured: the
+// pair epilogue 1.6x slower with it)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+// tensor copies of a CTA pair completing on the LEADER's mbarrier (bar: shared::cluster address)
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2 [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2 [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 // ---- tcgen05 ----
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -144,6 +183,30 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// commit of the pair's MMAs, arriving on the same barrier in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// an epilogue warp frees an accumulator buffer: on its own barrier, or (pair) on the leader's
+template <bool PAIR>
+__device__ __forceinline__ void acc_release(uint64_t* bar) {
+  if constexpr (PAIR)
+    mbar_arrive_cluster(map_rank(bar, 0));
+  else
+    mbar_arrive(bar);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -186,10 +249,11 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return d;
 }
 
-// instruction descriptor: kind::f16, D f32, A/B fp16, A K-major, B MN-major, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+// instruction descriptor: kind::f16, D f32, A/B fp16, A K-major, B MN-major, M (128, or 256 for
+// a CTA pair), N = n
+__host__ __device__ constexpr uint32_t idesc_f16(int n, int m = 128) {
   return (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
+         ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ float sqrt_fast(float x) {
@@ -366,6 +430,8 @@ struct TcParams {
   int nsel;        // number of selected chunks
   int n_mpart, n_mblk;  // M-parts and 128-pair-row M-blocks per part
   int stat;        // 1: A stationary (the CTA's part loaded once; grid % n_mpart == 0), 0: A ring
+  // CTA pairs (PAIR kernels): n_mblk counts M-block PAIRS per part; CTA rank r of a pair owns
+  // the blocks 2 i + r (M = 256 MMAs: rows 0..127 from the leader's A, 128..255 from the peer's)
   int L, nframes, Mpp;
   int nsig;
   unsigned long long* prof;  // measurement only (JTFS_KD_PROF flag): per-role wait-cycle counters or nullptr
@@ -392,11 +458,12 @@ struct SmemLayout {
   uint32_t b[2], ast, wt, bars, total;
 };
 __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, uint32_t abytes, int nab, int NF,
-                                                  int pool_mode) {
+                                                  int pool_mode, int pair = 0) {
   SmemLayout l{};
   auto up = [](uint32_t v, uint32_t a) { return (v + a - 1) / a * a; };
   uint32_t o = 0;
-  const uint32_t bsz = (uint32_t)(K16 * 2 * Nt * 2);  // one fp16 K16 x 2Nt image ((re, im) along N)
+  // one fp16 K16 x 2Nt image ((re, im) along N); a CTA of a pair holds half of its columns
+  const uint32_t bsz = (uint32_t)(K16 * 2 * Nt * 2) >> (pair ? 1 : 0);
   for (int i = 0; i < 2; ++i) {
     if (i < NBB) {
       l.b[i] = o;
@@ -467,31 +534,40 @@ __device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2
 // unit), walked incrementally: the unit's fields (runtime divisions) once per unit.
 struct TileCursor {
   int tile, u, mpart, chunk, b;
+  int cta = -1, ncta = 0;  // work-distribution index of this CTA (pair index for CTA pairs) and count
   __device__ __forceinline__ void unit_fields(const TcParams& p) {
     mpart = u % p.n_mpart;
     const int c = (u / p.n_mpart) % p.nsel;
     chunk = p.chunk_sel ? p.chunk_sel[c] : c;
     b = u / (p.n_mpart * p.nsel);
   }
-  __device__ __forceinline__ void start(const TcParams& p) {
+  __device__ __forceinline__ void start(const TcParams& p, int cta_, int ncta_) {
+    cta = cta_;
+    ncta = ncta_;
     tile = 0;
-    u = (int)blockIdx.x;
+    u = cta;
     unit_fields(p);
   }
   __device__ __forceinline__ void next(const TcParams& p) {
     if (++tile == p.tpu) {
       tile = 0;
-      u += (int)gridDim.x;
+      u += ncta;
       unit_fields(p);
     }
   }
 };
 
 // NTC: the tile width Nt as a compile-time constant (64 / 32: the epilogue's column loops
-// unroll completely).  PROF: the instrumented variant (JTFS_KD_PROF plan flag).
-template <int NF, int MAXSLOT, bool PROF, int NTC>
+// unroll completely).  PROF: the instrumented variant (JTFS_KD_PROF plan flag).  PAIR: a
+// cluster of two CTAs runs tcgen05.mma.cta_group::2 (M = 256 = one M-block per CTA, N = 2 Nt
+// with each CTA holding half of the B tile's columns): per SM an MMA reads 4 KiB of A and
+// 2 KiB of B instead of 4 + 4, the SS-mode shared-memory port limit of the N = 128 stream
+// (tools/tc_rate2cta.cu mode 5).  The leader (rank 0) issues; both CTAs' tensor copies
+// complete on the leader's barriers; commits multicast to both CTAs; both epilogues free the
+// leader's accumulator barrier.
+template <int NF, int MAXSLOT, bool PROF, int NTC, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_kd_tc(const __grid_constant__ CUtensorMap tmB, TcParams p) {
+    k_kd_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmA, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B align by offsetting the __shared__ array itself (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
@@ -500,7 +576,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nab = p.stat ? p.n_mblk : p.S;  // A barrier pairs
   const SmemLayout lay = smem_layout(p.K16, Nt, p.NBB, p.stat ? (uint32_t)(p.n_mblk * p.nkc * kRec)
                                                               : (uint32_t)(p.S * p.rps * kRec),
-                                     nab, NF, p.pool_mode);
+                                     nab, NF, p.pool_mode, PAIR ? 1 : 0);
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int cta_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // work-distribution index
+  const int ncta = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int wfl = Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
   uint8_t* Ast = base + lay.ast;
   float* Wt = reinterpret_cast<float*>(base + lay.wt);
@@ -525,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kNbuf; ++i) {
       mbar_init(acc_full + i, 1);
-      mbar_init(acc_empty + i, 8);
+      mbar_init(acc_empty + i, PAIR ? 16 : 8);  // pair: both CTAs' epilogues free the leader's buffer
     }
     for (int i = 0; i < nab; ++i) {
       mbar_init(a_full + i, 1);
@@ -534,33 +613,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / copy
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int units = p.nsig * p.nsel * p.n_mpart;
   const int nst = (p.nkc + p.rps - 1) / p.rps;  // A'' stages (<= rps records of 16 K-columns) per M-block
   const uint32_t stage_bytes = (uint32_t)(p.rps * kRec);
-  // the CTA's tile sequence: unit u = blockIdx.x + i * gridDim.x, tile 0..tpu-1
-  const int my_units = (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  // the tile sequence of this CTA (pair): unit u = cta_id + i * ncta, tile 0..tpu-1
+  const int my_units = (units - cta_id + ncta - 1) / ncta;
   const int my_tiles = my_units * p.tpu;
 
   if (warp == kBWarp) {
     // ===================== B producer: the packed fp16 tile + pooling table =====================
     // one copy per lane (copies issued by one thread complete one after another):
     // lane 0 the table, lanes 1.. the TMA boxes (64-column groups x row boxes)
-    constexpr int ncg = 2 * Nt / 64;
+    constexpr int ncg = PAIR ? 1 : 2 * Nt / 64;  // pair: this CTA's half = one 64-column group
     const int nboxes = ncg * p.nbr;
-    const uint32_t btx = (uint32_t)(p.K16 * 2 * Nt * 2);
+    const uint32_t btx = (uint32_t)(p.K16 * 2 * Nt * 2);  // the whole tile (pair: both halves, leader)
     const int wcol = p.pool_mode ? NF / 8 : NF;  // table floats per time column
     const uint32_t wbytes = (uint32_t)(Nt * wcol * 4);
     TileCursor cur;
-    cur.start(p);
+    cur.start(p, cta_id, ncta);
     for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
       const int chunk = cur.chunk, b = cur.b;
       const int t0 = (chunk * p.tpu + cur.tile) * Nt;
@@ -570,13 +656,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(w_full + wi, wbytes);
         bulk_load(Wt + wi * wfl, p.wtab + (size_t)t0 * wcol, wbytes, w_full + wi);
         mbar_wait(b_empty + bi, (uint32_t)((gt / p.NBB) + 1) & 1u);
-        mbar_expect_tx(b_full + bi, btx);
+        if (rank == 0) mbar_expect_tx(b_full + bi, btx);
       }
       __syncwarp();
       for (int i = lane - 1; i >= 0 && i < nboxes; i += 31) {
         const int cg = i / p.nbr, rb = i % p.nbr;
         uint8_t* dst = base + lay.b[bi] + cg * (p.K16 * 128) + rb * (p.BRk * 128);
-        tma_load_3d(dst, &tmB, b_full + bi, 2 * t0 + cg * 64, rb * p.BRk, b);
+        if constexpr (PAIR)
+          tma_load_3d_pair(dst, &tmB, map_rank(b_full + bi, 0), 2 * t0 + 64 * (int)rank, rb * p.BRk, b);
+        else
+          tma_load_3d(dst, &tmB, b_full + bi, 2 * t0 + cg * 64, rb * p.BRk, b);
       }
     }
   } else if (warp == kProdWarp) {
@@ -597,17 +686,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       // parallel; a slot is always served by the same lane: unambiguous parity waits)
       uint32_t s = 0, ph = 0;
       TileCursor cur;
-      cur.start(p);
+      cur.start(p, cta_id, ncta);
       for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
         const int mpart = cur.mpart;
         for (int mb = 0; mb < p.n_mblk; ++mb) {
-          const uint16_t* arec = p.A + (size_t)(mpart * p.n_mblk + mb) * p.nkc * (kRec / 2);
+          const int blk = PAIR ? (mpart * p.n_mblk + mb) * 2 + (int)rank : mpart * p.n_mblk + mb;
+          const uint16_t* arec = p.A + (size_t)blk * p.nkc * (kRec / 2);
           for (int st = 0; st < nst; ++st) {
             if ((int)s == lane) {
               mbar_wait(a_empty + s, ph ^ 1);
-              const uint32_t bytes = (uint32_t)(min(p.rps, p.nkc - p.rps * st) * kRec);
-              mbar_expect_tx(a_full + s, bytes);
-              bulk_load(Ast + s * stage_bytes, arec + (size_t)(p.rps * st) * (kRec / 2), bytes, a_full + s);
+              if constexpr (PAIR) {
+                // full-stage boxes (rps records; a short last stage reads past its block, unused)
+                // of this CTA's block, completing on the leader's barrier (expect: both CTAs)
+                if (rank == 0) mbar_expect_tx(a_full + s, 2u * stage_bytes);
+                tma_load_2d_pair(Ast + s * stage_bytes, &tmA, map_rank(a_full + s, 0), 0,
+                                 (blk * p.nkc + p.rps * st) * 8);
+              } else {
+                const uint32_t bytes = (uint32_t)(min(p.rps, p.nkc - p.rps * st) * kRec);
+                mbar_expect_tx(a_full + s, bytes);
+                bulk_load(Ast + s * stage_bytes, arec + (size_t)(p.rps * st) * (kRec / 2), bytes, a_full + s);
+              }
             }
             if (++s == (uint32_t)p.S) {
               s = 0;
@@ -617,13 +715,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaWarp && (!PAIR || rank == 0)) {
     // ===================== MMA issuer (warp-wide loop, one elected lane issues) =====================
     // per M-block and 16-wide K chunk: acc1 += Re A'' . B, acc2 += Im A'' . B (N = 2 Nt)
+    // (pair: the leader issues M = 256 for both CTAs' M-blocks; the peer's MMA warp idles)
     uint32_t s = 0, ph = 0, cnt = 0;
     long long w_b = 0, w_acc = 0, w_a = 0;
     const long long t_start = clk<PROF>();
-    const uint32_t idesc = idesc_f16(2 * Nt);
+    const uint32_t idesc = idesc_f16(2 * Nt, PAIR ? 256 : 128);
     const uint32_t colstride = (uint32_t)(p.K16 * 128);
     const uint64_t dA0 = sdesc(smem_u32(Ast), 16, 256, kLayoutSW32);
     for (int gt = 0; gt < my_tiles; ++gt) {
@@ -664,11 +763,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const uint64_t a = dst + (uint64_t)((r * kRec) >> 4);
                   const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
                   const uint32_t acc0 = kc > 0 ? 1u : 0u;
-                  mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
-                  mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
+                  if constexpr (PAIR) {
+                    mma_f16_pair(d1, a, dB + yo, idesc, acc0);
+                    mma_f16_pair(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);
+                  } else {
+                    mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
+                    mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
+                  }
                 }
               }
-              mma_commit(a_empty + s);
+              if constexpr (PAIR)
+                mma_commit_pair(a_empty + s);
+              else
+                mma_commit(a_empty + s);
             }
             __syncwarp();
             if (++s == (uint32_t)p.S) {
@@ -677,10 +784,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (elect_one()) mma_commit(acc_full + ab);
+        if (elect_one()) {
+          if constexpr (PAIR)
+            mma_commit_pair(acc_full + ab);
+          else
+            mma_commit(acc_full + ab);
+        }
         __syncwarp();
       }
-      if (elect_one()) mma_commit(b_empty + bi);
+      if (elect_one()) {
+        if constexpr (PAIR)
+          mma_commit_pair(b_empty + bi);
+        else
+          mma_commit(b_empty + bi);
+      }
       __syncwarp();
     }
     if (PROF && p.prof && lane == 0) {
@@ -689,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       atomicAdd(p.prof + 2, (unsigned long long)w_acc);
       atomicAdd(p.prof + 3, (unsigned long long)w_a);
     }
-  } else {
+  } else if (warp < kMmaWarp) {
     // ===================== epilogue (warps 0..7) =====================
     const int eset = warp >> 2;  // column half
     const int q = warp & 3;      // TMEM lane quarter (warp_id % 4)
@@ -700,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t cnt = 0;
     float2 accm[MAXSLOT][NF / 2], accp[MAXSLOT][NF / 2];  // pooled partials of both spins of my pair rows
     TileCursor cur;
-    cur.start(p);
+    cur.start(p, cta_id, ncta);
     for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
       const int mpart = cur.mpart, chunk = cur.chunk, b = cur.b, tile = cur.tile;
       if (tile == 0) {
@@ -736,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(acc_empty + ab);  // accumulator buffer read: back to the MMA
+          if (lane == 0) acc_release<PAIR>(acc_empty + ab);  // accumulator buffer read: back to the MMA
           const float4* g4 = reinterpret_cast<const float4*>(Wt + wi * wfl + (cbeg / 32) * 4 * NF);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -757,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(acc_empty + ab);
+          if (lane == 0) acc_release<PAIR>(acc_empty + ab);
         }
         e_math += clk<PROF>() - tm0;
         // warp-uniform branch to the M-block's slot (a predicated loop over all
@@ -787,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k) {
           if (k < p.n_mblk) {
-            const int row = (mpart * p.n_mblk + k) * 128 + q * 32 + lane;
+            const int row = (PAIR ? (mpart * p.n_mblk + k) * 2 + (int)rank : mpart * p.n_mblk + k) * 128 + q * 32 + lane;
             const float ia = __ldg(p.ainv + row);
             float* d0 = dst + (int64_t)row * p.nframes;
             float* d1 = dst + (int64_t)(p.Mpp + row) * p.nframes;
@@ -815,9 +932,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no remote arrive / MMA into the peer is still in flight
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
@@ -856,7 +977,9 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, void* base, int rank, const 
 int nf_of(int nframes) { return nframes <= 8 ? 8 : nframes <= 16 ? 16 : 32; }
 size_t tc_smem(const AlphaKD& d, int nf) {
   const uint32_t abytes = d.tc_stat ? (uint32_t)(d.tc_mblk * d.tc_nkc * tc::kRec) : (uint32_t)(d.tc_S * d.tc_rps * tc::kRec);
-  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, abytes, d.tc_stat ? d.tc_mblk : d.tc_S, nf, d.pool_mode).total;
+  return tc::smem_layout(d.tc_K16, d.tc_Nt, d.tc_NBB, abytes, d.tc_stat ? d.tc_mblk : d.tc_S, nf, d.pool_mode,
+                         d.tc_pair)
+      .total;
 }
 }  // namespace
 
@@ -930,10 +1053,31 @@ std::string plan_tc(Plan& P) {
     if (!ok) {
       d.tc_mpart = P.tc_n_mpart;
       d.tc_mblk = P.tc_n_mblk;
+      d.tc_pair = 0;
       ok = choose();
       if (ok && d.pool_mode && d.tc_Nt != 64) {
         d.pool_mode = 0;
         ok = choose();
+      }
+      // CTA pairs (cta_group::2): the ring alphas whose M-blocks split into pairs with
+      // <= MAXSLOT blocks per CTA and an Nt = 64 tile (half of its B columns per CTA).
+      // Not where the A'' ring's L2 stream bounds the single-CTA kernel (10..15 K-chunks:
+      // measured on c3, tools/pair_check.py, 64 signals: alpha 2 / 3 (nkc 10 / 13) 1.78 ->
+      // 2.13 / 1.28 -> 1.33 ms with pairs, as each SM still streams 8 KiB of A'' per two
+      // MMAs, ~40 B/cycle/SM at the chip's L2 limit, and the pair adds the coupling of two
+      // streams; alpha 1 (nkc 7) 2.92 -> 2.65 and alpha 4-6 (nkc 16-22, where the single CTA
+      // fits one B buffer or few A stages) 1.47 -> 1.30 ms gain)
+      const int nblocks = P.Mpp / 128, maxslot = NF == 8 ? 5 : NF == 16 ? 2 : 1;
+      const bool a_stream_bound = d.tc_nkc >= 10 && d.tc_nkc < 16;
+      if (ok && !(P.prm.flags & JTFS_KD_NOPAIR) && !a_stream_bound && d.tc_Nt == 64 && nblocks % 2 == 0) {
+        const AlphaKD keep = d;
+        const int npair = nblocks / 2;
+        int np = (npair + maxslot - 1) / maxslot;
+        while (npair % np) ++np;
+        d.tc_pair = 1;
+        d.tc_mpart = np;
+        d.tc_mblk = npair / np;
+        if (!choose() || d.tc_Nt != 64) d = keep;
       }
     }
     if (!ok) return "tensor-core KD: no tile of alpha " + std::to_string(d.alpha) + " fits shared memory";
@@ -941,7 +1085,7 @@ std::string plan_tc(Plan& P) {
     // about 4 units per SM for a full micro-batch (partials are per chunk; measured on
     // c3, round 1: 4096 / 8192 / 16384-column chunks equal within noise)
     const int64_t sig = (P.prm.flags & JTFS_LATENCY) ? 1 : P.mb;  // signals per KD launch
-    const int64_t target = sig * d.tc_mpart * d.L / (4 * 148);
+    const int64_t target = sig * d.tc_mpart * d.L / (4 * (d.tc_pair ? 74 : 148));  // units per SM (pair)
     int ch = 4096;
     while (ch > d.tc_Nt && ch > target) ch /= 2;  // (JTFS_LATENCY: one signal per launch)
     d.chunk = std::min(ch, d.L);
@@ -981,8 +1125,9 @@ cudaError_t tc_setup_device(Plan& P) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
   };
 #define JTFS_SET_KD(NF_, MS_)                                                                      \
-  set(tc::k_kd_tc<NF_, MS_, false, 64>); set(tc::k_kd_tc<NF_, MS_, false, 32>);                    \
-  set(tc::k_kd_tc<NF_, MS_, true, 64>); set(tc::k_kd_tc<NF_, MS_, true, 32>);
+  set(tc::k_kd_tc<NF_, MS_, false, 64, false>); set(tc::k_kd_tc<NF_, MS_, false, 32, false>);      \
+  set(tc::k_kd_tc<NF_, MS_, true, 64, false>); set(tc::k_kd_tc<NF_, MS_, true, 32, false>);        \
+  set(tc::k_kd_tc<NF_, MS_, false, 64, true>); set(tc::k_kd_tc<NF_, MS_, true, 64, true>);
   if (NF == 8) { JTFS_SET_KD(8, 5) }
   else if (NF == 16) { JTFS_SET_KD(16, 2) }
   else { JTFS_SET_KD(32, 1) }
@@ -1049,6 +1194,22 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       *err = 1;
       break;  // the join below still orders the side stream before the caller's
     }
+    // pair: A'' records as rows of 1 KiB (8 rows per record), one box = one ring stage,
+    // copied verbatim (the records are pre-swizzled); a short last stage reads past the
+    // alpha's records (zero fill) or into the next block's (never multiplied)
+    CUtensorMap tmA;
+    std::memset(&tmA, 0, sizeof(tmA));
+    if (d.tc_pair) {
+      const int64_t nrec = (int64_t)(P.Mpp / 128) * d.tc_nkc;
+      cuuint64_t adims[2] = {256, (cuuint64_t)(nrec * 8)};
+      cuuint64_t astr[1] = {1024};
+      cuuint32_t abox[2] = {256, (cuuint32_t)(8 * d.tc_rps)};
+      if (!encode(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT32, const_cast<uint16_t*>(P.d_A16 + d.tc_a16_off), 2, adims, astr,
+                  abox, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+        *err = 1;
+        break;
+      }
+    }
     tc::TcParams p{};
     p.K16 = d.tc_K16;
     p.nkc = d.tc_nkc;
@@ -1085,8 +1246,9 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
     p.part_stride = P.part_total;
     const int units = nsig * nsel * d.tc_mpart;
     // stationary A: a multiple of n_mpart CTAs, so CTA b always gets M-part b % n_mpart
-    const int grid = d.tc_stat ? std::max(d.tc_mpart, std::min(units, sms) / d.tc_mpart * d.tc_mpart)
-                               : std::min(units, sms);
+    const int grid = d.tc_stat   ? std::max(d.tc_mpart, std::min(units, sms) / d.tc_mpart * d.tc_mpart)
+                     : d.tc_pair ? 2 * std::min(units, sms / 2)
+                                 : std::min(units, sms);
     const size_t sm = tc_smem(d, NF);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (P.prof) {
@@ -1096,10 +1258,26 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       cudaEventRecord(e0, st);
       P.prof_kd[i].push_back({(void*)e0, (void*)e1});
     }
-    auto go = [&](auto kern) { kern<<<grid, tc::kThreads, sm, st>>>(tmB, p); };
+    auto go = [&](auto kern) { kern<<<grid, tc::kThreads, sm, st>>>(tmB, tmA, p); };
+    auto go_pair = [&](auto kern) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(tc::kThreads);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kern, tmB, tmA, p);
+    };
 #define JTFS_GO_KD(NF_, MS_)                                                                        \
-  if (d.tc_Nt == 64) { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 64>); else go(tc::k_kd_tc<NF_, MS_, false, 64>); } \
-  else { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 32>); else go(tc::k_kd_tc<NF_, MS_, false, 32>); }
+  if (d.tc_pair) { if (do_prof) go_pair(tc::k_kd_tc<NF_, MS_, true, 64, true>); else go_pair(tc::k_kd_tc<NF_, MS_, false, 64, true>); } \
+  else if (d.tc_Nt == 64) { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 64, false>); else go(tc::k_kd_tc<NF_, MS_, false, 64, false>); } \
+  else { if (do_prof) go(tc::k_kd_tc<NF_, MS_, true, 32, false>); else go(tc::k_kd_tc<NF_, MS_, false, 32, false>); }
     if (NF == 8) { JTFS_GO_KD(8, 5) }
     else if (NF == 16) { JTFS_GO_KD(16, 2) }
     else { JTFS_GO_KD(32, 1) }
@@ -1112,9 +1290,9 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       cudaStreamSynchronize(st);
       const double nm = (double)grid, ne = (double)grid * 8;
       std::fprintf(stderr,
-                   "KDPROF alpha %zu Nt %d NBB %d S %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
+                   "KDPROF alpha %zu pair %d nkc %d mblk %d Nt %d NBB %d S %d rps %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
                    "epi: total %.0f wait_w %.0f wait_acc %.0f math %.0f (kcycles/CTA)\n",
-                   i, d.tc_Nt, d.tc_NBB, d.tc_S, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
+                   i, d.tc_pair, d.tc_nkc, d.tc_mblk, d.tc_Nt, d.tc_NBB, d.tc_S, d.tc_rps, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
                    h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3);
     }
   }

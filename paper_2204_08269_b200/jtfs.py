@@ -26,7 +26,7 @@ JTFS_OK, JTFS_ERR_INVALID_ARG, JTFS_ERR_UNSUPPORTED, JTFS_ERR_OOM = 0, 1, 2, 3
 JTFS_ERR_CUDA, JTFS_ERR_WORKSPACE, JTFS_ERR_NONFINITE = 4, 5, 6
 JTFS_CHECK_FINITE = 1
 JTFS_LATENCY = 2
-JTFS_KD_SIMT, JTFS_POOL_EXACT, JTFS_KD_PROF = 4, 8, 16   # validation / measurement plan flags
+JTFS_KD_SIMT, JTFS_POOL_EXACT, JTFS_KD_PROF, JTFS_KD_NOPAIR = 4, 8, 16, 32  # validation / measurement plan flags
 JTFS_PAD_REFLECT, JTFS_PAD_PERIODIC = 0, 1
 PATH_SPIN, PATH_PSI_T_PHI_F, PATH_PHI_T_PSI_F, PATH_PHI_T_PHI_F = 0, 1, 2, 3
 

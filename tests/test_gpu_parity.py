@@ -162,6 +162,21 @@ def test_kd_tensor_core_matches_simt(jt, kw):
         assert np.linalg.norm(a[i] - b[i]) <= 1e-5 * np.linalg.norm(a[i])
 
 
+@pytest.mark.parametrize("kw", [dict(N=2 ** 13, J=8, Q=16, J_fr=4, T=2 ** 13, F=16, average_fr=False),
+                                dict(N=2 ** 16, J=12, Q=16, J_fr=5, T=2 ** 13, F=4)], ids=["c2", "c3"])
+def test_kd_cta_pairs_match_single_ctas(jt, kw):
+    # the cta_group::2 KD (CTA pairs, M = 256) against the single-CTA KD (plan flag
+    # JTFS_KD_NOPAIR): same fp16 operands and per-row K order, so equal up to the order of
+    # the epilogue's fp32 sums (in practice bit-identical)
+    import torch
+    X = signals.notes(5, N=kw["N"], seed0=313)
+    x = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    a = jt.Plan(**kw, flags=jt.JTFS_KD_NOPAIR).forward(x).cpu().numpy().astype(np.float64)
+    b = jt.Plan(**kw).forward(x).cpu().numpy().astype(np.float64)
+    for i in range(len(X)):
+        assert np.linalg.norm(a[i] - b[i]) <= 1e-6 * np.linalg.norm(a[i])
+
+
 def test_determinism_and_batch_independence(jt):
     import torch
     X = np.concatenate([_c1_inputs(), signals.white(37, 2 ** 10, seed=9)])
