@@ -406,6 +406,14 @@ JTFS_API jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir
                            const void* in, void* out, int64_t rows, void* tmp, size_t tmp_bytes,
                            void* stream);
 
+/* Density of the KD's tensor-core operand A''_alpha (VERDICT r1 "measure A's
+ * density"): per active alpha a, { records (128 pair rows x 16 packed
+ * K-columns), records holding an entry > thr x its row's largest coefficient, records in
+ * the per-M-block band [first, last] such record, K-chunks per M-block, coefficients
+ * A_alpha[p][lambda] > thr x row max, coefficients (pair rows x K) }: out[6a..6a+5].
+ * Host only (works on a host plan, device < 0); cap >= 6 x n_alpha. */
+JTFS_API jtfs_status jtfs_debug_a16_density(jtfs_plan_t plan, double thr, int64_t* out, int32_t cap);
+
 /* Host copy of a sampled filter spectrum as the plan generated it (fp64), for
  * cross-checking the plan generator against the oracle's independent one.
  *   bank 1: psi_lambda, 2: psi_alpha, 3: psi_beta (theta=-1), 4: phi_T, 5: phi_F

@@ -1181,6 +1181,15 @@ jtfs_status jtfs_debug_joint(jtfs_plan_t plan, const float* y2, const float* yph
   return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
 }
 
+jtfs_status jtfs_debug_a16_density(jtfs_plan_t plan, double thr, int64_t* out, int32_t cap) {
+  if (!plan || !out || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  std::vector<int64_t> v;
+  jtfs::a16_density(plan->P, thr, v);
+  if ((size_t)cap < v.size()) return fail(JTFS_ERR_INVALID_ARG, "cap < 6 x n_alpha");
+  std::copy(v.begin(), v.end(), out);
+  return JTFS_OK;
+}
+
 jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir, int32_t fp64, const void* in, void* out,
                            int64_t rows, void* tmp, size_t tmp_bytes, void* stream) {
   if (!plan) return fail(JTFS_ERR_INVALID_ARG, "plan is NULL");

@@ -196,6 +196,7 @@ struct Plan {
 
 // plan.cpp
 std::string build_plan(const jtfs_params& p, Plan& plan);   // returns "" or an error message
+void a16_density(const Plan& P, double thr, std::vector<int64_t>& out);  // 6 values per alpha
 int ilog2_exact(int64_t v);  // -1 if not a power of two
 
 // workspace guard bands (validation builds: -DJTFS_WS_GUARDS, abi.cu checks them after

@@ -184,6 +184,49 @@ static double pool_tap(const Plan& P, const AlphaKD& d, int m, int64_t t) {
   return (double)P.g[d.g_off + i];
 }
 
+// Density of the tensor-core operand A''_alpha (measurement, jtfs_debug_a16_density): per
+// alpha, the 8 KiB records (128 pair rows x 16 packed K-columns x {Re, Im}) and how many hold
+// an entry above thr relative to its row's scale (rows are scaled to a maximum in [2^13,
+// 2^14), so |fp16| > thr 2^13 is "above thr of the row's largest coefficient").
+void a16_density(const Plan& P, double thr, std::vector<int64_t>& out) {
+  out.clear();
+  for (const auto& d : P.kd) {
+    const int nkc = (3 * d.K + 15) / 16, nblk = P.Mpp / 128;
+    int64_t live = 0, band = 0;
+    for (int mb = 0; mb < nblk; ++mb) {
+      int lo = nkc, hi = -1;
+      for (int kc = 0; kc < nkc; ++kc) {
+        const uint16_t* r = P.A16.data() + d.tc_a16_off + ((size_t)mb * nkc + kc) * 4096;
+        double mx = 0;
+        for (int i = 0; i < 4096; ++i) mx = std::max(mx, std::abs(half_to_double(r[i])));
+        if (mx > thr * 8192.0) {
+          ++live;
+          lo = std::min(lo, kc);
+          hi = kc;
+        }
+      }
+      if (hi >= lo) band += hi - lo + 1;
+    }
+    // entry level: coefficients A_alpha[p][lambda] (the hi copy, packed columns 0..K-1) above thr
+    int64_t ent = 0;
+    for (int m = 0; m < P.Mpp; ++m)
+      for (int lam = 0; lam < d.K; ++lam) {
+        const int mb = m / 128, r = m % 128, kc = lam / 16, kk = lam % 16;
+        const uint32_t o = (uint32_t)((r / 8) * 256 + (r % 8) * 32 + kk * 2);
+        const uint32_t sw = o ^ (((o >> 7) & 1u) << 4);
+        const uint16_t* rec = P.A16.data() + d.tc_a16_off + ((size_t)mb * nkc + kc) * 4096;
+        const double a = std::max(std::abs(half_to_double(rec[sw / 2])), std::abs(half_to_double(rec[2048 + sw / 2])));
+        if (a > thr * 8192.0) ++ent;
+      }
+    out.push_back((int64_t)nblk * nkc);
+    out.push_back(live);
+    out.push_back(band);
+    out.push_back(nkc);
+    out.push_back(ent);
+    out.push_back((int64_t)P.Mpp_rows * d.K);
+  }
+}
+
 std::string build_plan(const jtfs_params& p, Plan& P) {
   P.prm = p;
   std::vector<std::vector<float>> mom_tabs;  // per alpha: moment-form pooling table (if eligible)

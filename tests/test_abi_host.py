@@ -173,3 +173,18 @@ def test_every_benchmarked_config_plans_on_the_tensor_cores(jt, name):
     assert p.floats_per_signal > 0
     q = hostplan(jt, **CFGS[name], flags=jt.JTFS_KD_SIMT)
     assert q.floats_per_signal == p.floats_per_signal
+
+
+def test_a16_density_bookkeeping(jt):
+    # jtfs_debug_a16_density on a host plan: per alpha the record / coefficient counts are
+    # consistent, thresholds are monotone, and at thr = 0 every row's largest coefficient
+    # (scaled into [2^13, 2^14)) makes its record live
+    p = hostplan(jt, **CFGS["c1"])
+    lay = p.layout
+    d0, d1 = p.a16_density(0.0), p.a16_density(1e-3)
+    assert len(d0) == lay.n_alpha
+    for (tot, live, band, nkc, ent, coef), (tot1, live1, band1, _, ent1, coef1) in zip(d0, d1):
+        assert tot == tot1 and coef == coef1 and tot % nkc == 0
+        assert 0 < live <= band <= tot and 0 < ent <= coef
+        assert live1 <= live and band1 <= band and ent1 <= ent
+        assert live >= tot // nkc  # at least one live record per M-block
