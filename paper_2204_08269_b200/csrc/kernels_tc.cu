@@ -455,7 +455,7 @@ constexpr int kNbuf = 2;  // TMEM accumulator buffers, each [acc1 | acc2] of 2 x
 // M-part when A is stationary), the pooling table buffers, the barriers (nab A barrier
 // pairs: S ring slots or n_mblk stationary blocks)
 struct SmemLayout {
-  uint32_t b[2], ast, wt, bars, total;
+  uint32_t b[4], ast, wt, bars, total;
 };
 __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, uint32_t abytes, int nab, int NF,
                                                   int pool_mode, int pair = 0) {
@@ -464,7 +464,7 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, uint
   uint32_t o = 0;
   // one fp16 K16 x 2Nt image ((re, im) along N); a CTA of a pair holds half of its columns
   const uint32_t bsz = (uint32_t)(K16 * 2 * Nt * 2) >> (pair ? 1 : 0);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 4; ++i) {
     if (i < NBB) {
       l.b[i] = o;
       o = up(o + bsz, 1024);
@@ -475,9 +475,9 @@ __host__ __device__ inline SmemLayout smem_layout(int K16, int Nt, int NBB, uint
   l.ast = o;
   o += abytes;
   l.wt = o;  // [2][Nt][NF] taps, or [2][Nt / 32][4][NF] moment coefficients
-  o += (uint32_t)(2 * Nt * (pool_mode ? NF / 8 : NF) * 4);
+  o += (uint32_t)((NBB < 2 ? 2 : NBB) * Nt * (pool_mode ? NF / 8 : NF) * 4);  // max(2, NBB) table buffers
   l.bars = up(o, 8);
-  o = l.bars + 8 * (4 + 4 + 2 * kNbuf + 2 * nab) + 16;
+  o = l.bars + 8 * (16 + 2 * kNbuf + 2 * nab) + 16;
   l.total = o + 1024;  // + alignment slack of the dynamic smem base
   return l;
 }
@@ -581,22 +581,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cta_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // work-distribution index
   const int ncta = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int wfl = Nt * (p.pool_mode ? NF / 8 : NF);  // taps / coefficients floats per buffer
+  const int nwb = p.NBB < 2 ? 2 : p.NBB;             // table buffers (the producer runs NBB tiles ahead)
   uint8_t* Ast = base + lay.ast;
   float* Wt = reinterpret_cast<float*>(base + lay.wt);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + lay.bars);
-  uint64_t* b_full = bars + 0;      // [2] B tile landed
-  uint64_t* b_empty = bars + 2;     // [2] MMA done with the B tile
-  uint64_t* w_full = bars + 4;      // [2] taps landed
-  uint64_t* w_empty = bars + 6;     // [2] epilogue done with the taps
-  uint64_t* acc_full = bars + 8;    // [kNbuf]
-  uint64_t* acc_empty = bars + 8 + kNbuf;
-  uint64_t* a_full = bars + 8 + 2 * kNbuf;  // [nab]
+  uint64_t* b_full = bars + 0;      // [NBB <= 4] B tile landed
+  uint64_t* b_empty = bars + 4;     // [NBB] MMA done with the B tile
+  uint64_t* w_full = bars + 8;      // [nwb] taps landed
+  uint64_t* w_empty = bars + 12;    // [nwb] epilogue done with the taps
+  uint64_t* acc_full = bars + 16;   // [kNbuf]
+  uint64_t* acc_empty = bars + 16 + kNbuf;
+  uint64_t* a_full = bars + 16 + 2 * kNbuf;  // [nab]
   uint64_t* a_empty = a_full + nab;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + nab);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(b_full + i, 1);
       mbar_init(b_empty + i, 1);
       mbar_init(w_full + i, 1);
@@ -650,9 +651,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
       const int chunk = cur.chunk, b = cur.b;
       const int t0 = (chunk * p.tpu + cur.tile) * Nt;
-      const int wi = gt & 1, bi = gt % p.NBB;
+      const int wi = gt % nwb, bi = gt % p.NBB;
       if (lane == 0) {
-        mbar_wait(w_empty + wi, (uint32_t)((gt >> 1) + 1) & 1u);
+        mbar_wait(w_empty + wi, (uint32_t)((gt / nwb) + 1) & 1u);
         mbar_expect_tx(w_full + wi, wbytes);
         bulk_load(Wt + wi * wfl, p.wtab + (size_t)t0 * wcol, wbytes, w_full + wi);
         mbar_wait(b_empty + bi, (uint32_t)((gt / p.NBB) + 1) & 1u);
@@ -671,14 +672,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kProdWarp) {
     // ===================== A producer =====================
     if (p.stat) {
-      // stationary: the CTA always works on M-part blockIdx % n_mpart (grid % n_mpart == 0);
-      // lane mb copies M-block mb's nkc records once, for the whole launch
-      const int mpart = (int)blockIdx.x % p.n_mpart;
+      // stationary: the CTA (pair) always works on M-part cta_id % n_mpart (the grid's CTA
+      // (pair) count is a multiple of n_mpart); lane mb copies M-block mb's nkc records once,
+      // for the whole launch (pair: this CTA's block of pair mb, one tensor copy completing on
+      // the leader's barrier, which expects both CTAs' bytes)
+      const int mpart = cta_id % p.n_mpart;
       if (lane < p.n_mblk) {
         const uint32_t bytes = (uint32_t)(p.nkc * kRec);
-        mbar_expect_tx(a_full + lane, bytes);
-        bulk_load(Ast + (size_t)lane * bytes, p.A + (size_t)(mpart * p.n_mblk + lane) * p.nkc * (kRec / 2), bytes,
-                  a_full + lane);
+        if constexpr (PAIR) {
+          const int blk = (mpart * p.n_mblk + lane) * 2 + (int)rank;
+          if (rank == 0) mbar_expect_tx(a_full + lane, 2u * bytes);
+          tma_load_2d_pair(Ast + (size_t)lane * bytes, &tmA, map_rank(a_full + lane, 0), 0, blk * p.nkc * 8);
+        } else {
+          mbar_expect_tx(a_full + lane, bytes);
+          bulk_load(Ast + (size_t)lane * bytes, p.A + (size_t)(mpart * p.n_mblk + lane) * p.nkc * (kRec / 2), bytes,
+                    a_full + lane);
+        }
       }
     } else if (lane < p.S) {
       // ring: bulk copies issued by one thread complete one after another (~600 cycles
@@ -745,8 +754,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t a = a0 + (uint64_t)((kc * kRec) >> 4);
               const uint64_t yo = (uint64_t)((kc * 2048) >> 4);  // 16 K-rows x 128 B
               const uint32_t acc0 = kc > 0 ? 1u : 0u;
-              mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
-              mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
+              if constexpr (PAIR) {
+                mma_f16_pair(d1, a, dB + yo, idesc, acc0);
+                mma_f16_pair(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);
+              } else {
+                mma_f16(d1, a, dB + yo, idesc, acc0);                         // Re A'' . B
+                mma_f16(d2, a + (uint64_t)(kImg >> 4), dB + yo, idesc, acc0);  // Im A'' . B
+              }
             }
           }
           __syncwarp();
@@ -818,17 +832,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     float2 accm[MAXSLOT][NF / 2], accp[MAXSLOT][NF / 2];  // pooled partials of both spins of my pair rows
     TileCursor cur;
     cur.start(p, cta_id, ncta);
+    float inv = 0.f;  // 1 / s_Y of the unit's signal (loaded once per unit, off the per-tile path)
     for (int gt = 0; gt < my_tiles; ++gt, cur.next(p)) {
       const int mpart = cur.mpart, chunk = cur.chunk, b = cur.b, tile = cur.tile;
       if (tile == 0) {
+        inv = __ldg(p.ys + (int64_t)b * p.ys_stride);
 #pragma unroll
         for (int k = 0; k < MAXSLOT; ++k)
 #pragma unroll
           for (int m = 0; m < NF / 2; ++m) accm[k][m] = accp[k][m] = make_float2(0.f, 0.f);
       }
-      const int wi = gt & 1;
-      mbar_wait_t<PROF>(w_full + wi, (uint32_t)(gt >> 1) & 1u, e_w);
-      const float inv = __ldg(p.ys + (int64_t)b * p.ys_stride);
+      const int wi = gt % nwb;
+      mbar_wait_t<PROF>(w_full + wi, (uint32_t)(gt / nwb) & 1u, e_w);
       const float* wt = Wt + wi * wfl + cbeg * NF;
 #pragma unroll 1
       for (int mb = 0; mb < p.n_mblk; ++mb, ++cnt) {
@@ -1069,7 +1084,41 @@ std::string plan_tc(Plan& P) {
       // fits one B buffer or few A stages) 1.47 -> 1.30 ms gain)
       const int nblocks = P.Mpp / 128, maxslot = NF == 8 ? 5 : NF == 16 ? 2 : 1;
       const bool a_stream_bound = d.tc_nkc >= 10 && d.tc_nkc < 16;
-      if (ok && !(P.prm.flags & JTFS_KD_NOPAIR) && !a_stream_bound && d.tc_Nt == 64 && nblocks % 2 == 0) {
+      bool pair_stat = false;
+#ifndef JTFS_PAIRSTAT_ALL
+#define JTFS_PAIRSTAT_ALL 0
+#endif
+      if (ok && !(P.prm.flags & JTFS_KD_NOPAIR) && (a_stream_bound || JTFS_PAIRSTAT_ALL) && d.tc_Nt == 64 &&
+          nblocks % 2 == 0 && d.tc_nkc <= 32) {
+        // stationary pairs first: each CTA keeps its M-blocks of the pair's part resident
+        // (the A'' stream never touches L2 again; the B tile's halves are re-read once per
+        // part), the fewest parts whose blocks fit next to two B half-buffers
+        const AlphaKD keep = d;
+        const int npair = nblocks / 2;
+        for (int np = 1; np <= npair && !pair_stat; ++np) {
+          if (npair % np || npair / np > maxslot) continue;
+          d.tc_pair = 1;
+          d.tc_stat = 1;
+          d.tc_mpart = np;
+          d.tc_mblk = npair / np;
+          d.tc_Nt = 64;
+          d.tc_NBB = 2;
+          d.tc_S = 0;
+          pair_stat = tc_smem(d, NF) <= budget;
+          // a few M-blocks per CTA consume a B tile fast: up to 4 B half-buffers keep the
+          // tile copies (L2 latency) ahead of the MMAs
+          while (pair_stat && d.tc_NBB < 4) {
+            ++d.tc_NBB;
+            if (tc_smem(d, NF) > budget) {
+              --d.tc_NBB;
+              break;
+            }
+          }
+        }
+        if (!pair_stat) d = keep;
+      }
+      if (ok && !pair_stat && !(P.prm.flags & JTFS_KD_NOPAIR) && !a_stream_bound && d.tc_Nt == 64 &&
+          nblocks % 2 == 0) {
         const AlphaKD keep = d;
         const int npair = nblocks / 2;
         int np = (npair + maxslot - 1) / maxslot;
@@ -1203,7 +1252,7 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       const int64_t nrec = (int64_t)(P.Mpp / 128) * d.tc_nkc;
       cuuint64_t adims[2] = {256, (cuuint64_t)(nrec * 8)};
       cuuint64_t astr[1] = {1024};
-      cuuint32_t abox[2] = {256, (cuuint32_t)(8 * d.tc_rps)};
+      cuuint32_t abox[2] = {256, (cuuint32_t)(8 * (d.tc_stat ? d.tc_nkc : d.tc_rps))};  // stationary: one block
       if (!encode(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT32, const_cast<uint16_t*>(P.d_A16 + d.tc_a16_off), 2, adims, astr,
                   abox, CU_TENSOR_MAP_SWIZZLE_NONE)) {
         *err = 1;
@@ -1246,7 +1295,9 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
     p.part_stride = P.part_total;
     const int units = nsig * nsel * d.tc_mpart;
     // stationary A: a multiple of n_mpart CTAs, so CTA b always gets M-part b % n_mpart
-    const int grid = d.tc_stat   ? std::max(d.tc_mpart, std::min(units, sms) / d.tc_mpart * d.tc_mpart)
+    const int grid = d.tc_stat && d.tc_pair
+                         ? 2 * std::max(d.tc_mpart, std::min(units, sms / 2) / d.tc_mpart * d.tc_mpart)
+                     : d.tc_stat ? std::max(d.tc_mpart, std::min(units, sms) / d.tc_mpart * d.tc_mpart)
                      : d.tc_pair ? 2 * std::min(units, sms / 2)
                                  : std::min(units, sms);
     const size_t sm = tc_smem(d, NF);
@@ -1290,9 +1341,9 @@ int launch_kd_tc(Plan& P, const uint16_t* y16, const float* ysi, int nsig, float
       cudaStreamSynchronize(st);
       const double nm = (double)grid, ne = (double)grid * 8;
       std::fprintf(stderr,
-                   "KDPROF alpha %zu pair %d nkc %d mblk %d Nt %d NBB %d S %d rps %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
+                   "KDPROF alpha %zu pair %d stat %d nkc %d mpart %d mblk %d Nt %d NBB %d S %d rps %d | mma: total %.0f wait_b %.0f wait_acc %.0f wait_a %.0f | "
                    "epi: total %.0f wait_w %.0f wait_acc %.0f math %.0f (kcycles/CTA)\n",
-                   i, d.tc_pair, d.tc_nkc, d.tc_mblk, d.tc_Nt, d.tc_NBB, d.tc_S, d.tc_rps, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
+                   i, d.tc_pair, d.tc_stat, d.tc_nkc, d.tc_mpart, d.tc_mblk, d.tc_Nt, d.tc_NBB, d.tc_S, d.tc_rps, h[0] / nm / 1e3, h[1] / nm / 1e3, h[2] / nm / 1e3, h[3] / nm / 1e3,
                    h[4] / ne / 1e3, h[5] / ne / 1e3, h[6] / ne / 1e3, h[7] / ne / 1e3);
     }
   }
