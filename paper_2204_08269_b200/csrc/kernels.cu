@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <type_traits>
+#include <utility>
 
 #include "fft.cuh"
 #include "jtfs_internal.h"
@@ -172,6 +174,107 @@ struct ProbPlain {  // jtfs_debug_fft: contiguous complex rows in -> rows out (t
 };
 
 // ---------------------------------------------------------------------------------
+// row-bound accessors: kernels whose CTA works on one row rho (four-step passes) bind the
+// problem to that row once, so the row's parameters (FoldRow, output offsets, scales)
+// sit in registers.  Through the generic (rho, i) interface every element re-read them
+// after the previous element's global store (the compiler cannot prove the tables and
+// the outputs do not alias): one dependent L1/L2 load per stored element.
+// ---------------------------------------------------------------------------------
+template <class P>
+struct BoundRow {  // generic: forwards to (rho, i) (a copy: no address of the kernel parameter)
+  P p;
+  int rho;
+  __device__ __forceinline__ typename P::CT load(int i) const { return p.load(rho, i); }
+  __device__ __forceinline__ void store(int o, typename P::CT v) const { p.store(rho, o, v); }
+};
+template <class P>
+__device__ __forceinline__ BoundRow<P> bind_row(const P& p, int rho) {
+  return BoundRow<P>{p, rho};
+}
+
+struct BoundFold {  // ProbFold / ProbFold16 loads: the band-limited fold gather of one row
+  const float2* src;
+  FoldRow d;
+  const float* bandvals;
+  int L;
+  __device__ __forceinline__ float2 load(int i) const { return fold_value(src, d, bandvals, i, L); }
+};
+
+struct BoundFold16 : BoundFold {  // + KC's packed fp16 store
+  __half* dst;  // hi segment of the row (lo at + seg, hi again at + 2 seg)
+  int64_t seg;
+  float s;
+  __device__ __forceinline__ void store(int o, float2 v) const {
+    const float xr = v.x * s, xi = v.y * s;
+    const __half2 hi = __floats2half2_rn(xr, xi);
+    const float2 f = __half22float2(hi);
+    const __half2 lo = __floats2half2_rn(xr - f.x, xi - f.y);
+    __half* q = dst + 2 * o;
+    *reinterpret_cast<__half2*>(q) = hi;
+    *reinterpret_cast<__half2*>(q + seg) = lo;
+    *reinterpret_cast<__half2*>(q + 2 * seg) = hi;
+  }
+};
+__device__ __forceinline__ BoundFold16 bind_row(const ProbFold16& p, int rho) {
+  const int b = rho / p.nrows, r = rho % p.nrows;
+  BoundFold16 x;
+  x.src = p.src + (int64_t)b * p.src_stride;
+  x.d = p.rows[r];
+  x.bandvals = p.bandvals;
+  x.L = p.L;
+  const Y16Row y = p.y16rows[r];
+  x.dst = p.y16 + (int64_t)b * p.y16_stride + y.off;
+  x.seg = y.seg;
+  x.s = x.d.scale * __ldg(p.ysc + (int64_t)b * p.nalpha + y.aslot);
+  return x;
+}
+
+struct BoundFoldP : BoundFold {  // ProbFold: + its store (modulus + row max, or planar complex)
+  float* real_row;    // dst_real row or nullptr
+  float* planar_row;  // dst_planar row (re; im at + L) or nullptr
+  unsigned int* umax; // the row's max |U1| slot or nullptr
+  __device__ __forceinline__ void store(int o, float2 v) const {
+    if (real_row) {
+      const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * d.scale;
+      real_row[o] = u;
+      if (umax) atomicMax(umax, __float_as_uint(u));
+    } else {
+      planar_row[o] = v.x * d.scale;
+      planar_row[L + o] = v.y * d.scale;
+    }
+  }
+};
+__device__ __forceinline__ BoundFoldP bind_row(const ProbFold& p, int rho) {
+  const int b = rho / p.nrows, r = rho % p.nrows;
+  BoundFoldP x;
+  x.src = p.src + (int64_t)b * p.src_stride;
+  x.d = p.rows[r];
+  x.bandvals = p.bandvals;
+  x.L = p.L;
+  x.real_row = p.dst_real ? p.dst_real + (int64_t)b * p.dst_stride + x.d.dst_off : nullptr;
+  x.planar_row = p.dst_planar ? p.dst_planar + (int64_t)b * p.dst_stride + x.d.dst_off : nullptr;
+  x.umax = p.u1max ? p.u1max + (int64_t)b * p.n1 + x.d.pad : nullptr;
+  return x;
+}
+
+struct BoundRealFwd {  // ProbRealFwd: one real row in, its spectrum out
+  const float* in;
+  float2* out;
+  __device__ __forceinline__ float2 load(int i) const { return make_float2(in[i], 0.f); }
+  __device__ __forceinline__ void store(int o, float2 v) const { out[o] = v; }
+};
+__device__ __forceinline__ BoundRealFwd bind_row(const ProbRealFwd& p, int rho) {
+  const int b = rho / p.nrows, r = rho % p.nrows;
+  const int64_t off = (int64_t)b * p.stride + p.rows[r].dst_off;
+  return BoundRealFwd{p.u1 + off, p.u1hat + off};
+}
+// problems with a row-bound accessor of their own (the others keep the (rho, i) interface);
+// k_fft_rows stages one per row in shared memory, kBoundRowBytes each
+constexpr int kBoundRowBytes = 128;
+template <class P>
+constexpr bool kRowBound = !std::is_same<decltype(bind_row(std::declval<const P&>(), 0)), BoundRow<P>>::value;
+
+// ---------------------------------------------------------------------------------
 // single-CTA FFT of G rows per block
 // ---------------------------------------------------------------------------------
 template <int LOG2L, int G, int NT, int DIR, class P>
@@ -183,7 +286,19 @@ __global__ void __launch_bounds__(NT) k_fft_rows(P prob, int nrows, const typena
   CT* Ws = smem + G * LS;
   stage_twiddles<LOG2L, NT>(Ws, Wtab + tw_offset(LOG2L));
   const int rho0 = blockIdx.x * G;
-  if constexpr (LOG2L >= 3) {
+  if constexpr (LOG2L >= 3 && kRowBound<P>) {
+    // the G rows' bound accessors staged once in shared memory (see bind_row)
+    using BR = decltype(bind_row(prob, 0));
+    static_assert(sizeof(BR) <= kBoundRowBytes, "bound row slot");
+    BR* brs = reinterpret_cast<BR*>(Ws + L);  // after the twiddles (launch_rows adds G slots)
+    if (threadIdx.x < G && rho0 + (int)threadIdx.x < nrows) brs[threadIdx.x] = bind_row(prob, rho0 + threadIdx.x);
+    __syncthreads();
+    auto ld = [&](int g, int e) -> CT { return (rho0 + g < nrows) ? brs[g].load(e) : CxT<CT>::make(0, 0); };
+    auto st = [&](int g, int e, CT v) {
+      if (rho0 + g < nrows) brs[g].store(e, v);
+    };
+    fft_fused<LOG2L, G, NT, DIR, LS, false, true, true>(smem, Ws, ld, st);
+  } else if constexpr (LOG2L >= 3) {
     // first pass straight from global memory, last pass straight to global memory
     auto ld = [&](int g, int e) -> CT {
       return (rho0 + g < nrows) ? prob.load(rho0 + g, e) : CxT<CT>::make(0, 0);
@@ -323,7 +438,8 @@ __global__ void __launch_bounds__(NT) k_fft4_a(P prob, typename P::CT* __restric
   CT* out = tmp + (int64_t)(rho - rho0) * L;
   // column g of this block = big-row column nb0 + g; consecutive threads take
   // consecutive columns (coalesced gathers and scatters), first / last pass fused
-  auto ld = [&](int g, int na) -> CT { return prob.load(rho, na * Lb + nb0 + g); };
+  const auto br = bind_row(prob, rho);
+  auto ld = [&](int g, int na) -> CT { return br.load(na * Lb + nb0 + g); };
   auto st = [&](int g, int ka, CT v) {
     const int x = ka * (nb0 + g);
     const CT t = cmul(Wlo[x & (La - 1)], Whi[x >> LOG2A]);
@@ -350,7 +466,8 @@ __global__ void __launch_bounds__(NT) k_fft4_b(P prob, const typename P::CT* __r
   // threads) is fused with the loads; the last pass (column-major threads: consecutive
   // ka, i.e. consecutive output bins ka + La kb) with the stores
   auto ld = [&](int g, int e) -> CT { return in[(ka0 + g) * Lb + e]; };
-  auto st = [&](int g, int kb, CT v) { prob.store(rho, ka0 + g + La * kb, v); };
+  const auto br = bind_row(prob, rho);
+  auto st = [&](int g, int kb, CT v) { br.store(ka0 + g + La * kb, v); };
   fft_fused<LOG2B, G, NT, DIR, LS, true, true, true, CT, decltype(ld), decltype(st), false>(smem, Ws, ld, st);
 }
 
@@ -985,7 +1102,8 @@ void launch_rows(const P& prob, int nrows, const typename P::CT* W, int, cudaStr
   constexpr int G = rows_G<LOG2L>();
   constexpr int NT = rows_NT<LOG2L>();
   const int grid = (nrows + G - 1) / G;
-  const size_t sm = ((size_t)G * pad_row(1 << LOG2L) + (1 << LOG2L)) * sizeof(typename P::CT);
+  const size_t sm = ((size_t)G * pad_row(1 << LOG2L) + (1 << LOG2L)) * sizeof(typename P::CT) +
+                    (size_t)G * kBoundRowBytes;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_rows<LOG2L, G, NT, DIR, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
