@@ -1157,7 +1157,10 @@ cudaError_t tc_setup_device(Plan& P) {
   // The first 5 active alphas (the long, fast ones: >= 90 % of KD's work in c3) run on
   // the caller's stream, the rest on the side stream.
   {
-    const int split = 5;
+#ifndef JTFS_KD_SIDE_FROM
+#define JTFS_KD_SIDE_FROM 5
+#endif
+    const int split = JTFS_KD_SIDE_FROM;
     if (split > 0 && split < (int)P.kd.size()) {
       cudaStream_t s = nullptr;
       cudaError_t es = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
