@@ -340,22 +340,41 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
   float2* Ws = smem + G * LS;
   stage_twiddles<LOG2L, NT>(Ws, Wtab + tw_offset(LOG2L));
   const int rho0 = blockIdx.x * G;
+  // the G rows' parameters staged once in shared memory (after the twiddles; launch_u1_fused
+  // adds the slots): the fold gather, the scale, U1hat / U1 row pointers, the max slot
+  struct U1Row {
+    BoundFold fold;
+    float2* hat;
+    float* dbg;
+    unsigned int* umax;
+  };
+  static_assert(sizeof(U1Row) <= kBoundRowBytes, "u1 row slot");
+  U1Row* rr = reinterpret_cast<U1Row*>(Ws + L);
+  if (threadIdx.x < G) {
+    const int rho = min(rho0 + (int)threadIdx.x, nrows - 1);
+    const int b = rho / prob.nrows, r = rho % prob.nrows;
+    U1Row x;
+    x.fold.src = prob.src + (int64_t)b * prob.src_stride;
+    x.fold.d = prob.rows[r];
+    x.fold.bandvals = prob.bandvals;
+    x.fold.L = prob.L;
+    x.hat = u1hat + (int64_t)b * prob.dst_stride + x.fold.d.dst_off;
+    x.dbg = u1dbg ? u1dbg + (int64_t)b * prob.dst_stride + x.fold.d.dst_off : nullptr;
+    x.umax = prob.u1max ? prob.u1max + (int64_t)b * prob.n1 + x.fold.d.pad : nullptr;
+    rr[threadIdx.x] = x;
+  }
+  __syncthreads();
   auto modulus = [&]() {
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
-      const int rho = min(rho0 + g, nrows - 1);
-      const float sc = prob.rows[rho % prob.nrows].scale;
+      const float sc = rr[g].fold.d.scale;
       const float2 v = smem[g * LS + padx(e)];
       const float u = sqrtf(fmaf(v.x, v.x, v.y * v.y)) * sc;
       smem[g * LS + padx(e)] = make_float2(u, 0.f);
-      if (u1dbg && rho0 + g < nrows) {
-        const int b = (rho0 + g) / prob.nrows, r = (rho0 + g) % prob.nrows;
-        u1dbg[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = u;
-      }
+      if (u1dbg && rho0 + g < nrows) rr[g].dbg[e] = u;
       if (prob.u1max) {  // per-row max |U1|: a warp's 32 elements share one row when L >= 32
-        const int b = rho / prob.nrows, r = rho % prob.nrows;
-        unsigned int* slot = prob.u1max + (int64_t)b * prob.n1 + prob.rows[r].pad;
+        unsigned int* slot = rr[g].umax;
         if constexpr (L >= 32) {
           const unsigned int m = __reduce_max_sync(0xffffffffu, rho0 + g < nrows ? __float_as_uint(u) : 0u);
           if ((threadIdx.x & 31) == 0 && rho0 + g < nrows) atomicMax(slot, m);
@@ -367,17 +386,13 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
     __syncthreads();
   };
   auto st = [&](int g, int e, float2 v) {
-    const int rho = rho0 + g;
-    if (rho < nrows) {
-      const int b = rho / prob.nrows, r = rho % prob.nrows;
-      u1hat[(int64_t)b * prob.dst_stride + prob.rows[r].dst_off + e] = v;
-    }
+    if (rho0 + g < nrows) rr[g].hat[e] = v;
   };
   if constexpr (LOG2L >= 3) {
     // IDFT: first pass straight from the band fold (global), result left in smem;
     // modulus in smem; DFT of U1: last pass straight to U1hat (global)
     auto ld = [&](int g, int e) -> float2 {
-      return (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+      return (rho0 + g < nrows) ? rr[g].fold.load(e) : make_float2(0.f, 0.f);
     };
     auto none = [&](int, int, float2) {};
     fft_fused<LOG2L, G, NT, +1, LS, false, true, false>(smem, Ws, ld, none);
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__(NT) k_u1_fused(ProbFold prob, float2* __restri
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int idx = threadIdx.x + i * NT, g = idx / L, e = idx % L;
-      v[i] = (rho0 + g < nrows) ? prob.load(rho0 + g, e) : make_float2(0.f, 0.f);
+      v[i] = (rho0 + g < nrows) ? rr[g].fold.load(e) : make_float2(0.f, 0.f);
     }
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -1118,7 +1133,7 @@ void launch_u1_fused(const ProbFold& prob, float2* u1hat, float* u1dbg, int nrow
   constexpr int G = rows_G<LOG2L>();
   constexpr int NT = rows_NT<LOG2L>();
   const int grid = (nrows + G - 1) / G;
-  const size_t sm = ((size_t)G * pad_row(1 << LOG2L) + (1 << LOG2L)) * sizeof(float2);
+  const size_t sm = ((size_t)G * pad_row(1 << LOG2L) + (1 << LOG2L)) * sizeof(float2) + (size_t)G * kBoundRowBytes;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_u1_fused<LOG2L, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
