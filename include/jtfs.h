@@ -406,6 +406,12 @@ JTFS_API jtfs_status jtfs_debug_fft(jtfs_plan_t plan, int32_t log2L, int32_t dir
                            const void* in, void* out, int64_t rows, void* tmp, size_t tmp_bytes,
                            void* stream);
 
+/* The KD tiling the plan chose (plan_tc, kernels_tc.cu; host plans too): per active alpha
+ * a, out[10a..10a+9] = { kd_impl (1 tcgen05, 0 SIMT validation), CTA pairs (cta_group::2),
+ * A stationary, Nt, M-parts, M-blocks per part (pairs: per CTA), B buffers, A ring stages,
+ * K-chunks, pooling form (0 taps, 1 cubic moments) }.  cap >= 10 x n_alpha. */
+JTFS_API jtfs_status jtfs_debug_kd_tiling(jtfs_plan_t plan, int32_t* out, int32_t cap);
+
 /* Density of the KD's tensor-core operand A''_alpha (VERDICT r1 "measure A's
  * density"): per active alpha a, { records (128 pair rows x 16 packed
  * K-columns), records holding an entry > thr x its row's largest coefficient, records in

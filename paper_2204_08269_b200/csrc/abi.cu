@@ -1181,6 +1181,19 @@ jtfs_status jtfs_debug_joint(jtfs_plan_t plan, const float* y2, const float* yph
   return e != cudaSuccess ? cuda_fail(e, "kernel launch") : JTFS_OK;
 }
 
+jtfs_status jtfs_debug_kd_tiling(jtfs_plan_t plan, int32_t* out, int32_t cap) {
+  if (!plan || !out || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
+  const auto& P = plan->P;
+  if ((size_t)cap < 10 * P.kd.size()) return fail(JTFS_ERR_INVALID_ARG, "cap < 10 x n_alpha");
+  int32_t* o = out;
+  for (const auto& d : P.kd) {
+    const int32_t v[10] = {P.kd_impl, d.tc_pair, d.tc_stat, d.tc_Nt, d.tc_mpart, d.tc_mblk,
+                           d.tc_NBB, d.tc_S, d.tc_nkc, d.pool_mode};
+    for (int i = 0; i < 10; ++i) *o++ = v[i];
+  }
+  return JTFS_OK;
+}
+
 jtfs_status jtfs_debug_a16_density(jtfs_plan_t plan, double thr, int64_t* out, int32_t cap) {
   if (!plan || !out || cap < 0) return fail(JTFS_ERR_INVALID_ARG, "bad argument");
   std::vector<int64_t> v;

@@ -34,7 +34,7 @@ EXPORTS = [
     "jtfs_plan", "jtfs_plan_create", "jtfs_plan_destroy", "jtfs_layout", "jtfs_paths",
     "jtfs_lambda_xi", "jtfs_workspace_size", "jtfs_forward", "jtfs_forward_host",
     "jtfs_debug_tap", "jtfs_debug_tap_size", "jtfs_debug_filter", "jtfs_debug_joint", "jtfs_debug_fft",
-    "jtfs_debug_a16_density",
+    "jtfs_debug_a16_density", "jtfs_debug_kd_tiling",
     "jtfs_measure_fp32_peak", "jtfs_cost", "jtfs_profile_enable",
     "jtfs_profile_read", "jtfs_profile_read_kd", "jtfs_status_string", "jtfs_last_error",
     "jtfs_units", "jtfs_partials_size", "jtfs_forward_units", "jtfs_reduce_pack",
@@ -90,6 +90,8 @@ _lib.jtfs_debug_tap_size.argtypes = [_P, C.c_int32, C.c_int64, C.POINTER(C.c_int
 _lib.jtfs_debug_joint.argtypes = [_P, _P, _P, C.c_int64, _P, _P, C.c_size_t, _P]
 _lib.jtfs_debug_fft.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_int64, _P, C.c_size_t, _P]
 _lib.jtfs_debug_a16_density.argtypes = [_P, C.c_double, C.POINTER(C.c_int64), C.c_int32]
+_lib.jtfs_debug_kd_tiling.argtypes = [_P, C.POINTER(C.c_int32), C.c_int32]
+KD_TILING_FIELDS = ("kd_impl", "pair", "stat", "Nt", "mpart", "mblk", "NBB", "S", "nkc", "pool_mode")
 _lib.jtfs_measure_fp32_peak.argtypes = [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 _lib.jtfs_debug_filter.argtypes = [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
 _lib.jtfs_cost.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32]
@@ -426,6 +428,13 @@ class Plan:
         _check(_lib.jtfs_debug_joint(self._h, _ptr(y2), _ptr(yphi), B, _ptr(out), _ptr(ws), ws.numel(),
                                      _stream_handle(stream)), "jtfs_debug_joint")
         return out
+
+    def kd_tiling(self):
+        """Per alpha, the KD tiling the plan chose (dict of KD_TILING_FIELDS)."""
+        n = self.layout.n_alpha
+        out = (C.c_int32 * (10 * n))()
+        _check(_lib.jtfs_debug_kd_tiling(self._h, out, 10 * n), "jtfs_debug_kd_tiling")
+        return [dict(zip(KD_TILING_FIELDS, out[10 * i:10 * i + 10])) for i in range(n)]
 
     def a16_density(self, thr: float):
         """Per alpha (records, records with an entry > thr x row max, records in the per-block

@@ -188,3 +188,22 @@ def test_a16_density_bookkeeping(jt):
         assert 0 < live <= band <= tot and 0 < ent <= coef
         assert live1 <= live and band1 <= band and ent1 <= ent
         assert live >= tot // nkc  # at least one live record per M-block
+
+
+def test_kd_tiling_policy(jt):
+    # the plan's KD tiling (jtfs_debug_kd_tiling) follows DESIGN.md §2: alpha 0 of c3 on
+    # single CTAs with A stationary; CTA pairs (cta_group::2) on every other alpha when the
+    # M-blocks split into pairs -- stationary where the A'' stream bounds the ring (10..15
+    # K-chunks), a ring otherwise; JTFS_KD_NOPAIR disables pairs; odd block counts never pair
+    t = hostplan(jt, **CFGS["c3"]).kd_tiling()
+    assert all(a["kd_impl"] == 1 and a["Nt"] == 64 for a in t)
+    assert (t[0]["pair"], t[0]["stat"]) == (0, 1)
+    for a in t[1:]:
+        assert a["pair"] == 1
+        assert a["stat"] == (1 if 10 <= a["nkc"] < 16 else 0), a
+        if a["stat"]:
+            assert a["mblk"] == 1 and a["NBB"] >= 2
+    assert not any(a["pair"] for a in hostplan(jt, **CFGS["c3"], flags=jt.JTFS_KD_NOPAIR).kd_tiling())
+    for name in ("c2", "p42"):  # 5 / 11 M-blocks of 128 pair rows: no pairs
+        assert not any(a["pair"] for a in hostplan(jt, **CFGS[name]).kd_tiling())
+    assert all(a["kd_impl"] == 0 for a in hostplan(jt, **CFGS["c1"], flags=jt.JTFS_KD_SIMT).kd_tiling())
