@@ -845,7 +845,7 @@ jtfs_status jtfs_scattering1d(jtfs_plan_t plan, const float* x, int64_t B, float
       sc.done(jtfs::launch_phi_first(P, w.xhat, w.u1hat, nb, w.yphi, ob, lay.floats_per_signal, lay.off_s0,
                                      lay.off_s1, P.d_u1_off, P.d_k1, P.d_band_L1, st));
     }
-    { StageScope sc(P, 3, st); sc.done(jtfs::launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st)); }
+    { StageScope sc(P, 3, st); sc.done(jtfs::launch_second_order(P, w.u1hat, nb, w.y2, w.tmp, st, true)); }
     {
       StageScope sc(P, 4, st);
       const jtfs::WsLayout L = jtfs::ws_layout(P, mb);

@@ -1482,14 +1482,18 @@ int launch_second_order16(const Plan& P, const float2* u1hat, int nsig, uint16_t
   return n;
 }
 
-int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st) {
+// modulus: store |Y2| (times the row scale) in the real row's place instead of the planar
+// complex row (Scattering1D needs only the modulus: half the bytes written by KC and read by KT)
+int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st,
+                        bool modulus) {
   const float2* W = (const float2*)P.d_twiddle;
   const int ltw = ilog2_exact(P.N_tw);
   int n = 0;
   for (const auto& g : P.y2_groups) {
     n += g.log2L <= 12 ? 1 : 2;
     const int nr = (int)g.rows.size();
-    ProbFold pf{u1hat, P.u1_total, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, nullptr, y2, 2 * P.y2_total};
+    ProbFold pf{u1hat, P.u1_total, g.d_rows, nr, P.d_bandvals, 1 << g.log2L, modulus ? y2 : nullptr,
+                modulus ? nullptr : y2, 2 * P.y2_total};
     dispatch_log2(g.log2L, [&](auto c) {
       constexpr int LG = decltype(c)::value;
       if constexpr (LG <= 12) {
@@ -1505,7 +1509,8 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2,
 // ---------------------------------------------------------------------------------
 // KT: second-order time scattering (Scattering1D):
 // S2_t[alpha][lambda][m] = sum_t g_alpha[(frame0 + m) D - t mod L] |Y2_alpha[lambda](t)|
-// -- the phi_T pooling of |Y2| at the retained frames, no lambda convolution.
+// -- the phi_T pooling of |Y2| at the retained frames, no lambda convolution.  KC stored
+// |Y2| itself (launch_second_order, modulus mode) in the place of each row's real part.
 // The pooling weights come from KD's per-alpha table (plan.cpp): exact taps [L][NF]
 // (one float4 row per column, no index arithmetic), or, where the plan verified it to fp32
 // accuracy, the cubic-moment form [L/32][4][NF] (per 32-column block S_k = sum_j |Y| u_j^k,
@@ -1513,7 +1518,7 @@ int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2,
 // reductions (bit-stable).
 // ---------------------------------------------------------------------------------
 struct KTParams {
-  const float* y2;    // planar Y2 of signal 0 at alpha's offset; signal stride y2_stride floats
+  const float* y2;    // |Y2| rows of signal 0 at alpha's offset (row l at 2 l L); signal stride y2_stride
   const float* wtab;  // alpha's phi_T pooling table (taps or moment coefficients)
   float* out;         // out record of signal 0 at row0's first frame; signal stride fps
   int64_t y2_stride, fps;
@@ -1526,8 +1531,7 @@ template <int NF>
 __global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
   __shared__ float red[8][NF];
   const int b = blockIdx.x / p.K, l = blockIdx.x % p.K;
-  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * l) * p.L;
-  const float* im = re + p.L;
+  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * l) * p.L;  // |Y2| row
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (p.pool_mode == 1) {
     // warp w takes the 32-column blocks w, w + 8, ...; lane j = column j of the block
@@ -1535,8 +1539,7 @@ __global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
     float accm = 0.f;  // lane m < NF: frame m
     for (int blk = warp; blk < p.L / 32; blk += 8) {
       const int t = blk * 32 + lane;
-      const float a = __ldg(re + t), c = __ldg(im + t);
-      const float mag = sqrtf(fmaf(a, a, c * c));
+      const float mag = __ldg(re + t);
       float S[4] = {mag, mag * u, mag * u * u, mag * u * u * u};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -1556,8 +1559,7 @@ __global__ void __launch_bounds__(256) k_time_scat(KTParams p) {
 #pragma unroll
     for (int m = 0; m < NF; ++m) acc[m] = 0.f;
     for (int t = threadIdx.x; t < p.L; t += 256) {
-      const float a = __ldg(re + t), c = __ldg(im + t);
-      const float mag = sqrtf(fmaf(a, a, c * c));
+      const float mag = __ldg(re + t);
       const float4* w4 = reinterpret_cast<const float4*>(p.wtab + (int64_t)t * NF);
 #pragma unroll
       for (int m4 = 0; m4 < NF / 4; ++m4) {
@@ -1605,8 +1607,7 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = grp * 32 + lane;
   const bool active = r < p.K;
-  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * (active ? r : 0)) * p.L;
-  const float* im = re + p.L;
+  const float* re = p.y2 + (int64_t)b * p.y2_stride + (int64_t)(2 * (active ? r : 0)) * p.L;  // |Y2| row
   // this CTA's 32-column blocks: split `split` of nsplit equal ranges
   const int nblk_all = p.L / 32;
   const int per = (nblk_all + p.nsplit - 1) / p.nsplit;
@@ -1629,9 +1630,7 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float4 a = __ldg(reinterpret_cast<const float4*>(re + t0) + q);
-          const float4 c = __ldg(reinterpret_cast<const float4*>(im + t0) + q);
-          const float mg[4] = {sqrtf(fmaf(a.x, a.x, c.x * c.x)), sqrtf(fmaf(a.y, a.y, c.y * c.y)),
-                               sqrtf(fmaf(a.z, a.z, c.z * c.z)), sqrtf(fmaf(a.w, a.w, c.w * c.w))};
+          const float mg[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float u = ((float)(4 * q + e) - 15.5f) * 0.0625f;  // compile-time
@@ -1654,9 +1653,7 @@ __global__ void __launch_bounds__(256) k_time_scat_rows(KTParams p) {
 #pragma unroll 2
         for (int q = 0; q < 8; ++q) {
           const float4 a = __ldg(reinterpret_cast<const float4*>(re + t0) + q);
-          const float4 c = __ldg(reinterpret_cast<const float4*>(im + t0) + q);
-          const float mg[4] = {sqrtf(fmaf(a.x, a.x, c.x * c.x)), sqrtf(fmaf(a.y, a.y, c.y * c.y)),
-                               sqrtf(fmaf(a.z, a.z, c.z * c.z)), sqrtf(fmaf(a.w, a.w, c.w * c.w))};
+          const float mg[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float4* w4 = reinterpret_cast<const float4*>(tb + (4 * q + e) * NF);

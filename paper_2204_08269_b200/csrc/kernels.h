@@ -74,7 +74,8 @@ int launch_y16_from_y2(Plan& P, const float* y2, int nsig, uint16_t* y16, float*
 int launch_phi_first(const Plan& P, const float2* xhat, const float2* u1hat, int nsig, float* yphi, float* out,
                       int64_t fps, int64_t off_s0, int64_t off_s1, const int64_t* d_u1_off, const int* d_k1,
                       const Band* d_band_L1, cudaStream_t st);
-int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st);
+int launch_second_order(const Plan& P, const float2* u1hat, int nsig, float* y2, float2* tmp, cudaStream_t st,
+                        bool modulus = false);
 int launch_kd(const Plan& P, const float* y2, int nsig, float* part, cudaStream_t st, const UnitSel* sel = nullptr);
 size_t ke_smem_bytes(const Plan& P);
 int launch_ke(const Plan& P, const KEParams& kp, int nsig, cudaStream_t st);
