@@ -508,25 +508,40 @@ __device__ __forceinline__ void epi_group_taps(uint32_t tb1, uint32_t tb2, const
   }
 }
 // moments of both spins, packed: S[k] = (sum_j |Z_-,j| u_j^k, sum_j |Z_+,j| u_j^k), u_j
-// compile-time (FFMA2 with an immediate operand).  One group = 16 time columns: two x32
-// TMEM loads (acc1, acc2) behind one wait, so 16 independent columns are in flight.
+// = (j - 15.5) / 16 compile-time (FFMA2 with an immediate operand).  The moments are taken
+// over column pairs (j, 31 - j), where u_{31-j} = -u_j: with s = z_j + z_{31-j} and d = z_j -
+// z_{31-j}, S0 += s, S1 += d u, S2 += s u^2, S3 += d u^3 -- 3 FMA-pipe instructions per
+// column instead of 4 (the epilogue is bound by the FMA pipe: tools/ffma2_forms.cu).  So a
+// group holds both columns of its pairs: group 0 the columns 0..7 and 24..31 of the 32-column
+// block (two x16 TMEM loads per accumulator), group 1 the columns 8..23 (one x32).
 template <int G>
 __device__ __forceinline__ void epi_group_mom(uint32_t tb1, uint32_t tb2, float2 (&S)[4]) {
   uint32_t v1[32], v2[32];
-  tmem_ld32(tb1 + 32 * G, v1);
-  tmem_ld32(tb2 + 32 * G, v2);
+  if constexpr (G == 0) {
+    // accumulator columns 2t, 2t + 1 of time column t: t in [0, 8) -> [0, 16), t in [24, 32) -> [48, 64)
+    tmem_ld16(tb1, *reinterpret_cast<uint32_t(*)[16]>(v1));
+    tmem_ld16(tb1 + 48, *reinterpret_cast<uint32_t(*)[16]>(v1 + 16));
+    tmem_ld16(tb2, *reinterpret_cast<uint32_t(*)[16]>(v2));
+    tmem_ld16(tb2 + 48, *reinterpret_cast<uint32_t(*)[16]>(v2 + 16));
+  } else {
+    tmem_ld32(tb1 + 16, v1);  // t in [8, 24)
+    tmem_ld32(tb2 + 16, v2);
+  }
   tmem_wait_ld();
   reg_fence(v1);
   reg_fence(v2);
-  float2 mz[16];
+  float2 mz[16];  // G 0: columns 0..7, 24..31; G 1: columns 8..23
   spin_mags<16>(v1, v2, mz);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float u = ((float)(16 * G + j) - 15.5f) * 0.0625f;  // compile-time
-    S[0] = add2(S[0], mz[j]);
-    S[1] = fma2(mz[j], make_float2(u, u), S[1]);
-    S[2] = fma2(mz[j], make_float2(u * u, u * u), S[2]);
-    S[3] = fma2(mz[j], make_float2(u * u * u, u * u * u), S[3]);
+  for (int i = 0; i < 8; ++i) {
+    const int c = (G == 0 ? 0 : 8) + i;  // column c pairs with 31 - c = mz[15 - i]
+    const float u = ((float)c - 15.5f) * 0.0625f;  // compile-time
+    const float2 sm = add2(mz[i], mz[15 - i]);
+    const float2 df = fma2(mz[15 - i], make_float2(-1.f, -1.f), mz[i]);
+    S[0] = add2(S[0], sm);
+    S[1] = fma2(df, make_float2(u, u), S[1]);
+    S[2] = fma2(sm, make_float2(u * u, u * u), S[2]);
+    S[3] = fma2(df, make_float2(u * u * u, u * u * u), S[3]);
   }
 }
 
