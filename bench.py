@@ -542,8 +542,8 @@ def run_c3(args, rank, world, local, dev):
                          "executed_flops_per_signal": cost["KD_tensor_executed"][0]},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 4),
                     "d2h_bytes_per_step": int(oh.numel() * 4), "ms_per_step": e2e_tot / args.steps,
-                    "how": "jtfs_forward_host (pinned host in/out; H2D / D2H pipelined per plan micro-batch (128 signals at c3) "
-                           "micro-batch on two copy streams), timed step by step interleaved with the headline "
+                    "how": "jtfs_forward_host (pinned host in/out; H2D / D2H pipelined per plan micro-batch, 128 "
+                           "signals at c3, on two copy streams), timed step by step interleaved with the headline "
                            "steps (same clocks), L2 flushed before each"},
             "path_roofline": _path_roofline(value / max(world, 1), fp32_peak, clocks,
                                             f"measured in this run: FFMA {ffma:.1f}, FFMA2 {ffma2:.1f} TFLOP/s "
